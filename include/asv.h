@@ -1,0 +1,147 @@
+/*
+ * asv.h — C ABI of the B200-native AlignedServe decode-iteration hot path.
+ *
+ * The reference (`/root/reference/proj`, header-only C++20 `prefixsim`) never
+ * executes the decode iteration: it PRICES it.  Each entry point below is the
+ * executed replacement of one priced/modeled function on that path; the C++
+ * API the reference's callers see (namespace `prefixsim`, same headers, same
+ * signatures) is kept verbatim in paper_2605_23389_b200/include/prefixsim/ and
+ * sits on top of this ABI (see INTEGRATION.md for the binding).
+ *
+ * Conventions: plain pointers and sizes, no C++ or torch types; every entry
+ * returns 0 on success or an ASV_ERR_* code; the message of the last failure
+ * on the calling thread is available from asv_last_error().  CUDA streams are
+ * passed as `void*` (cudaStream_t).  The ABI never allocates on the hot path:
+ * device buffers (KV page pool, plan, workspace, outputs) belong to the caller.
+ */
+#ifndef ASV_H_
+#define ASV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* error codes; the C++ wrapper rethrows the reference's exception types */
+#define ASV_OK 0
+#define ASV_ERR_INVALID 1 /* std::invalid_argument (e.g. "empty batch", cost_model.hpp:114) */
+#define ASV_ERR_RUNTIME 2 /* std::runtime_error ("unschedulable: zero-capacity HBM", scheduler.hpp:155) */
+#define ASV_ERR_LOGIC 3   /* std::logic_error (engine invariants, cluster_sim.hpp:641-697) */
+#define ASV_ERR_CUDA 4    /* CUDA runtime failure (no counterpart: the reference has no GPU) */
+
+const char* asv_last_error(void);
+int asv_abi_version(void);
+
+/* ------------------------------------------------------------------------ */
+/* Paged KV layout (device HBM and pinned host pool share it, so KV moves are  */
+/* opaque byte copies of whole pages):                                       */
+/*   page = [num_layers][2 (K,V)][num_kv_heads][page_size=16][head_dim=128]  */
+/* bf16.  Inside each (page, layer, K|V, head) 4 KiB block the 16-byte chunk  */
+/* c of token row t is stored at chunk position c ^ (t & 7) (XOR swizzle), so */
+/* a 1-D bulk TMA of the block lands bank-conflict-free in shared memory for  */
+/* both the FFMA (MHA) and ldmatrix/mma (GQA) consumers.                     */
+/* Page = 16 tokens = ClusterConfig::block_size (cluster_sim.hpp:45);         */
+/* bytes per token over all layers = ModelSpec::kv_bytes_per_token()          */
+/* (cost_model.hpp:34-36) when num_kv_heads*head_dim == hidden_dim.           */
+/* ------------------------------------------------------------------------ */
+typedef struct asv_attn_shape {
+    int32_t num_q_heads;  /* n_h */
+    int32_t num_kv_heads; /* n_kv; n_h % n_kv == 0, group n_h/n_kv <= 8 */
+    int32_t head_dim;     /* must be 128 */
+    int32_t page_size;    /* must be 16 */
+    int32_t num_layers;   /* L (layers resident per page) */
+} asv_attn_shape;
+
+/* bytes of one page (all layers, K and V) */
+int64_t asv_page_bytes(const asv_attn_shape* shape);
+/* byte offset of token row t, dim-chunk c (8 elements) of (layer, kv, head) inside a page */
+int64_t asv_page_offset(const asv_attn_shape* shape, int32_t layer, int32_t kv, int32_t head,
+                        int32_t token, int32_t dim);
+
+/* ------------------------------------------------------------------------ */
+/* Split-KV work plan (host side, K4 in SURVEY §2).  Built once per decode    */
+/* iteration from the batch in `SchedulerState::running` order                */
+/* (scheduler.hpp:59; cluster_sim.hpp:476-478) and uploaded as ONE int32      */
+/* buffer; reused by every layer of that iteration.                          */
+/* ------------------------------------------------------------------------ */
+typedef struct asv_attn_plan {
+    int32_t batch;          /* b */
+    int32_t total_splits;   /* G: sum over requests of their split counts */
+    int32_t num_items;      /* G * num_kv_heads warp work items */
+    int32_t num_pages;      /* P = page_indptr[batch] */
+    int32_t num_workers;    /* persistent warps the plan was balanced for */
+    int32_t off_seq_lens;   /* int32 offsets inside the plan buffer */
+    int32_t off_page_indptr;
+    int32_t off_page_indices;
+    int32_t off_split_indptr;
+    int32_t off_item_tab;   /* int2 {request, split} per global split */
+    int32_t total_int32;    /* size of the plan buffer in int32 */
+    int32_t max_item_pages; /* largest work item, pages */
+} asv_attn_plan;
+
+/* Persistent warp count of the decode-attention kernel on `device` (SMs x resident warps). */
+int asv_attn_num_workers(const asv_attn_shape* shape, int device, int32_t* workers_out);
+
+/* Fill `plan_buf` (host, capacity `plan_cap` int32) for a batch.
+ *   seq_lens[b]        tokens attended per request (= prefix_len, >= 1)
+ *   page_indptr[b+1]   CSR over page_indices; request i owns
+ *                      page_indices[page_indptr[i] .. page_indptr[i+1]) which must cover
+ *                      ceil((seq_lens[i]+1)/16) pages when a KV append is requested
+ *   page_indices[P]    physical page ids in the device pool
+ * The split count per request is chosen so every warp streams a near-equal KV span. */
+int asv_attn_plan_build(const asv_attn_shape* shape, int32_t batch, const int32_t* seq_lens,
+                        const int32_t* page_indptr, const int32_t* page_indices,
+                        int32_t num_workers, int32_t* plan_buf, int64_t plan_cap,
+                        asv_attn_plan* plan_out);
+
+/* Workspace: split partials + per-(request, kv head) semaphores. */
+size_t asv_attn_workspace_bytes(const asv_attn_shape* shape, int32_t max_batch,
+                                int32_t max_total_splits);
+int asv_attn_workspace_init(void* workspace, size_t bytes, void* stream);
+
+typedef struct asv_attn_args {
+    const void* q;          /* [b][n_h][128] bf16, this layer */
+    void* kv_pool;          /* device page pool base (layout above) */
+    int64_t pool_pages;     /* pages in the pool (bounds checking on the plan) */
+    int32_t layer;          /* layer slice of every page to attend over */
+    const int32_t* plan_dev;/* device copy of the plan buffer */
+    const asv_attn_plan* plan;
+    const void* k_new;      /* [b][n_kv][128] bf16 appended at position seq_len (nullable) */
+    const void* v_new;      /* [b][n_kv][128] bf16 (nullable together with k_new) */
+    void* out;              /* [b][n_h][128] bf16 */
+    float* lse;             /* [b][n_h] natural-log sum-exp (nullable) */
+    void* workspace;
+    size_t workspace_bytes;
+    float sm_scale;         /* 1/sqrt(128) for the paper's Eq. 2 */
+} asv_attn_args;
+
+/* K1+K2+K3: paged split-KV decode attention, in-kernel split merge (last-arriving
+ * warp per (request, kv head)), fused KV append.  Replaces the attention term of
+ * iteration_latency (cost_model.hpp:112-135). */
+int asv_decode_attention(const asv_attn_shape* shape, const asv_attn_args* args, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Host-side decision path (reference API underneath, C ABI on top).          */
+/* ------------------------------------------------------------------------ */
+
+/* Run one experiment config (reference JSON format, proj/configs/<name>.json,
+ * io.hpp:184-254) through the B200-native engine in VIRTUAL-CLOCK mode (the
+ * reference cost model advances time, so decisions are bit-exact) and return
+ * the schema-1 JSONL log (io.hpp:279-323).  `*out` is malloc'ed; free it with
+ * asv_free().  `policy_override` may be NULL. */
+int asv_run_config_jsonl(const char* config_json, const char* policy_override, char** out,
+                         int64_t* out_len);
+void asv_free(void* p);
+
+/* Density-first search on a pool snapshot (batch_gen.hpp:126-210).
+ * residents: n x {id, prefix_len, kv_blocks} in insertion order (all inserted at t=0).
+ * Writes the batch member ids in page-table order; returns count via *n_out (0 = no batch). */
+int asv_dfs_batch(const int64_t* residents, int64_t n, int64_t b_max, int64_t k_min,
+                  int64_t* ids_out, int64_t* n_out, int64_t* total_blocks_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ASV_H_ */

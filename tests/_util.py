@@ -1,0 +1,145 @@
+"""Test helpers: deterministic inputs, the oracle loaders (TEST INFRASTRUCTURE).
+
+Inputs follow SURVEY §8(d): splitmix64 (reference prng.hpp:10-55) -> U[-1, 1)
+-> round-to-nearest-even bf16.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ORACLE_SO = os.path.join(ROOT, "oracle", "libasv_oracle.so")
+REF_SO = os.path.join(ROOT, "oracle", "_ref", "libprefixsim_ref.so")
+
+GOLDEN = 0x9E3779B97F4A7C15
+M1 = 0xBF58476D1CE4E5B9
+M2 = 0x94D049BB133111EB
+
+
+def splitmix64(seed: int, n: int) -> np.ndarray:
+    """The n outputs of prefixsim::Rng(seed).next_u64() (prng.hpp:14-19), vectorised."""
+    with np.errstate(over="ignore"):
+        idx = np.arange(1, n + 1, dtype=np.uint64)
+        z = np.uint64(seed) + idx * np.uint64(GOLDEN)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(M1)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(M2)
+        return z ^ (z >> np.uint64(31))
+
+
+def uniform_pm1(seed: int, n: int) -> np.ndarray:
+    u = (splitmix64(seed, n) >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+    return (2.0 * u - 1.0).astype(np.float32)
+
+
+def f32_to_bf16_bits(x: np.ndarray) -> np.ndarray:
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
+    r = ((u >> np.uint32(16)) & np.uint32(1)) + np.uint32(0x7FFF)
+    return ((u + r) >> np.uint32(16)).astype(np.uint16)
+
+
+def bf16_bits_to_f32(b: np.ndarray) -> np.ndarray:
+    return (b.astype(np.uint32) << np.uint32(16)).view(np.float32)
+
+
+def random_bf16(seed: int, n: int) -> np.ndarray:
+    return f32_to_bf16_bits(uniform_pm1(seed, n))
+
+
+def swz_off(t: int, d: int) -> int:
+    c = d // 8
+    return t * 256 + ((c ^ (t & 7)) << 4) + (d % 8) * 2
+
+
+def page_bytes(n_kv: int, num_layers: int) -> int:
+    return num_layers * 2 * n_kv * 4096
+
+
+def block_view(pool: np.ndarray, n_kv: int, num_layers: int) -> np.ndarray:
+    """uint8 pool -> [pages][layers][2][n_kv][4096] byte view."""
+    return pool.reshape(-1, num_layers, 2, n_kv, 4096)
+
+
+def unswizzle_block(block: np.ndarray) -> np.ndarray:
+    """4096-byte (16x128 bf16) swizzled block -> [16][128] uint16 row-major."""
+    out = np.empty((16, 128), dtype=np.uint16)
+    b16 = block.view(np.uint16)
+    for t in range(16):
+        for c in range(16):
+            pc = c ^ (t & 7)
+            out[t, c * 8:(c + 1) * 8] = b16[(t * 256 + pc * 16) // 2:(t * 256 + pc * 16) // 2 + 8]
+    return out
+
+
+def make_batch(seq_lens, pool_pages: int, seed: int, append: bool = True):
+    """CSR page table over a random permutation of pool pages."""
+    rng = np.random.default_rng(seed)
+    perm = rng.permutation(pool_pages).astype(np.int32)
+    indptr = [0]
+    indices = []
+    pos = 0
+    for s in seq_lens:
+        n = (s + (1 if append else 0) + 15) // 16
+        indices.extend(perm[pos:pos + n])
+        pos += n
+        indptr.append(len(indices))
+    assert pos <= pool_pages, "pool too small for the batch"
+    return np.asarray(indptr, np.int32), np.asarray(indices, np.int32)
+
+
+class Oracle:
+    """fp32 CPU attention oracle (oracle/attn_oracle.c) — checker only."""
+
+    def __init__(self):
+        if not os.path.exists(ORACLE_SO):
+            raise RuntimeError("oracle/libasv_oracle.so missing: run __graft_entry__.build()")
+        self.h = C.CDLL(ORACLE_SO)
+        f = self.h.asv_oracle_decode_attention
+        f.restype = C.c_int
+        f.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int64,
+                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_float, C.c_void_p,
+                      C.c_void_p, C.c_int]
+
+    def attention(self, n_q, n_kv, num_layers, layer, q_bits, pool, seq_lens, indptr, indices,
+                  sm_scale, threads=None):
+        b = len(seq_lens)
+        q_bits = np.ascontiguousarray(q_bits, dtype=np.uint16)
+        pool = np.ascontiguousarray(pool, dtype=np.uint8)
+        seq = np.ascontiguousarray(seq_lens, dtype=np.int32)
+        indptr = np.ascontiguousarray(indptr, dtype=np.int32)
+        indices = np.ascontiguousarray(indices, dtype=np.int32)
+        out = np.zeros((b, n_q, 128), dtype=np.float32)
+        lse = np.zeros((b, n_q), dtype=np.float32)
+        rc = self.h.asv_oracle_decode_attention(
+            n_q, n_kv, num_layers, layer, q_bits.ctypes.data, pool.ctypes.data,
+            page_bytes(n_kv, num_layers), seq.ctypes.data, indptr.ctypes.data, indices.ctypes.data,
+            b, float(sm_scale), out.ctypes.data, lse.ctypes.data, threads or os.cpu_count() or 1)
+        assert rc == 0
+        return out, lse
+
+
+def numpy_attention(n_q, n_kv, num_layers, layer, q_bits, pool, seq_lens, indptr, indices, sm_scale):
+    """Independent pure-numpy restatement of PAPER Eq. 2 over the paged layout (small cases)."""
+    blocks = block_view(pool, n_kv, num_layers)
+    g = n_q // n_kv
+    q = bf16_bits_to_f32(np.asarray(q_bits, np.uint16)).astype(np.float64)
+    b = len(seq_lens)
+    out = np.zeros((b, n_q, 128))
+    lse = np.zeros((b, n_q))
+    for r in range(b):
+        s = int(seq_lens[r])
+        pages = indices[indptr[r]:indptr[r + 1]]
+        for kvh in range(n_kv):
+            K = np.concatenate([unswizzle_block(blocks[p, layer, 0, kvh]) for p in pages[:(s + 15) // 16]])[:s]
+            V = np.concatenate([unswizzle_block(blocks[p, layer, 1, kvh]) for p in pages[:(s + 15) // 16]])[:s]
+            K = bf16_bits_to_f32(K).astype(np.float64)
+            V = bf16_bits_to_f32(V).astype(np.float64)
+            for h in range(kvh * g, (kvh + 1) * g):
+                sc = K @ q[r, h] * sm_scale
+                m = sc.max()
+                p = np.exp(sc - m)
+                out[r, h] = p @ V / p.sum()
+                lse[r, h] = m + np.log(p.sum())
+    return out, lse

@@ -1,0 +1,153 @@
+"""Parity of the sm_100a decode-attention kernel (K1+K2+K3) against the fp32 CPU oracle.
+
+Tolerance (bf16 KV, bf16 output; P rounded to bf16 before PV as in FA2/FA3):
+    |gpu - oracle| <= ATOL + RTOL * |oracle| elementwise, and rel-L2 <= RL2,
+with ATOL = 4e-3, RTOL = 8e-3, RL2 = 5e-3; lse within 2e-3 absolute.
+The measured max-abs / rel-L2 are printed so runs record the achieved error.
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import _util as U  # noqa: E402
+
+ATOL, RTOL, RL2, LSE_ATOL = 4e-3, 8e-3, 5e-3, 2e-3
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def oracle():
+    return U.Oracle()
+
+
+def _run_case(oracle, n_q, n_kv, L, layer, seq_lens, seed=1, num_workers=None, append=True,
+              poison_tail=False, const_v=None, repeat=1):
+    from paper_2605_23389_b200 import PagedDecodeAttention
+
+    dev = torch.device("cuda", 0)
+    att = PagedDecodeAttention(n_q, n_kv, L, device=0)
+    pb = att.page_bytes
+    need = sum((s + 16) // 16 for s in seq_lens)
+    pool_pages = need + 7
+    pool = U.random_bf16(seed, pool_pages * pb // 2).view(np.uint8).copy()
+    indptr, indices = U.make_batch(seq_lens, pool_pages, seed + 1, append=True)
+    blocks = U.block_view(pool, n_kv, L)
+    if const_v is not None:
+        # every element of every V block equal: the swizzle is irrelevant
+        cv = U.f32_to_bf16_bits(np.array([const_v], np.float32))[0]
+        blocks[:, :, 1] = np.full(2048, cv, np.uint16).view(np.uint8)
+    if poison_tail:
+        # rows >= seq_len in each last page hold NaN bit patterns; the kernel must ignore them
+        nan_row = np.full(128, 0x7FC1, np.uint16)
+        for r, s in enumerate(seq_lens):
+            last = indices[indptr[r] + (s - 1) // 16]
+            for t in range(s % 16 or 16, 16):
+                for kv in range(2):
+                    for h in range(n_kv):
+                        for d in range(128):
+                            off = U.swz_off(t, d)
+                            blocks[last, layer, kv, h].view(np.uint16)[off // 2] = nan_row[d]
+    b = len(seq_lens)
+    q_bits = U.random_bf16(seed + 2, b * n_q * 128).reshape(b, n_q, 128)
+    kn_bits = U.random_bf16(seed + 3, b * n_kv * 128).reshape(b, n_kv, 128)
+    vn_bits = U.random_bf16(seed + 4, b * n_kv * 128).reshape(b, n_kv, 128)
+
+    ref_out, ref_lse = oracle.attention(n_q, n_kv, L, layer, q_bits, pool, seq_lens, indptr, indices,
+                                        att.sm_scale)
+
+    pool_d = torch.from_numpy(pool).to(dev)
+    q_d = torch.from_numpy(q_bits.view(np.int16)).to(dev).view(torch.bfloat16)
+    kn_d = torch.from_numpy(kn_bits.view(np.int16)).to(dev).view(torch.bfloat16) if append else None
+    vn_d = torch.from_numpy(vn_bits.view(np.int16)).to(dev).view(torch.bfloat16) if append else None
+    out_d = torch.empty(b, n_q, 128, dtype=torch.bfloat16, device=dev)
+    lse_d = torch.empty(b, n_q, dtype=torch.float32, device=dev)
+    plan = att.plan(seq_lens, indptr, indices, num_workers=num_workers)
+    for _ in range(repeat):
+        att.run(q_d, pool_d, layer, plan, out_d, lse_d, kn_d, vn_d)
+    torch.cuda.synchronize()
+    got = out_d.float().cpu().numpy()
+    got_lse = lse_d.cpu().numpy()
+
+    err = np.abs(got - ref_out)
+    rel_l2 = float(np.linalg.norm(got - ref_out) / max(np.linalg.norm(ref_out), 1e-30))
+    print(f"n_q={n_q} n_kv={n_kv} b={b} splits={plan.total_splits} max_abs={err.max():.3e} "
+          f"rel_l2={rel_l2:.3e} lse_max_abs={np.abs(got_lse - ref_lse).max():.3e}")
+    assert np.isfinite(got).all()
+    assert (err <= ATOL + RTOL * np.abs(ref_out)).all(), f"max abs err {err.max()}"
+    assert rel_l2 <= RL2
+    assert np.abs(got_lse - ref_lse).max() <= LSE_ATOL
+
+    if append:
+        # fused KV append (K3): token row seq_len of (layer, kv head) holds k_new / v_new
+        pool_after = pool_d.cpu().numpy()
+        ba = U.block_view(pool_after, n_kv, L)
+        for r, s in enumerate(seq_lens):
+            page = indices[indptr[r] + s // 16]
+            t = s % 16
+            for h in range(n_kv):
+                krow = U.unswizzle_block(ba[page, layer, 0, h])[t]
+                vrow = U.unswizzle_block(ba[page, layer, 1, h])[t]
+                assert (krow == kn_bits[r, h]).all()
+                assert (vrow == vn_bits[r, h]).all()
+    return got, ref_out, plan
+
+
+def test_mha_config1_shape(oracle):
+    """C1: Llama-2-7B attention (32 heads, d=128), batch 16, KV lengths 256-2048."""
+    rng = np.random.default_rng(7)
+    seq = rng.integers(256, 2049, size=16).tolist()
+    _run_case(oracle, 32, 32, 2, 1, seq)
+
+
+def test_mha_edge_lengths(oracle):
+    seq = [1, 2, 15, 16, 17, 31, 32, 33, 255, 256, 257]
+    _run_case(oracle, 32, 32, 1, 0, seq, seed=11)
+
+
+def test_mha_long_request_many_splits(oracle):
+    _run_case(oracle, 32, 32, 1, 0, [40000, 3], seed=5)
+
+
+def test_mha_few_workers_cross_item_pipeline(oracle):
+    # 4 warps total: every warp walks many items, exercising the cross-item ring
+    rng = np.random.default_rng(3)
+    seq = rng.integers(1, 900, size=9).tolist()
+    _run_case(oracle, 32, 32, 2, 0, seq, seed=21, num_workers=4)
+
+
+def test_mha_poisoned_tail_rows(oracle):
+    _run_case(oracle, 32, 32, 1, 0, [5, 21, 100], seed=31, poison_tail=True, append=False)
+
+
+def test_constant_v_known_answer(oracle):
+    got, ref, _ = _run_case(oracle, 32, 32, 1, 0, [1, 7, 300], seed=41, const_v=0.375, append=False)
+    assert np.all(got == np.float32(0.375))
+
+
+def test_repeat_launch_rearms_semaphores(oracle):
+    _run_case(oracle, 32, 32, 1, 0, [3000, 2500, 10], seed=51, repeat=3, append=False)
+
+
+@pytest.mark.parametrize("n_q,n_kv", [(32, 8), (40, 8), (64, 8), (16, 8)])
+def test_gqa_groups(oracle, n_q, n_kv):
+    rng = np.random.default_rng(n_q)
+    seq = rng.integers(1, 3000, size=12).tolist() + [16, 17]
+    _run_case(oracle, n_q, n_kv, 2, 1, seq, seed=61 + n_q)
+
+
+def test_gqa_poisoned_tail_and_long(oracle):
+    _run_case(oracle, 40, 8, 1, 0, [5, 23, 20000], seed=71, poison_tail=True, append=False)
+
+
+def test_empty_batch_raises():
+    from paper_2605_23389_b200 import PagedDecodeAttention
+
+    att = PagedDecodeAttention(32, 32, 1, device=0)
+    with pytest.raises(ValueError, match="empty batch"):
+        att.plan([], [0], [])
+    with pytest.raises(ValueError, match="prefix lengths must be >= 1"):
+        att.plan([0], [0, 1], [0])
