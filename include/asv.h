@@ -72,13 +72,11 @@ typedef struct asv_attn_plan {
     int32_t num_items;      /* G * num_kv_heads warp work items */
     int32_t num_pages;      /* P = page_indptr[batch] */
     int32_t num_workers;    /* persistent warps the plan was balanced for */
-    int32_t off_seq_lens;   /* int32 offsets inside the plan buffer */
-    int32_t off_page_indptr;
-    int32_t off_page_indices;
-    int32_t off_split_indptr;
-    int32_t off_item_tab;   /* int2 {request, split} per global split */
+    int32_t off_desc;       /* int32 offset of the G split descriptors (40 words each,
+                               sorted longest first: the dynamic schedule is LPT) */
+    int32_t off_split_base; /* int32 offset of split_base[b+1] (partial slots per request) */
     int32_t total_int32;    /* size of the plan buffer in int32 */
-    int32_t max_item_pages; /* largest work item, pages */
+    int32_t max_item_pages; /* largest work item, pages (<= 32) */
 } asv_attn_plan;
 
 /* Persistent warp count of the decode-attention kernel on `device` (SMs x resident warps). */
@@ -115,6 +113,8 @@ typedef struct asv_attn_args {
     void* workspace;
     size_t workspace_bytes;
     float sm_scale;         /* 1/sqrt(128) for the paper's Eq. 2 */
+    uint32_t launch_index;  /* consecutive launches on one workspace must alternate parity */
+    int32_t pdl;            /* 1: programmatic dependent launch (overlap with the previous kernel) */
 } asv_attn_args;
 
 /* K1+K2+K3: paged split-KV decode attention, in-kernel split merge (last-arriving

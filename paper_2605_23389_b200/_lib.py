@@ -31,11 +31,8 @@ class AttnPlan(C.Structure):
         ("num_items", C.c_int32),
         ("num_pages", C.c_int32),
         ("num_workers", C.c_int32),
-        ("off_seq_lens", C.c_int32),
-        ("off_page_indptr", C.c_int32),
-        ("off_page_indices", C.c_int32),
-        ("off_split_indptr", C.c_int32),
-        ("off_item_tab", C.c_int32),
+        ("off_desc", C.c_int32),
+        ("off_split_base", C.c_int32),
         ("total_int32", C.c_int32),
         ("max_item_pages", C.c_int32),
     ]
@@ -56,6 +53,8 @@ class AttnArgs(C.Structure):
         ("workspace", C.c_void_p),
         ("workspace_bytes", C.c_size_t),
         ("sm_scale", C.c_float),
+        ("launch_index", C.c_uint32),
+        ("pdl", C.c_int32),
     ]
 
 

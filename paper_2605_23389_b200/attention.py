@@ -76,6 +76,8 @@ class PagedDecodeAttention:
         self.page_bytes = int(self.lib.asv_page_bytes(C.byref(self.shape)))
         self._ws = None
         self._ws_splits = 0
+        self._launches = 0
+        self.pdl = True
 
     # ------------------------------------------------------------------ plan
     def plan(self, seq_lens, page_indptr, page_indices, num_workers: int | None = None,
@@ -87,7 +89,8 @@ class PagedDecodeAttention:
         if b == 0:
             raise ValueError("empty batch")
         nw = int(num_workers) if num_workers is not None else self.num_workers
-        cap = 4 * b + 10 + int(indices.shape[0]) + 2 * (b + 16 * (self.num_workers + 1))
+        npages = int(((seq + 15) // 16).sum())
+        cap = 40 * (npages // 2 + b + 1) + b + 8  # every split holds >= 2 pages or a whole request
         host = torch.empty(cap, dtype=torch.int32, pin_memory=True)
         desc = _lib.AttnPlan()
         hp = C.cast(C.c_void_p(host.data_ptr()), C.POINTER(C.c_int32))
@@ -137,6 +140,9 @@ class PagedDecodeAttention:
         args.workspace = self._ws.data_ptr()
         args.workspace_bytes = self._ws.numel()
         args.sm_scale = self.sm_scale
+        args.launch_index = self._launches & 0xFFFFFFFF
+        args.pdl = 1 if self.pdl else 0
+        self._launches += 1
         with torch.cuda.device(self.device):
             _lib.check(self.lib.asv_decode_attention(C.byref(self.shape), C.byref(args),
                                                       C.c_void_p(_stream_ptr(stream))))

@@ -9,20 +9,23 @@
 
 namespace asv {
 
+// Words per split descriptor in the plan buffer (decode_attn.cu Desc):
+// [r, slot, page_begin, page_end, seq_len, nsplit, append_phys, 0] + 32 page ids.
+constexpr int kDescWords = 40;
+constexpr int kMaxItemPages = 32;
+
 // Launch description for the decode-attention kernel (decode_attn.cu).
 struct AttnLaunch {
     int group;              // n_q / n_kv
     int grid;               // persistent CTAs
+    bool pdl;               // programmatic dependent launch
     const void* q;
     void* pool;
     int64_t page_bytes;
     int64_t layer_off;
     int64_t v_off;
-    const int32_t* seq_lens;
-    const int32_t* page_indptr;
-    const int32_t* page_indices;
-    const int32_t* split_indptr;
-    const int32_t* item_tab;  // int2 pairs
+    const int32_t* gdesc;
+    const int32_t* split_base;
     int32_t num_items;
     int32_t n_kv;
     int32_t n_q;
@@ -33,6 +36,7 @@ struct AttnLaunch {
     float* part_o;
     float* part_ml;           // float2 pairs
     int32_t* sem;
+    uint32_t* work;           // 2 counters of this launch parity
     float sm_scale;
 };
 

@@ -18,6 +18,8 @@ namespace asv {
 namespace {
 thread_local std::string g_last_error;
 constexpr int64_t kSemBytes = 256 * 1024;  // 65536 (request, kv head) semaphores
+constexpr int64_t kWorkBytes = 256;        // per-parity dynamic-schedule counters
+constexpr int64_t kHeadBytes = kSemBytes + kWorkBytes;
 constexpr int64_t kBlockBytes = 16 * 128 * 2;
 
 int group_of(const asv_attn_shape* s) { return s->num_q_heads / s->num_kv_heads; }
@@ -34,28 +36,6 @@ int check_shape(const asv_attn_shape* s) {
     if (g != 1 && g != 2 && g != 4 && g != 5 && g != 8)
         return fail(ASV_ERR_INVALID, "query group size must be one of 1, 2, 4, 5, 8");
     return ASV_OK;
-}
-
-// Simulated makespan (page units) of the static round-robin item schedule.
-double makespan(const std::vector<int32_t>& npages, const std::vector<int32_t>& ns, int n_kv,
-                int workers, double overhead, std::vector<double>& load) {
-    load.assign(static_cast<size_t>(workers), 0.0);
-    int64_t k = 0;
-    double worst = 0.0;
-    for (size_t r = 0; r < npages.size(); ++r) {
-        const int n = npages[r];
-        const int chunk = (n + ns[r] - 1) / ns[r];
-        for (int s = 0; s < ns[r]; ++s) {
-            const int pages = std::min(n, (s + 1) * chunk) - s * chunk;
-            const double cost = pages + overhead + (ns[r] > 1 ? 0.25 : 0.0);
-            for (int h = 0; h < n_kv; ++h, ++k) {
-                double& w = load[static_cast<size_t>(k % workers)];
-                w += cost;
-                worst = std::max(worst, w);
-            }
-        }
-    }
-    return worst;
 }
 
 // Split count so that ceil(n / ceil(n / ns)) == ns: every split non-empty.
@@ -157,35 +137,39 @@ int asv_attn_plan_build(const asv_attn_shape* shape, int32_t batch, const int32_
     }
     if (page_indptr[0] != 0) return fail(ASV_ERR_INVALID, "page_indptr[0] must be 0");
 
-    // choose per-request split counts: candidates at 1..8 waves of items plus "no split"
-    const double overhead = 1.5;  // per item: q load, state reset, epilogue (page units)
+    // Split size (pages per warp item, <= 32): items are pulled dynamically in
+    // longest-first order, so the makespan is ~ total/W plus about half an item
+    // of tail; each item also pays a fixed cost (q load, epilogue) and each
+    // split request a merge.
+    const double item_overhead = 1.5, merge_cost = 0.5;
     std::vector<int32_t> best_ns(static_cast<size_t>(batch), 1), ns(static_cast<size_t>(batch));
-    std::vector<double> load;
-    double best = makespan(npages, best_ns, n_kv, num_workers, overhead, load);
-    int64_t best_items = static_cast<int64_t>(batch) * n_kv;
-    for (int waves = 1; waves <= 8; ++waves) {
-        const double target_items = static_cast<double>(waves) * num_workers;
-        const double chunk = std::max(2.0, std::ceil(static_cast<double>(total_pages) * n_kv / target_items));
-        int64_t items = 0;
+    double best = -1.0;
+    static const int kChunks[] = {2, 3, 4, 6, 8, 10, 12, 16, 20, 24, 28, 32};
+    for (const int c : kChunks) {
+        double total = 0.0;
+        int max_item = 0;
         for (int r = 0; r < batch; ++r) {
             const int n = npages[static_cast<size_t>(r)];
-            ns[static_cast<size_t>(r)] = normalize_splits(n, static_cast<int>(std::ceil(n / chunk)));
-            items += static_cast<int64_t>(ns[static_cast<size_t>(r)]) * n_kv;
+            const int k = normalize_splits(n, (n + c - 1) / c);
+            ns[static_cast<size_t>(r)] = k;
+            const int chunk = (n + k - 1) / k;
+            max_item = std::max(max_item, chunk);
+            total += static_cast<double>(n_kv) * (n + k * item_overhead + (k > 1 ? merge_cost : 0.0));
         }
-        const double ms = makespan(npages, ns, n_kv, num_workers, overhead, load);
-        if (ms < best - 1e-9 || (std::fabs(ms - best) <= 1e-9 && items < best_items)) {
-            best = ms;
+        if (max_item > kMaxItemPages) continue;
+        const double est = total / num_workers + 0.5 * (max_item + item_overhead);
+        if (best < 0 || est < best - 1e-9) {
+            best = est;
             best_ns = ns;
-            best_items = items;
         }
     }
 
     int64_t total_splits = 0;
     for (int32_t v : best_ns) total_splits += v;
     const int64_t P = page_indptr[batch];
-    // item_tab holds int2 pairs: keep it 8-byte aligned inside the int32 buffer
-    const int64_t off_tab = (batch + (batch + 1) + P + (batch + 1) + 1) & ~int64_t{1};
-    const int64_t need = off_tab + 2 * total_splits;
+    const int64_t off_desc = 0;
+    const int64_t off_split = off_desc + total_splits * kDescWords;
+    const int64_t need = off_split + batch + 1;
     if (need > plan_cap) return fail(ASV_ERR_INVALID, "plan buffer too small: need " + std::to_string(need));
 
     asv_attn_plan pl{};
@@ -194,31 +178,47 @@ int asv_attn_plan_build(const asv_attn_shape* shape, int32_t batch, const int32_
     pl.num_items = static_cast<int32_t>(total_splits * n_kv);
     pl.num_pages = static_cast<int32_t>(P);
     pl.num_workers = num_workers;
-    pl.off_seq_lens = 0;
-    pl.off_page_indptr = batch;
-    pl.off_page_indices = pl.off_page_indptr + batch + 1;
-    pl.off_split_indptr = static_cast<int32_t>(pl.off_page_indices + P);
-    pl.off_item_tab = static_cast<int32_t>(off_tab);
+    pl.off_desc = static_cast<int32_t>(off_desc);
+    pl.off_split_base = static_cast<int32_t>(off_split);
     pl.total_int32 = static_cast<int32_t>(need);
     pl.max_item_pages = 0;
 
-    std::memcpy(plan_buf + pl.off_seq_lens, seq_lens, sizeof(int32_t) * batch);
-    std::memcpy(plan_buf + pl.off_page_indptr, page_indptr, sizeof(int32_t) * (batch + 1));
-    std::memcpy(plan_buf + pl.off_page_indices, page_indices, sizeof(int32_t) * P);
-    int32_t* sp = plan_buf + pl.off_split_indptr;
-    int32_t* tab = plan_buf + pl.off_item_tab;
-    sp[0] = 0;
-    int64_t g = 0;
+    // split_base: partial slots are request-major (the merge walks them)
+    int32_t* sb = plan_buf + off_split;
+    sb[0] = 0;
+    for (int r = 0; r < batch; ++r) sb[r + 1] = sb[r] + best_ns[static_cast<size_t>(r)];
+    // descriptors, counting-sorted by item size descending (stable: request, split)
+    std::vector<int32_t> bucket(kMaxItemPages + 2, 0);
     for (int r = 0; r < batch; ++r) {
-        const int n = npages[static_cast<size_t>(r)];
-        const int k = best_ns[static_cast<size_t>(r)];
+        const int n = npages[static_cast<size_t>(r)], k = best_ns[static_cast<size_t>(r)];
         const int chunk = (n + k - 1) / k;
-        pl.max_item_pages = std::max(pl.max_item_pages, chunk);
-        for (int s = 0; s < k; ++s, ++g) {
-            tab[2 * g] = r;
-            tab[2 * g + 1] = s;
+        for (int s = 0; s < k; ++s) bucket[static_cast<size_t>(std::min(n, (s + 1) * chunk) - s * chunk)]++;
+    }
+    std::vector<int64_t> pos(kMaxItemPages + 2, 0);
+    for (int sz = kMaxItemPages, acc = 0; sz >= 1; --sz) {
+        pos[static_cast<size_t>(sz)] = acc;
+        acc += bucket[static_cast<size_t>(sz)];
+    }
+    for (int r = 0; r < batch; ++r) {
+        const int n = npages[static_cast<size_t>(r)], k = best_ns[static_cast<size_t>(r)];
+        const int chunk = (n + k - 1) / k;
+        const int32_t* pages = page_indices + page_indptr[r];
+        const int32_t owned = page_indptr[r + 1] - page_indptr[r];
+        const int app = seq_lens[r] / 16;
+        for (int s = 0; s < k; ++s) {
+            const int pb = s * chunk, pe = std::min(n, pb + chunk);
+            int32_t* d = plan_buf + off_desc + pos[static_cast<size_t>(pe - pb)]++ * kDescWords;
+            d[0] = r;
+            d[1] = sb[r] + s;
+            d[2] = pb;
+            d[3] = pe;
+            d[4] = seq_lens[r];
+            d[5] = k;
+            d[6] = (s == k - 1 && app < owned) ? pages[app] : -1;
+            d[7] = 0;
+            for (int j = 0; j < kMaxItemPages; ++j) d[8 + j] = (pb + j < pe) ? pages[pb + j] : 0;
+            pl.max_item_pages = std::max(pl.max_item_pages, pe - pb);
         }
-        sp[r + 1] = static_cast<int32_t>(g);
     }
     *plan_out = pl;
     return ASV_OK;
@@ -228,13 +228,13 @@ size_t asv_attn_workspace_bytes(const asv_attn_shape* shape, int32_t max_batch, 
     if (check_shape(shape) != ASV_OK) return 0;
     (void)max_batch;
     const int64_t per = static_cast<int64_t>(shape->num_q_heads) * (128 * 4 + 8);
-    return static_cast<size_t>(kSemBytes + per * std::max<int64_t>(1, max_total_splits));
+    return static_cast<size_t>(kHeadBytes + per * std::max<int64_t>(1, max_total_splits));
 }
 
 int asv_attn_workspace_init(void* workspace, size_t bytes, void* stream) {
-    if (workspace == nullptr || bytes < static_cast<size_t>(kSemBytes))
+    if (workspace == nullptr || bytes < static_cast<size_t>(kHeadBytes))
         return fail(ASV_ERR_INVALID, "workspace too small");
-    cudaError_t e = cudaMemsetAsync(workspace, 0, kSemBytes, static_cast<cudaStream_t>(stream));
+    cudaError_t e = cudaMemsetAsync(workspace, 0, kHeadBytes, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(workspace)");
     return ASV_OK;
 }
@@ -253,7 +253,7 @@ int asv_decode_attention(const asv_attn_shape* shape, const asv_attn_args* a, vo
     const int n_kv = shape->num_kv_heads, n_q = shape->num_q_heads;
     if (static_cast<int64_t>(pl.batch) * n_kv * 4 > kSemBytes)
         return fail(ASV_ERR_INVALID, "batch * num_kv_heads exceeds the semaphore capacity");
-    const int64_t need = kSemBytes + static_cast<int64_t>(pl.total_splits) * n_q * (128 * 4 + 8);
+    const int64_t need = kHeadBytes + static_cast<int64_t>(pl.total_splits) * n_q * (128 * 4 + 8);
     if (a->workspace == nullptr || static_cast<int64_t>(a->workspace_bytes) < need)
         return fail(ASV_ERR_INVALID, "workspace too small for plan: need " + std::to_string(need));
     const int nw = attn_warps_per_cta();
@@ -268,11 +268,9 @@ int asv_decode_attention(const asv_attn_shape* shape, const asv_attn_args* a, vo
     L.page_bytes = static_cast<int64_t>(shape->num_layers) * 2 * n_kv * kBlockBytes;
     L.layer_off = static_cast<int64_t>(a->layer) * 2 * n_kv * kBlockBytes;
     L.v_off = static_cast<int64_t>(n_kv) * kBlockBytes;
-    L.seq_lens = a->plan_dev + pl.off_seq_lens;
-    L.page_indptr = a->plan_dev + pl.off_page_indptr;
-    L.page_indices = a->plan_dev + pl.off_page_indices;
-    L.split_indptr = a->plan_dev + pl.off_split_indptr;
-    L.item_tab = a->plan_dev + pl.off_item_tab;
+    L.gdesc = a->plan_dev + pl.off_desc;
+    L.split_base = a->plan_dev + pl.off_split_base;
+    L.pdl = a->pdl != 0;
     L.num_items = pl.num_items;
     L.n_kv = n_kv;
     L.n_q = n_q;
@@ -282,9 +280,10 @@ int asv_decode_attention(const asv_attn_shape* shape, const asv_attn_args* a, vo
     L.lse = a->lse;
     char* ws = static_cast<char*>(a->workspace);
     L.sem = reinterpret_cast<int32_t*>(ws);
+    L.work = reinterpret_cast<uint32_t*>(ws + kSemBytes) + 4 * (a->launch_index & 1u);
     // partial outputs first (16-byte aligned float4 rows), then the (m, l) pairs
-    L.part_o = reinterpret_cast<float*>(ws + kSemBytes);
-    L.part_ml = reinterpret_cast<float*>(ws + kSemBytes + static_cast<int64_t>(pl.total_splits) * n_q * 512);
+    L.part_o = reinterpret_cast<float*>(ws + kHeadBytes);
+    L.part_ml = reinterpret_cast<float*>(ws + kHeadBytes + static_cast<int64_t>(pl.total_splits) * n_q * 512);
     L.sm_scale = a->sm_scale;
     cudaError_t e = attn_launch(L, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "decode attention launch");

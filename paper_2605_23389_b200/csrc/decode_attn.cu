@@ -5,23 +5,27 @@
 // s = prefix_len tokens per (request, head) — the `lens` vector the reference
 // builds in SchedulerState::running order (cluster_sim.hpp:476-479).
 //
-// Design (see DESIGN.md §3):
-//  * persistent kernel, every WARP is an independent worker with its own
-//    S-stage shared-memory ring fed by 1-D bulk TMA (cp.async.bulk + mbarrier);
-//    warps walk a static round-robin over equal-sized (request, kv head, split)
-//    work items built by the host plan, so every warp streams a near-equal KV
-//    span (length-aligned batches make the items near-identical);
+// Design (DESIGN.md §3):
+//  * persistent kernel; every WARP is an independent worker that both produces
+//    (one elected lane issues 1-D bulk TMA, cp.async.bulk + mbarrier, into a
+//    private S-stage shared-memory ring) and consumes its pages;
+//  * work items (request, kv head, <=32-page split) are grabbed dynamically from
+//    a global counter in longest-first order (host plan), with a two-item
+//    lookahead: the next item's descriptor + page indices are loaded while the
+//    current one streams, so the TMA ring never waits on index loads;
 //  * pages are stored XOR-swizzled in HBM (chunk c of row t at c ^ (t&7)), so the
 //    bulk copy lands them bank-conflict-free with no tensor map;
 //  * MHA (group 1): CUDA-core math with the sm_100 mixed-precision
-//    fma.rn.f32.bf16 (one FHFMA per MAC, no bf16->fp32 converts), warp-shuffle
-//    online softmax;
+//    fma.rn.f32.bf16 (one FHFMA per MAC, no converts), warp-shuffle softmax;
 //  * GQA (group 2..8): mma.sync.m16n8k16 bf16 on the query group (rows = heads),
-//    FA2-style register reuse of the S fragment as the PV A operand;
-//  * split partials merge in-kernel: the last-arriving warp per (request, kv head)
-//    (semaphore) combines the log-sum-exp partials and writes the output;
-//  * the warp that owns a request's last split appends the step's K/V row at
-//    position seq_len (prefix_len += 1, cluster_sim.hpp:443-447).
+//    S fragment reused in registers as the PV A operand;
+//  * split partials merge in-kernel: a warp publishes its partial, announces it
+//    with a release atomic one page later (so the store round trip is hidden),
+//    and the last arrival per (request, kv head) merges (log-sum-exp);
+//  * the owner of a request's last split appends the step's K/V row at position
+//    seq_len (prefix_len += 1, cluster_sim.hpp:443-447);
+//  * programmatic dependent launch: the KV prefetch of layer l+1 overlaps layer
+//    l's tail; q, outputs and the append wait on griddepcontrol.wait.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -33,34 +37,34 @@ namespace {
 
 constexpr int kD = 128;
 constexpr int kPage = 16;
-constexpr int kRowBytes = kD * 2;                 // 256
-constexpr int kBlockBytes = kPage * kRowBytes;    // 4096: one (page, layer, K|V, head) block
-constexpr int kStageBytes = 2 * kBlockBytes;      // K + V
+constexpr int kRowBytes = kD * 2;               // 256
+constexpr int kBlockBytes = kPage * kRowBytes;  // 4096: one (page, layer, K|V, head) block
+constexpr int kStageBytes = 2 * kBlockBytes;    // K + V
+constexpr int kRing = 4;                        // descriptor ring depth (>= stages + 1)
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct Params {
     const __nv_bfloat16* q;
-    const char* pool;          // bytes
-    char* pool_w;              // same, writable (append)
-    int64_t page_bytes;        // one page, all layers
-    int64_t layer_off;         // byte offset of the layer slice inside a page
-    int64_t v_off;             // K block -> V block, bytes (n_kv * 4096)
-    const int32_t* seq_lens;
-    const int32_t* page_indptr;
-    const int32_t* page_indices;
-    const int32_t* split_indptr;
-    const int2* item_tab;      // per global split: {request, split}
+    const char* pool;
+    char* pool_w;
+    int64_t page_bytes;
+    int64_t layer_off;
+    int64_t v_off;
+    const int32_t* gdesc;       // [G][kDescWords]
+    const int32_t* split_base;  // [b+1]
     int32_t num_items;
     int32_t n_kv;
     int32_t n_q;
+    int32_t total_warps;
     const __nv_bfloat16* k_new;
     const __nv_bfloat16* v_new;
     __nv_bfloat16* out;
     float* lse;
-    float* part_o;             // [G * n_q][128]
-    float2* part_ml;           // [G * n_q] (m in log2 units, l)
-    int32_t* sem;              // [b * n_kv]
-    float scale_log2;          // sm_scale * log2(e)
+    float* part_o;    // [slots * n_q][128]
+    float2* part_ml;  // [slots * n_q]
+    int32_t* sem;     // [b * n_kv]
+    uint32_t* work;   // [2]: grab counter, finished warps (this launch parity)
+    float scale_log2;
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -101,9 +105,9 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
         "l"(src), "r"(bytes), "r"(bar), "l"(pol)
         : "memory");
 }
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
     uint4 v;
     asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
@@ -116,7 +120,7 @@ __device__ __forceinline__ uint2 lds64(uint32_t a) {
     asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
     return v;
 }
-// d = a.lo * b.lo + c  /  a.hi * b.hi + c   (bf16 x bf16 -> fp32, sm_100 FHFMA)
+// d = a.{lo|hi} * b.{lo|hi} + c   (bf16 x bf16 -> fp32, sm_100 FHFMA)
 template <int AH, int BH>
 __device__ __forceinline__ float fma_bf(uint32_t a, uint32_t b, float c) {
     asm("{\n .reg .b16 a0, a1, b0, b1;\n mov.b32 {a0, a1}, %1;\n mov.b32 {b0, b1}, %2;\n"
@@ -144,88 +148,68 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t a, uint32_t& r0, uint32_t& r1
                  : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
                  : "r"(a));
 }
-__device__ __forceinline__ void mma_bf16(float* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
-                                         uint32_t b0, uint32_t b1) {
+__device__ __forceinline__ void mma_bf16(float* c, uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+    // rows 8..15 of A (a1, a3) are the zero padding of the <= 8-head query group
     asm volatile(
         "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7},"
         " {%8,%9}, {%0,%1,%2,%3};"
         : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+        : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
 }
-
 // zero the bf16 halves of a packed pair {token k (lo), token k+1 (hi)} past `valid`
 __device__ __forceinline__ uint32_t mask_tokens(uint32_t b, int k, int valid) {
     if (k >= valid) return 0u;
     if (k + 1 >= valid) return b & 0x0000ffffu;
     return b;
 }
-
 // swizzled byte offset of (row t, 16-byte chunk c) inside a 4 KiB block
 __device__ __forceinline__ uint32_t swz(int t, int c) {
     return static_cast<uint32_t>(t * kRowBytes + ((c ^ (t & 7)) << 4));
 }
 
-// ------------------------------------------------------- work-item decoding
-struct Item {
-    int r, head, split, nsplit, g;
-    int pb, pe;          // page range [pb, pe) within the request's page list
-    int seq;             // tokens attended
-    int idx_base;        // page_indptr[r]
+// ------------------------------------------------------- work items
+// Host plan descriptor per global split g (asv_attn_plan_build):
+//   [0] request  [1] partial slot  [2] page_begin  [3] page_end  [4] seq_len
+//   [5] nsplit   [6] append page (physical id, -1: none)  [7] 0
+//   [8 .. 8+32) physical page ids of pages page_begin .. page_end-1
+struct Desc {
+    int r, slot, pb, pe, seq, nsplit, append_phys, head;
 };
 
-__device__ __forceinline__ Item decode_item(const Params& p, int k) {
-    Item it;
-    it.g = k / p.n_kv;
-    it.head = k - it.g * p.n_kv;
-    const int2 rs = __ldg(p.item_tab + it.g);
-    it.r = rs.x;
-    it.split = rs.y;
-    const int s0 = __ldg(p.split_indptr + it.r);
-    it.nsplit = __ldg(p.split_indptr + it.r + 1) - s0;
-    it.seq = __ldg(p.seq_lens + it.r);
-    it.idx_base = __ldg(p.page_indptr + it.r);
-    const int npages = (it.seq + kPage - 1) / kPage;
-    const int chunk = (npages + it.nsplit - 1) / it.nsplit;
-    it.pb = it.split * chunk;
-    it.pe = min(npages, it.pb + chunk);
-    if (it.pe < it.pb) it.pe = it.pb;
-    return it;
+// lane 0 reserves `n` consecutive item ids; the raw result stays in lane 0's
+// register until broadcast, so the atomic's latency overlaps useful work.
+__device__ __forceinline__ uint32_t grab_raw(const Params& p, int lane, uint32_t n) {
+    uint32_t k = 0;
+    if (lane == 0) k = atomicAdd(p.work, n);
+    return k;
 }
+__device__ __forceinline__ uint32_t bcast(uint32_t v) { return __shfl_sync(0xffffffffu, v, 0); }
 
-// Warp-local cursor over the flattened (item, page) stream of one warp.
-struct Cursor {
-    int k;      // current item id (>= num_items => done)
-    int page;   // absolute page index inside the item range
-    Item it;
-};
-
-__device__ __forceinline__ void cursor_seek(const Params& p, Cursor& c, int stride) {
-    // advance to the first item (from c.k) that has at least one page
-    while (c.k < p.num_items) {
-        c.it = decode_item(p, c.k);
-        if (c.it.pe > c.it.pb) {
-            c.page = c.it.pb;
-            return;
-        }
-        c.k += stride;
+// Issue the (independent) loads of item k's descriptor; lane j also fetches the
+// physical id of the item's j-th page.  Nothing here is consumed until the item
+// becomes current, so the latency hides behind the previous item.
+__device__ __forceinline__ void load_desc(const Params& p, uint32_t k, int lane, Desc& d, int& phys) {
+    if (k >= static_cast<uint32_t>(p.num_items)) {
+        d.pb = d.pe = 0;
+        phys = 0;
+        return;
     }
-}
-
-__device__ __forceinline__ void cursor_next(const Params& p, Cursor& c, int stride) {
-    if (++c.page >= c.it.pe) {
-        c.k += stride;
-        cursor_seek(p, c, stride);
-    }
+    const int g = static_cast<int>(k) / p.n_kv;
+    d.head = static_cast<int>(k) - g * p.n_kv;
+    const int32_t* gd = p.gdesc + static_cast<int64_t>(g) * kDescWords;
+    const int4 a = __ldg(reinterpret_cast<const int4*>(gd));
+    const int4 b = __ldg(reinterpret_cast<const int4*>(gd) + 1);
+    phys = __ldg(gd + 8 + lane);
+    d.r = a.x;
+    d.slot = a.y;
+    d.pb = a.z;
+    d.pe = a.w;
+    d.seq = b.x;
+    d.nsplit = b.y;
+    d.append_phys = b.z;
 }
 
 // ------------------------------------------------------------- epilogues
-// Finish one (request, q head) row: o (unnormalised, 4 dims per lane for MHA
-// layout), m (log2 units) and l.  Either writes the output directly
-// (single split) or publishes a partial and lets the last arrival merge.
-struct RowOut {
-    float o[4];   // dims 4*lane .. 4*lane+3
-};
-
 __device__ __forceinline__ void write_final_row(const Params& p, int r, int qh, int lane, const float* o,
                                                 float m, float l) {
     const float inv = l > 0.f ? 1.f / l : 0.f;
@@ -238,10 +222,10 @@ __device__ __forceinline__ void write_final_row(const Params& p, int r, int qh, 
     }
 }
 
-// Merge all split partials of (r, qh); every lane owns dims 4*lane..+3.
+// Merge all split partials of (r, qh); every lane owns dims 4*lane .. 4*lane+3.
 __device__ __forceinline__ void merge_row(const Params& p, int r, int qh, int lane) {
-    const int s0 = __ldg(p.split_indptr + r);
-    const int ns = __ldg(p.split_indptr + r + 1) - s0;
+    const int s0 = __ldg(p.split_base + r);
+    const int ns = __ldg(p.split_base + r + 1) - s0;
     float M = -INFINITY;
     for (int s = 0; s < ns; ++s) {
         const float2 ml = __ldcg(p.part_ml + static_cast<int64_t>(s0 + s) * p.n_q + qh);
@@ -263,440 +247,481 @@ __device__ __forceinline__ void merge_row(const Params& p, int r, int qh, int la
     write_final_row(p, r, qh, lane, o, M, L);
 }
 
-// Publish one row partial; returns via the caller's semaphore logic.
-__device__ __forceinline__ void store_partial_row(const Params& p, int g, int qh, int lane, const float* o,
-                                                  float m, float l) {
-    const int64_t slot = static_cast<int64_t>(g) * p.n_q + qh;
-    __stcg(reinterpret_cast<float4*>(p.part_o + slot * kD) + lane, make_float4(o[0], o[1], o[2], o[3]));
-    if (lane == 0) __stcg(p.part_ml + slot, make_float2(m, l));
-}
-
-// After all rows of an item are published: bump the (r, kv head) semaphore and
-// return true on the last arrival (which then merges).
-__device__ __forceinline__ bool arrive_last(const Params& p, const Item& it, int lane) {
-    __threadfence();
+// Announce a published partial (release) and, on the last arrival for this
+// (request, kv head), merge every query head of the group.
+template <int GROUP>
+__device__ __forceinline__ void announce(const Params& p, int r, int head, int nsplit, int lane) {
     __syncwarp();
-    int last = 0;
+    int prev = 0;
     if (lane == 0) {
-        int32_t* s = p.sem + static_cast<int64_t>(it.r) * p.n_kv + it.head;
-        const int prev = atomicAdd(s, 1);
-        last = (prev == it.nsplit - 1);
-        if (last) *s = 0;  // re-arm for the next launch (stream-ordered)
+        int32_t* s = p.sem + static_cast<int64_t>(r) * p.n_kv + head;
+        asm volatile("atom.release.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(s) : "memory");
+        if (prev == nsplit - 1) *s = 0;  // re-arm for the next launch (stream-ordered)
     }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (last) __threadfence();
-    return last != 0;
+    prev = __shfl_sync(0xffffffffu, prev, 0);
+    if (prev == nsplit - 1) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        for (int gh = 0; gh < GROUP; ++gh) merge_row(p, r, head * GROUP + gh, lane);
+    }
 }
 
-// KV append (K3): the owner of the last split writes token row `seq` of
-// (layer, head).  Lanes 0-15: K row, 16-31: V row; 16 bytes each, swizzled.
-__device__ __forceinline__ void append_row(const Params& p, const Item& it, int lane) {
-    if (p.k_new == nullptr || it.split != it.nsplit - 1) return;
-    const int pos = it.seq;
-    const int pidx = pos / kPage;
-    const int npl = __ldg(p.page_indptr + it.r + 1) - it.idx_base;
-    if (pidx >= npl) return;  // host did not provision the append page
-    const int t = pos % kPage;
-    const int64_t phys = __ldg(p.page_indices + it.idx_base + pidx);
+// KV append (K3): lanes 0-15 write the K row, 16-31 the V row (16 B each, swizzled).
+__device__ __forceinline__ void append_row(const Params& p, const Desc& d, int lane) {
+    if (p.k_new == nullptr || d.append_phys < 0) return;
+    const int t = d.seq % kPage;
     const int c = lane & 15;
     const bool is_v = lane >= 16;
-    const __nv_bfloat16* src = (is_v ? p.v_new : p.k_new) +
-                               (static_cast<int64_t>(it.r) * p.n_kv + it.head) * kD + c * 8;
-    char* dst = p.pool_w + phys * p.page_bytes + p.layer_off + (is_v ? p.v_off : 0) +
-                static_cast<int64_t>(it.head) * kBlockBytes + swz(t, c);
+    const __nv_bfloat16* src =
+        (is_v ? p.v_new : p.k_new) + (static_cast<int64_t>(d.r) * p.n_kv + d.head) * kD + c * 8;
+    char* dst = p.pool_w + static_cast<int64_t>(d.append_phys) * p.page_bytes + p.layer_off +
+                (is_v ? p.v_off : 0) + static_cast<int64_t>(d.head) * kBlockBytes + swz(t, c);
     *reinterpret_cast<uint4*>(dst) = __ldg(reinterpret_cast<const uint4*>(src));
 }
+
+// ------------------------------------------------------------- q staging
+// MHA: lane (t = lane & 15, half = lane >> 4) keeps the 64 q dims of its half.
+template <int GROUP>
+struct QRegs;
+
+template <>
+struct QRegs<1> {
+    uint32_t v[32];
+    __device__ __forceinline__ void load(const Params& p, const Desc& d, int lane) {
+        const uint4* src = reinterpret_cast<const uint4*>(
+            p.q + (static_cast<int64_t>(d.r) * p.n_q + d.head) * kD + (lane >> 4) * 64);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint4 x = __ldg(src + j);
+            v[4 * j + 0] = x.x;
+            v[4 * j + 1] = x.y;
+            v[4 * j + 2] = x.z;
+            v[4 * j + 3] = x.w;
+        }
+    }
+};
+
+// GQA: A fragments (rows = query heads of the group, 8 k-steps of 16 dims).
+template <int GROUP>
+struct QRegs {
+    uint32_t v[16];
+    __device__ __forceinline__ void load(const Params& p, const Desc& d, int lane) {
+        const int qrow = lane >> 2, qcol = (lane & 3) * 2;
+        const bool rv = qrow < GROUP;
+        const __nv_bfloat16* src =
+            p.q + (static_cast<int64_t>(d.r) * p.n_q + d.head * GROUP + (rv ? qrow : 0)) * kD;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+            v[2 * ks] = rv ? __ldg(reinterpret_cast<const uint32_t*>(src + ks * 16 + qcol)) : 0u;
+            v[2 * ks + 1] = rv ? __ldg(reinterpret_cast<const uint32_t*>(src + ks * 16 + 8 + qcol)) : 0u;
+        }
+    }
+};
+
+// ------------------------------------------------------- per-item state
+template <int GROUP>
+struct Acc;
+
+template <>
+struct Acc<1> {
+    float m, l, o[4];
+    __device__ __forceinline__ void reset() {
+        m = -INFINITY;
+        l = 0.f;
+        o[0] = o[1] = o[2] = o[3] = 0.f;
+    }
+    // one 16-token page: scores, online softmax, P.V
+    __device__ __forceinline__ void page(const QRegs<1>& q, uint32_t ks, uint32_t vs, uint32_t sp,
+                                         __nv_bfloat16* scratch, int valid, float scale, int lane) {
+        const int t = lane & 15;
+        const int half = lane >> 4;
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint4 kv = lds128(ks + swz(t, half * 8 + j));
+            a0 = fma_bf<0, 0>(kv.x, q.v[4 * j + 0], a0);
+            a1 = fma_bf<1, 1>(kv.x, q.v[4 * j + 0], a1);
+            a2 = fma_bf<0, 0>(kv.y, q.v[4 * j + 1], a2);
+            a3 = fma_bf<1, 1>(kv.y, q.v[4 * j + 1], a3);
+            a0 = fma_bf<0, 0>(kv.z, q.v[4 * j + 2], a0);
+            a1 = fma_bf<1, 1>(kv.z, q.v[4 * j + 2], a1);
+            a2 = fma_bf<0, 0>(kv.w, q.v[4 * j + 3], a2);
+            a3 = fma_bf<1, 1>(kv.w, q.v[4 * j + 3], a3);
+        }
+        float s = (a0 + a1) + (a2 + a3);
+        s += __shfl_xor_sync(0xffffffffu, s, 16);
+        s = (t < valid) ? s * scale : -INFINITY;
+        float mx = s;
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+        const float m_new = fmaxf(m, mx);
+        const float alpha = exp2f(m - m_new);
+        m = m_new;
+        // P rounded to bf16 for the PV product (FA2/FA3 convention); l sums the
+        // rounded weights so O / l stays an exact convex combination of V rows.
+        const __nv_bfloat16 pb = __float2bfloat16_rn(exp2f(s - m_new));
+        l = l * alpha + ((half == 0) ? __bfloat162float(pb) : 0.f);
+        o[0] *= alpha;
+        o[1] *= alpha;
+        o[2] *= alpha;
+        o[3] *= alpha;
+        if (half == 0) scratch[t] = pb;
+        __syncwarp();
+        const uint4 p0 = lds128(sp);
+        const uint4 p1 = lds128(sp + 16);
+        const uint32_t pw[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+        const int cidx = lane >> 1;
+        const uint32_t coff = (lane & 1) * 8;
+        if (valid == kPage) {
+#pragma unroll
+            for (int tt = 0; tt < kPage; tt += 2) {
+                const uint2 v0 = lds64(vs + swz(tt, cidx) + coff);
+                const uint2 v1 = lds64(vs + swz(tt + 1, cidx) + coff);
+                const uint32_t pp = pw[tt >> 1];
+                o[0] = fma_bf<0, 0>(v0.x, pp, o[0]);
+                o[1] = fma_bf<1, 0>(v0.x, pp, o[1]);
+                o[2] = fma_bf<0, 0>(v0.y, pp, o[2]);
+                o[3] = fma_bf<1, 0>(v0.y, pp, o[3]);
+                o[0] = fma_bf<0, 1>(v1.x, pp, o[0]);
+                o[1] = fma_bf<1, 1>(v1.x, pp, o[1]);
+                o[2] = fma_bf<0, 1>(v1.y, pp, o[2]);
+                o[3] = fma_bf<1, 1>(v1.y, pp, o[3]);
+            }
+        } else {
+            // partial last page: rows >= valid may hold stale data (0 * NaN = NaN)
+#pragma unroll
+            for (int tt = 0; tt < kPage; tt += 2) {
+                uint2 v0 = lds64(vs + swz(tt, cidx) + coff);
+                uint2 v1 = lds64(vs + swz(tt + 1, cidx) + coff);
+                if (tt >= valid) v0 = make_uint2(0u, 0u);
+                if (tt + 1 >= valid) v1 = make_uint2(0u, 0u);
+                const uint32_t pp = pw[tt >> 1];
+                o[0] = fma_bf<0, 0>(v0.x, pp, o[0]);
+                o[1] = fma_bf<1, 0>(v0.x, pp, o[1]);
+                o[2] = fma_bf<0, 0>(v0.y, pp, o[2]);
+                o[3] = fma_bf<1, 0>(v0.y, pp, o[3]);
+                o[0] = fma_bf<0, 1>(v1.x, pp, o[0]);
+                o[1] = fma_bf<1, 1>(v1.x, pp, o[1]);
+                o[2] = fma_bf<0, 1>(v1.y, pp, o[2]);
+                o[3] = fma_bf<1, 1>(v1.y, pp, o[3]);
+            }
+        }
+    }
+    // returns true when a partial was published (announce pending)
+    __device__ __forceinline__ bool finish(const Params& p, const Desc& d, int lane) {
+        float lt = l;
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) lt += __shfl_xor_sync(0xffffffffu, lt, off);
+        if (d.nsplit == 1) {
+            write_final_row(p, d.r, d.head, lane, o, m, lt);
+            return false;
+        }
+        const int64_t slot = static_cast<int64_t>(d.slot) * p.n_q + d.head;
+        __stcg(reinterpret_cast<float4*>(p.part_o + slot * kD) + lane, make_float4(o[0], o[1], o[2], o[3]));
+        if (lane == 0) __stcg(p.part_ml + slot, make_float2(m, lt));
+        return true;
+    }
+};
+
+template <int GROUP>
+struct Acc {
+    float m, l;
+    float o[16][2];  // C rows 0-7 (query heads), 16 n-tiles of 8 dims
+    __device__ __forceinline__ void reset() {
+        m = -INFINITY;
+        l = 0.f;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = 0.f;
+    }
+    __device__ __forceinline__ void page(const QRegs<GROUP>& q, uint32_t ks, uint32_t vs, uint32_t,
+                                         __nv_bfloat16*, int valid, float scale, int lane) {
+        const int qcol = (lane & 3) * 2;
+        // S = Q K^T: two n-tiles of 8 tokens, 8 k-steps of 16 dims
+        float sacc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+            const int trow = nt * 8 + (lane & 7);
+#pragma unroll
+            for (int kk = 0; kk < 8; kk += 2) {
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4(ks + swz(trow, 2 * kk + (lane >> 3)), b0, b1, b2, b3);
+                mma_bf16(sacc[nt], q.v[2 * kk], q.v[2 * kk + 1], b0, b1);
+                mma_bf16(sacc[nt], q.v[2 * kk + 2], q.v[2 * kk + 3], b2, b3);
+            }
+        }
+        float sv[4];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int tok = nt * 8 + qcol + e;
+                sv[nt * 2 + e] = (tok < valid) ? sacc[nt][e] * scale : -INFINITY;
+            }
+        }
+        float mx = fmaxf(fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3]));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float m_new = fmaxf(m, mx);
+        const float alpha = exp2f(m - m_new);
+        m = m_new;
+        uint32_t pa[2];
+        float psum = 0.f;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+            pa[nt] = pack_bf16(exp2f(sv[nt * 2] - m_new), exp2f(sv[nt * 2 + 1] - m_new));
+            psum += bf16_lo(pa[nt]) + bf16_hi(pa[nt]);
+        }
+        l = l * alpha + psum;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            o[i][0] *= alpha;
+            o[i][1] *= alpha;
+        }
+        // O += P V: A = P (the S fragments, bf16), B = V tile via ldmatrix.trans
+        const int trow = (lane & 7) + ((lane >> 3) & 1) * 8;
+#pragma unroll
+        for (int dn = 0; dn < 16; dn += 2) {
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4_t(vs + swz(trow, dn + (lane >> 4)), b0, b1, b2, b3);
+            if (valid < kPage) {
+                b0 = mask_tokens(b0, qcol, valid);
+                b2 = mask_tokens(b2, qcol, valid);
+                b1 = mask_tokens(b1, qcol + 8, valid);
+                b3 = mask_tokens(b3, qcol + 8, valid);
+            }
+            float c0[4] = {o[dn][0], o[dn][1], 0.f, 0.f};
+            float c1[4] = {o[dn + 1][0], o[dn + 1][1], 0.f, 0.f};
+            mma_bf16(c0, pa[0], pa[1], b0, b1);
+            mma_bf16(c1, pa[0], pa[1], b2, b3);
+            o[dn][0] = c0[0];
+            o[dn][1] = c0[1];
+            o[dn + 1][0] = c1[0];
+            o[dn + 1][1] = c1[1];
+        }
+    }
+    __device__ __forceinline__ bool finish(const Params& p, const Desc& d, int lane) {
+        float lt = l;
+        lt += __shfl_xor_sync(0xffffffffu, lt, 1);
+        lt += __shfl_xor_sync(0xffffffffu, lt, 2);
+        const int qrow = lane >> 2, qcol = (lane & 3) * 2;
+        const bool rv = qrow < GROUP;
+        const int qh = d.head * GROUP + qrow;
+        if (d.nsplit == 1) {
+            if (rv) {
+                const float inv = lt > 0.f ? 1.f / lt : 0.f;
+                __nv_bfloat16* dst = p.out + (static_cast<int64_t>(d.r) * p.n_q + qh) * kD;
+#pragma unroll
+                for (int nt = 0; nt < 16; ++nt) {
+                    *reinterpret_cast<uint32_t*>(dst + nt * 8 + qcol) = pack_bf16(o[nt][0] * inv, o[nt][1] * inv);
+                }
+                if (p.lse != nullptr && (lane & 3) == 0) {
+                    p.lse[static_cast<int64_t>(d.r) * p.n_q + qh] =
+                        lt > 0.f ? (m + __log2f(lt)) / kLog2e : -INFINITY;
+                }
+            }
+            return false;
+        }
+        if (rv) {
+            const int64_t slot = static_cast<int64_t>(d.slot) * p.n_q + qh;
+            float* dst = p.part_o + slot * kD;
+#pragma unroll
+            for (int nt = 0; nt < 16; ++nt) {
+                __stcg(reinterpret_cast<float2*>(dst + nt * 8 + qcol), make_float2(o[nt][0], o[nt][1]));
+            }
+            if ((lane & 3) == 0) __stcg(p.part_ml + slot, make_float2(m, lt));
+        }
+        return true;
+    }
+};
 
 // ============================================================ the kernel
 template <int NW, int S, int GROUP>
 __global__ void __launch_bounds__(NW * 32)
 decode_attn_kernel(const Params p) {
+    static_assert(kRing >= S + 1, "descriptor ring must cover the TMA lookahead");
     extern __shared__ __align__(1024) char smem_raw[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    // per-warp region: S stages (8 KiB each) + S mbarriers + scratch
-    constexpr int kWarpBytes = S * kStageBytes + 128;
+    // per warp: S stages (8 KiB) | S mbarriers (64 B) | p scratch (64 B) | desc ring (128 B)
+    constexpr int kWarpBytes = S * kStageBytes + 256;
     char* wbase = smem_raw + warp * kWarpBytes;
     const uint32_t stage0 = smem_u32(wbase);
     const uint32_t bar0 = smem_u32(wbase + S * kStageBytes);
-    char* scratch = wbase + S * kStageBytes + 64;  // 64 bytes
+    __nv_bfloat16* scratch = reinterpret_cast<__nv_bfloat16*>(wbase + S * kStageBytes + 64);
+    const uint32_t sp = smem_u32(scratch);
+    Desc* ring = reinterpret_cast<Desc*>(wbase + S * kStageBytes + 128);
 
     if (lane == 0) {
         for (int s = 0; s < S; ++s) mbar_init(bar0 + 8 * s, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncwarp();
-
-    const int stride = gridDim.x * NW;            // total persistent warps
-    const int wid = blockIdx.x * NW + warp;       // this warp's worker id
     const uint64_t pol = evict_first_policy();
 
-    // producer cursor (only lane 0 issues, but all lanes track it uniformly)
-    Cursor pc;
-    pc.k = wid;
-    cursor_seek(p, pc, stride);
+    // ---- producer state: current item (descriptor + lane-distributed page ids),
+    // next item (loads in flight), and the id after that (atomic in flight)
+    Desc cur, nxt;
+    int cur_phys, nxt_phys;
+    const uint32_t k0 = bcast(grab_raw(p, lane, 3u));
+    uint32_t k1 = k0 + 1u;
+    uint32_t k2_raw = k0 + 2u;  // valid on every lane here; later only on lane 0
+    load_desc(p, k0, lane, cur, cur_phys);
+    load_desc(p, k1, lane, nxt, nxt_phys);
+    int ppage = cur.pb;
+    bool have_cur = k0 < static_cast<uint32_t>(p.num_items);
+    int pushed = 0;
+    if (have_cur && lane == 0) ring[0] = cur;
+    if (have_cur) pushed = 1;
+    __syncwarp();
 
+    auto advance_producer = [&]() {
+        cur = nxt;
+        cur_phys = nxt_phys;
+        have_cur = k1 < static_cast<uint32_t>(p.num_items);
+        if (have_cur) {
+            k1 = bcast(k2_raw);
+            ppage = cur.pb;
+            if (lane == 0) ring[pushed % kRing] = cur;
+            ++pushed;
+            load_desc(p, k1, lane, nxt, nxt_phys);
+            if (k1 < static_cast<uint32_t>(p.num_items)) k2_raw = grab_raw(p, lane, 1u);
+        }
+    };
     auto issue = [&](int slot) {
+        const int phys = __shfl_sync(0xffffffffu, cur_phys, ppage - cur.pb);
         if (lane == 0) {
-            const int64_t phys = __ldg(p.page_indices + pc.it.idx_base + pc.page);
-            const char* kblk = p.pool + phys * p.page_bytes + p.layer_off +
-                               static_cast<int64_t>(pc.it.head) * kBlockBytes;
+            const char* kblk = p.pool + static_cast<int64_t>(phys) * p.page_bytes + p.layer_off +
+                               static_cast<int64_t>(cur.head) * kBlockBytes;
             const uint32_t bar = bar0 + 8 * slot;
             const uint32_t dst = stage0 + slot * kStageBytes;
             mbar_expect_tx(bar, kStageBytes);
             bulk_g2s(dst, kblk, kBlockBytes, bar, pol);
             bulk_g2s(dst + kBlockBytes, kblk + p.v_off, kBlockBytes, bar, pol);
         }
-        cursor_next(p, pc, stride);
+        if (++ppage >= cur.pe) advance_producer();
     };
 
-    // prologue: fill the ring
+    // prologue: fill the ring (KV does not depend on the previous layer)
     int issued = 0;
-#pragma unroll 1
-    for (; issued < S && pc.k < p.num_items; ++issued) issue(issued);
+    for (; issued < S && have_cur; ++issued) issue(issued);
 
-    Cursor cc;  // consumer cursor
-    cc.k = wid;
-    cursor_seek(p, cc, stride);
-    int consumed = 0;
+    // everything below reads q / writes outputs: wait for the previous grid
+    grid_dep_wait();
+    grid_dep_launch();
 
-    if constexpr (GROUP == 1) {
-        // ---------------------------------------------------------- MHA / FHFMA
-        const int t = lane & 15;      // token row for QK
-        const int half = lane >> 4;   // which 64-dim half of the row
-        uint32_t qreg[32];            // this lane's 64 q dims (bf16x2)
-        float m = -INFINITY, l = 0.f;
-        float o[4] = {0.f, 0.f, 0.f, 0.f};
-        int cur_k = -1;
-#pragma unroll 1
-        while (cc.k < p.num_items) {
-            const Item& it = cc.it;
-            if (cc.k != cur_k) {
-                // new item: load q, reset state, append the step's KV row
-                cur_k = cc.k;
-                const uint4* qs = reinterpret_cast<const uint4*>(
-                    p.q + (static_cast<int64_t>(it.r) * p.n_q + it.head) * kD + half * 64);
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const uint4 v = __ldg(qs + j);
-                    qreg[4 * j + 0] = v.x;
-                    qreg[4 * j + 1] = v.y;
-                    qreg[4 * j + 2] = v.z;
-                    qreg[4 * j + 3] = v.w;
-                }
-                m = -INFINITY;
-                l = 0.f;
-                o[0] = o[1] = o[2] = o[3] = 0.f;
-                append_row(p, it, lane);
-            }
-            const int slot = consumed % S;
-            const uint32_t phase = (consumed / S) & 1;
-            mbar_wait(bar0 + 8 * slot, phase);
-            const uint32_t ks = stage0 + slot * kStageBytes;
-            const uint32_t vs = ks + kBlockBytes;
-            const int valid = min(kPage, it.seq - cc.page * kPage);
+    QRegs<GROUP> q, qn;
+    Acc<GROUP> acc;
+    int consumed = 0;   // pages
+    int citem = 0;      // items started by the consumer
+    bool qn_ready = false;
+    Desc cd;            // consumer's current item
+    int cpage = 0;
+    // deferred partial announcement
+    bool pend = false;
+    int pend_r = 0, pend_head = 0, pend_ns = 0;
 
-            // ---- scores: lane (t, half) dots its 64 dims, then combine halves
-            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const uint4 kv = lds128(ks + swz(t, half * 8 + j));
-                a0 = fma_bf<0, 0>(kv.x, qreg[4 * j + 0], a0);
-                a1 = fma_bf<1, 1>(kv.x, qreg[4 * j + 0], a1);
-                a2 = fma_bf<0, 0>(kv.y, qreg[4 * j + 1], a2);
-                a3 = fma_bf<1, 1>(kv.y, qreg[4 * j + 1], a3);
-                a0 = fma_bf<0, 0>(kv.z, qreg[4 * j + 2], a0);
-                a1 = fma_bf<1, 1>(kv.z, qreg[4 * j + 2], a1);
-                a2 = fma_bf<0, 0>(kv.w, qreg[4 * j + 3], a2);
-                a3 = fma_bf<1, 1>(kv.w, qreg[4 * j + 3], a3);
-            }
-            float s = (a0 + a1) + (a2 + a3);
-            s += __shfl_xor_sync(0xffffffffu, s, 16);
-            s = (t < valid) ? s * p.scale_log2 : -INFINITY;
-            // ---- online softmax (warp-uniform running max)
-            float mx = s;
-            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
-            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
-            const float m_new = fmaxf(m, mx);
-            const float alpha = exp2f(m - m_new);  // m=-inf -> 0
-            m = m_new;
-            const float pf = exp2f(s - m_new);     // masked rows -> 0
-            // P is rounded to bf16 for the PV product (FA2/FA3 convention); l sums
-            // the rounded weights so O/l stays an exact convex combination.
-            const __nv_bfloat16 pb = __float2bfloat16_rn(pf);
-            l = l * alpha + ((half == 0) ? __bfloat162float(pb) : 0.f);
-            o[0] *= alpha;
-            o[1] *= alpha;
-            o[2] *= alpha;
-            o[3] *= alpha;
-            if (half == 0) reinterpret_cast<__nv_bfloat16*>(scratch)[t] = pb;
-            __syncwarp();
-            const uint32_t sp = smem_u32(scratch);
-            const uint4 p0 = lds128(sp);
-            const uint4 p1 = lds128(sp + 16);
-            const uint32_t pw[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
-            // ---- PV: lane owns dims 4*lane .. 4*lane+3
-            const int cidx = lane >> 1;           // 16-byte chunk holding the dims
-            const uint32_t coff = (lane & 1) * 8; // 8-byte half inside the chunk
-            if (valid == kPage) {
-#pragma unroll
-                for (int tt = 0; tt < kPage; tt += 2) {
-                    const uint2 v0 = lds64(vs + swz(tt, cidx) + coff);
-                    const uint2 v1 = lds64(vs + swz(tt + 1, cidx) + coff);
-                    const uint32_t pp = pw[tt >> 1];
-                    o[0] = fma_bf<0, 0>(v0.x, pp, o[0]);
-                    o[1] = fma_bf<1, 0>(v0.x, pp, o[1]);
-                    o[2] = fma_bf<0, 0>(v0.y, pp, o[2]);
-                    o[3] = fma_bf<1, 0>(v0.y, pp, o[3]);
-                    o[0] = fma_bf<0, 1>(v1.x, pp, o[0]);
-                    o[1] = fma_bf<1, 1>(v1.x, pp, o[1]);
-                    o[2] = fma_bf<0, 1>(v1.y, pp, o[2]);
-                    o[3] = fma_bf<1, 1>(v1.y, pp, o[3]);
-                }
-            } else {
-                // partial last page: never touch rows >= valid (may be stale)
-#pragma unroll
-                for (int tt = 0; tt < kPage; tt += 2) {
-                    uint2 v0 = lds64(vs + swz(tt, cidx) + coff);
-                    uint2 v1 = lds64(vs + swz(tt + 1, cidx) + coff);
-                    if (tt >= valid) v0 = make_uint2(0u, 0u);
-                    if (tt + 1 >= valid) v1 = make_uint2(0u, 0u);
-                    const uint32_t pp = pw[tt >> 1];
-                    o[0] = fma_bf<0, 0>(v0.x, pp, o[0]);
-                    o[1] = fma_bf<1, 0>(v0.x, pp, o[1]);
-                    o[2] = fma_bf<0, 0>(v0.y, pp, o[2]);
-                    o[3] = fma_bf<1, 0>(v0.y, pp, o[3]);
-                    o[0] = fma_bf<0, 1>(v1.x, pp, o[0]);
-                    o[1] = fma_bf<1, 1>(v1.x, pp, o[1]);
-                    o[2] = fma_bf<0, 1>(v1.y, pp, o[2]);
-                    o[3] = fma_bf<1, 1>(v1.y, pp, o[3]);
-                }
-            }
-            __syncwarp();
-            ++consumed;
-            // refill the slot we just drained
-            if (pc.k < p.num_items) {
-                fence_proxy_async();
-                issue(slot);
-                ++issued;
-            }
-            const bool item_end = (cc.page + 1 >= it.pe);
-            if (item_end) {
-                // finalize the (request, head) row of this item
-                float lt = l;
-#pragma unroll
-                for (int off = 16; off >= 1; off >>= 1) lt += __shfl_xor_sync(0xffffffffu, lt, off);
-                if (it.nsplit == 1) {
-                    write_final_row(p, it.r, it.head, lane, o, m, lt);
-                } else {
-                    store_partial_row(p, it.g, it.head, lane, o, m, lt);
-                    if (arrive_last(p, it, lane)) merge_row(p, it.r, it.head, lane);
-                }
-            }
-            cursor_next(p, cc, stride);
+    while (citem < pushed) {
+        // ---- start the next item (the producer pushed it >= 1 page ago or just now)
+        __syncwarp();
+        cd = ring[citem % kRing];
+        ++citem;
+        if (qn_ready) {
+            q = qn;
+            qn_ready = false;
+        } else {
+            q.load(p, cd, lane);
         }
-    } else {
-        // -------------------------------------------------- GQA / mma.sync
-        // rows of the m16 tile = the GROUP query heads of this kv head (padded)
-        const int qrow = lane >> 2;          // A/C fragment row owned (0..7)
-        const int qcol = (lane & 3) * 2;     // fragment column pair
-        uint32_t qa[8][2];                   // A fragments (rows 0-7) for 8 k-steps
-        float oacc[16][2];                   // C rows 0-7, 16 n-tiles of 8 dims
-        float m = -INFINITY, l = 0.f;
-        int cur_k = -1;
-#pragma unroll 1
-        while (cc.k < p.num_items) {
-            const Item& it = cc.it;
-            if (cc.k != cur_k) {
-                cur_k = cc.k;
-                const int qh = it.head * GROUP + qrow;
-                const bool rv = qrow < GROUP;
-                const __nv_bfloat16* qsrc = p.q + (static_cast<int64_t>(it.r) * p.n_q + qh) * kD;
-#pragma unroll
-                for (int ks = 0; ks < 8; ++ks) {
-                    qa[ks][0] = rv ? __ldg(reinterpret_cast<const uint32_t*>(qsrc + ks * 16 + qcol)) : 0u;
-                    qa[ks][1] = rv ? __ldg(reinterpret_cast<const uint32_t*>(qsrc + ks * 16 + 8 + qcol)) : 0u;
-                }
-#pragma unroll
-                for (int nt = 0; nt < 16; ++nt) oacc[nt][0] = oacc[nt][1] = 0.f;
-                m = -INFINITY;
-                l = 0.f;
-                append_row(p, it, lane);
-            }
+        acc.reset();
+        append_row(p, cd, lane);
+        for (cpage = cd.pb; cpage < cd.pe; ++cpage) {
             const int slot = consumed % S;
-            const uint32_t phase = (consumed / S) & 1;
-            mbar_wait(bar0 + 8 * slot, phase);
-            const uint32_t ks_base = stage0 + slot * kStageBytes;
-            const uint32_t vs_base = ks_base + kBlockBytes;
-            const int valid = min(kPage, it.seq - cc.page * kPage);
-
-            // ---- S = Q K^T : two n-tiles of 8 tokens, 8 k-steps of 16 dims
-            float sacc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-                const int trow = nt * 8 + (lane & 7);
-#pragma unroll
-                for (int kk = 0; kk < 8; kk += 2) {
-                    // matrices: chunks 2kk, 2kk+1, 2kk+2, 2kk+3 of rows trow
-                    const int chunk = 2 * kk + (lane >> 3);
-                    uint32_t b0, b1, b2, b3;
-                    ldsm_x4(ks_base + swz(trow, chunk), b0, b1, b2, b3);
-                    mma_bf16(sacc[nt], qa[kk][0], 0u, qa[kk][1], 0u, b0, b1);
-                    mma_bf16(sacc[nt], qa[kk + 1][0], 0u, qa[kk + 1][1], 0u, b2, b3);
-                }
-            }
-            // lane holds S[row=qrow][tokens nt*8 + qcol, +1] in sacc[nt][0..1]
-            float sv[4];
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int tok = nt * 8 + qcol + e;
-                    sv[nt * 2 + e] = (tok < valid) ? sacc[nt][e] * p.scale_log2 : -INFINITY;
-                }
-            }
-            float mx = fmaxf(fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3]));
-            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-            const float m_new = fmaxf(m, mx);
-            const float alpha = exp2f(m - m_new);
-            m = m_new;
-            uint32_t pa[2];
-            float psum = 0.f;
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-                const float e0 = exp2f(sv[nt * 2] - m_new);
-                const float e1 = exp2f(sv[nt * 2 + 1] - m_new);
-                pa[nt] = pack_bf16(e0, e1);
-                psum += bf16_lo(pa[nt]) + bf16_hi(pa[nt]);
-            }
-            l = l * alpha + psum;
-#pragma unroll
-            for (int nt = 0; nt < 16; ++nt) {
-                oacc[nt][0] *= alpha;
-                oacc[nt][1] *= alpha;
-            }
-            // ---- O += P V : A = P (k = 16 tokens), B = V tile via ldmatrix.trans
-            // rows >= valid of V must not leak NaN/Inf: P is 0 there, but 0*Inf = NaN,
-            // so for partial pages re-zero the stale rows' contribution by masking B.
-#pragma unroll
-            for (int dn = 0; dn < 16; dn += 2) {
-                // matrices: (tokens 0-7, dims 8dn..), (tokens 8-15, dims 8dn..),
-                //           (tokens 0-7, dims 8dn+8..), (tokens 8-15, dims 8dn+8..)
-                const int trow = (lane & 7) + ((lane >> 3) & 1) * 8;
-                const int chunk = dn + (lane >> 4);
-                uint32_t b0, b1, b2, b3;
-                ldsm_x4_t(vs_base + swz(trow, chunk), b0, b1, b2, b3);
-                if (valid < kPage) {
-                    // lane holds B[k = tokens qcol, qcol+1 (b0,b2) / +8 (b1,b3)][n]
-                    b0 = mask_tokens(b0, qcol, valid);
-                    b2 = mask_tokens(b2, qcol, valid);
-                    b1 = mask_tokens(b1, qcol + 8, valid);
-                    b3 = mask_tokens(b3, qcol + 8, valid);
-                }
-                float c0[4] = {oacc[dn][0], oacc[dn][1], 0.f, 0.f};
-                float c1[4] = {oacc[dn + 1][0], oacc[dn + 1][1], 0.f, 0.f};
-                mma_bf16(c0, pa[0], 0u, pa[1], 0u, b0, b1);
-                mma_bf16(c1, pa[0], 0u, pa[1], 0u, b2, b3);
-                oacc[dn][0] = c0[0];
-                oacc[dn][1] = c0[1];
-                oacc[dn + 1][0] = c1[0];
-                oacc[dn + 1][1] = c1[1];
-            }
+            mbar_wait(bar0 + 8 * slot, (consumed / S) & 1);
+            const uint32_t ks = stage0 + slot * kStageBytes;
+            acc.page(q, ks, ks + kBlockBytes, sp, scratch, min(kPage, cd.seq - cpage * kPage), p.scale_log2, lane);
             __syncwarp();
             ++consumed;
-            if (pc.k < p.num_items) {
-                fence_proxy_async();
+            if (have_cur) {
                 issue(slot);
                 ++issued;
             }
-            const bool item_end = (cc.page + 1 >= it.pe);
-            if (item_end) {
-                float lt = l;
-                lt += __shfl_xor_sync(0xffffffffu, lt, 1);
-                lt += __shfl_xor_sync(0xffffffffu, lt, 2);
-                // lane holds O[row qrow][dims 8nt + qcol, +1]; stage through the
-                // (drained) scratch-free path: write rows directly.
-                const bool rv = qrow < GROUP;
-                const int qh = it.head * GROUP + qrow;
-                if (it.nsplit == 1) {
-                    if (rv) {
-                        const float inv = lt > 0.f ? 1.f / lt : 0.f;
-                        __nv_bfloat16* dst = p.out + (static_cast<int64_t>(it.r) * p.n_q + qh) * kD;
-#pragma unroll
-                        for (int nt = 0; nt < 16; ++nt) {
-                            *reinterpret_cast<uint32_t*>(dst + nt * 8 + qcol) =
-                                pack_bf16(oacc[nt][0] * inv, oacc[nt][1] * inv);
-                        }
-                        if (p.lse != nullptr && (lane & 3) == 0) {
-                            p.lse[static_cast<int64_t>(it.r) * p.n_q + qh] =
-                                lt > 0.f ? (m + __log2f(lt)) / kLog2e : -INFINITY;
-                        }
-                    }
-                } else {
-                    if (rv) {
-                        const int64_t slotp = static_cast<int64_t>(it.g) * p.n_q + qh;
-                        float* dst = p.part_o + slotp * kD;
-#pragma unroll
-                        for (int nt = 0; nt < 16; ++nt) {
-                            __stcg(reinterpret_cast<float2*>(dst + nt * 8 + qcol),
-                                   make_float2(oacc[nt][0], oacc[nt][1]));
-                        }
-                        if ((lane & 3) == 0) __stcg(p.part_ml + slotp, make_float2(m, lt));
-                    }
-                    if (arrive_last(p, it, lane)) {
-                        for (int gh = 0; gh < GROUP; ++gh) merge_row(p, it.r, it.head * GROUP + gh, lane);
-                    }
-                }
+            if (pend) {  // the partial's stores have had a page to drain
+                announce<GROUP>(p, pend_r, pend_head, pend_ns, lane);
+                pend = false;
             }
-            cursor_next(p, cc, stride);
+            if (!qn_ready && citem < pushed) {  // prefetch the next item's q
+                qn.load(p, ring[citem % kRing], lane);
+                qn_ready = true;
+            }
+        }
+        if (acc.finish(p, cd, lane)) {
+            pend = true;
+            pend_r = cd.r;
+            pend_head = cd.head;
+            pend_ns = cd.nsplit;
+        }
+    }
+    if (pend) announce<GROUP>(p, pend_r, pend_head, pend_ns, lane);
+
+    // last warp out re-arms the work counters of this launch parity
+    if (lane == 0) {
+        const uint32_t done = atomicAdd(p.work + 1, 1u);
+        if (done == static_cast<uint32_t>(p.total_warps) - 1u) {
+            p.work[0] = 0u;
+            p.work[1] = 0u;
         }
     }
 }
 
 // ------------------------------------------------------------- launcher
-template <int NW, int S, int GROUP>
-struct Launch {
-    static constexpr int kSmem = NW * (S * kStageBytes + 128);
-    static cudaError_t configure() {
-        return cudaFuncSetAttribute(decode_attn_kernel<NW, S, GROUP>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    }
-    static cudaError_t occupancy(int* blocks) {
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, decode_attn_kernel<NW, S, GROUP>,
-                                                             NW * 32, kSmem);
-    }
-    static cudaError_t run(const Params& p, int grid, cudaStream_t st) {
-        decode_attn_kernel<NW, S, GROUP><<<grid, NW * 32, kSmem, st>>>(p);
-        return cudaGetLastError();
-    }
-};
-
 constexpr int kNW = 4;
 constexpr int kStages = 3;
 
 template <int GROUP>
-cudaError_t dispatch_group(bool query, int* blocks, const Params* p, int grid, cudaStream_t st) {
-    using L = Launch<kNW, kStages, GROUP>;
-    static bool configured = false;  // attribute set is idempotent; racing is harmless
+struct Launch {
+    static constexpr int kSmem = kNW * (kStages * kStageBytes + 256);
+    static cudaError_t configure() {
+        return cudaFuncSetAttribute(decode_attn_kernel<kNW, kStages, GROUP>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    }
+    static cudaError_t occupancy(int* blocks) {
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, decode_attn_kernel<kNW, kStages, GROUP>,
+                                                             kNW * 32, kSmem);
+    }
+    static cudaError_t run(const Params& p, int grid, bool pdl, cudaStream_t st) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kNW * 32);
+        cfg.dynamicSmemBytes = kSmem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = pdl ? 1 : 0;
+        return cudaLaunchKernelEx(&cfg, decode_attn_kernel<kNW, kStages, GROUP>, p);
+    }
+};
+
+template <int GROUP>
+cudaError_t dispatch_group(bool query, int* blocks, const Params* p, int grid, bool pdl, cudaStream_t st) {
+    static bool configured = false;  // attribute set is idempotent; a race is harmless
     if (!configured) {
-        cudaError_t e = L::configure();
+        cudaError_t e = Launch<GROUP>::configure();
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    if (query) return L::occupancy(blocks);
-    return L::run(*p, grid, st);
+    if (query) return Launch<GROUP>::occupancy(blocks);
+    return Launch<GROUP>::run(*p, grid, pdl, st);
 }
 
-cudaError_t dispatch(int group, bool query, int* blocks, const Params* p, int grid, cudaStream_t st) {
+cudaError_t dispatch(int group, bool query, int* blocks, const Params* p, int grid, bool pdl,
+                     cudaStream_t st) {
     switch (group) {
-        case 1: return dispatch_group<1>(query, blocks, p, grid, st);
-        case 2: return dispatch_group<2>(query, blocks, p, grid, st);
-        case 4: return dispatch_group<4>(query, blocks, p, grid, st);
-        case 5: return dispatch_group<5>(query, blocks, p, grid, st);
-        case 8: return dispatch_group<8>(query, blocks, p, grid, st);
+        case 1: return dispatch_group<1>(query, blocks, p, grid, pdl, st);
+        case 2: return dispatch_group<2>(query, blocks, p, grid, pdl, st);
+        case 4: return dispatch_group<4>(query, blocks, p, grid, pdl, st);
+        case 5: return dispatch_group<5>(query, blocks, p, grid, pdl, st);
+        case 8: return dispatch_group<8>(query, blocks, p, grid, pdl, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -706,7 +731,7 @@ cudaError_t dispatch(int group, bool query, int* blocks, const Params* p, int gr
 int attn_warps_per_cta() { return kNW; }
 
 cudaError_t attn_occupancy(int group, int* blocks_per_sm) {
-    return dispatch(group, true, blocks_per_sm, nullptr, 0, nullptr);
+    return dispatch(group, true, blocks_per_sm, nullptr, 0, false, nullptr);
 }
 
 cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st) {
@@ -717,14 +742,12 @@ cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st) {
     p.page_bytes = a.page_bytes;
     p.layer_off = a.layer_off;
     p.v_off = a.v_off;
-    p.seq_lens = a.seq_lens;
-    p.page_indptr = a.page_indptr;
-    p.page_indices = a.page_indices;
-    p.split_indptr = a.split_indptr;
-    p.item_tab = reinterpret_cast<const int2*>(a.item_tab);
+    p.gdesc = a.gdesc;
+    p.split_base = a.split_base;
     p.num_items = a.num_items;
     p.n_kv = a.n_kv;
     p.n_q = a.n_q;
+    p.total_warps = a.grid * kNW;
     p.k_new = static_cast<const __nv_bfloat16*>(a.k_new);
     p.v_new = static_cast<const __nv_bfloat16*>(a.v_new);
     p.out = static_cast<__nv_bfloat16*>(a.out);
@@ -732,9 +755,10 @@ cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st) {
     p.part_o = a.part_o;
     p.part_ml = reinterpret_cast<float2*>(a.part_ml);
     p.sem = a.sem;
+    p.work = a.work;
     p.scale_log2 = a.sm_scale * kLog2e;
     if (p.num_items <= 0) return cudaSuccess;
-    return dispatch(a.group, false, nullptr, &p, a.grid, st);
+    return dispatch(a.group, false, nullptr, &p, a.grid, a.pdl, st);
 }
 
 }  // namespace asv

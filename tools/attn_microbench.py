@@ -58,6 +58,8 @@ def run(n_q, n_kv, L, seq_lens, iters=20, warmup=3, num_workers=None, seed=0):
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--case", default=None)
     a = ap.parse_args()
     rng = np.random.default_rng(1)
     cases = {
@@ -69,6 +71,8 @@ if __name__ == "__main__":
         "mha_b1_128k": (32, 32, 4, [131072]),
     }
     for name, (nq, nkv, L, seq) in cases.items():
-        r = run(nq, nkv, L, seq, iters=a.iters)
+        if a.case and a.case != name:
+            continue
+        r = run(nq, nkv, L, seq, iters=a.iters, warmup=a.warmup)
         r["case"] = name
         print(json.dumps(r), flush=True)
