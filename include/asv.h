@@ -75,6 +75,8 @@ typedef struct asv_attn_plan {
     int32_t off_desc;       /* int32 offset of the G split descriptors (40 words each,
                                sorted longest first: the dynamic schedule is LPT) */
     int32_t off_split_base; /* int32 offset of split_base[b+1] (partial slots per request) */
+    int32_t off_merge;      /* int32 offset of the requests split more than once */
+    int32_t n_merge;        /* their count (rows of the merge kernel = n_merge * n_h) */
     int32_t total_int32;    /* size of the plan buffer in int32 */
     int32_t max_item_pages; /* largest work item, pages (<= 32) */
 } asv_attn_plan;
@@ -117,9 +119,10 @@ typedef struct asv_attn_args {
     int32_t pdl;            /* 1: programmatic dependent launch (overlap with the previous kernel) */
 } asv_attn_args;
 
-/* K1+K2+K3: paged split-KV decode attention, in-kernel split merge (last-arriving
- * warp per (request, kv head)), fused KV append.  Replaces the attention term of
- * iteration_latency (cost_model.hpp:112-135). */
+/* K1+K2+K3: paged split-KV decode attention with fused KV append (K1+K3), then the
+ * log-sum-exp merge of split requests (K2), chained with programmatic dependent
+ * launch when pdl = 1.  Replaces the attention term of iteration_latency
+ * (cost_model.hpp:112-135). */
 int asv_decode_attention(const asv_attn_shape* shape, const asv_attn_args* args, void* stream);
 
 /* ------------------------------------------------------------------------ */

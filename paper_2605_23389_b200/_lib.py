@@ -33,6 +33,8 @@ class AttnPlan(C.Structure):
         ("num_workers", C.c_int32),
         ("off_desc", C.c_int32),
         ("off_split_base", C.c_int32),
+        ("off_merge", C.c_int32),
+        ("n_merge", C.c_int32),
         ("total_int32", C.c_int32),
         ("max_item_pages", C.c_int32),
     ]
@@ -73,6 +75,11 @@ SIGNATURES = [
     ("asv_attn_workspace_bytes", C.c_size_t, [C.POINTER(AttnShape), C.c_int32, C.c_int32]),
     ("asv_attn_workspace_init", C.c_int, [C.c_void_p, C.c_size_t, C.c_void_p]),
     ("asv_decode_attention", C.c_int, [C.POINTER(AttnShape), C.POINTER(AttnArgs), C.c_void_p]),
+    ("asv_run_config_jsonl", C.c_int,
+     [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
+    ("asv_dfs_batch", C.c_int,
+     [C.POINTER(C.c_int64), C.c_int64, C.c_int64, C.c_int64, C.POINTER(C.c_int64),
+      C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
 ]
 
 _lib = None

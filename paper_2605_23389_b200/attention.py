@@ -90,7 +90,7 @@ class PagedDecodeAttention:
             raise ValueError("empty batch")
         nw = int(num_workers) if num_workers is not None else self.num_workers
         npages = int(((seq + 15) // 16).sum())
-        cap = 40 * (npages // 2 + b + 1) + b + 8  # every split holds >= 2 pages or a whole request
+        cap = 40 * (npages // 2 + b + 1) + 2 * b + 8  # every split holds >= 2 pages or a whole request
         host = torch.empty(cap, dtype=torch.int32, pin_memory=True)
         desc = _lib.AttnPlan()
         hp = C.cast(C.c_void_p(host.data_ptr()), C.POINTER(C.c_int32))

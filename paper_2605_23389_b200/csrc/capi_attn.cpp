@@ -122,8 +122,6 @@ int asv_attn_plan_build(const asv_attn_shape* shape, int32_t batch, const int32_
     if (num_workers < 1) return fail(ASV_ERR_INVALID, "num_workers must be >= 1");
     const int n_kv = shape->num_kv_heads;
     std::vector<int32_t> npages(static_cast<size_t>(batch));
-    int64_t total_pages = 0;
-    int32_t max_pages = 0;
     for (int r = 0; r < batch; ++r) {
         const int32_t s = seq_lens[r];
         if (s < 1) return fail(ASV_ERR_INVALID, "prefix lengths must be >= 1");
@@ -132,8 +130,6 @@ int asv_attn_plan_build(const asv_attn_shape* shape, int32_t batch, const int32_
             return fail(ASV_ERR_INVALID, "page table shorter than ceil(seq_len/16) for request " +
                                              std::to_string(r));
         npages[static_cast<size_t>(r)] = np;
-        total_pages += np;
-        max_pages = std::max(max_pages, np);
     }
     if (page_indptr[0] != 0) return fail(ASV_ERR_INVALID, "page_indptr[0] must be 0");
 
@@ -168,8 +164,11 @@ int asv_attn_plan_build(const asv_attn_shape* shape, int32_t batch, const int32_
     for (int32_t v : best_ns) total_splits += v;
     const int64_t P = page_indptr[batch];
     const int64_t off_desc = 0;
+    int32_t n_merge = 0;
+    for (int32_t v : best_ns) n_merge += v > 1 ? 1 : 0;
     const int64_t off_split = off_desc + total_splits * kDescWords;
-    const int64_t need = off_split + batch + 1;
+    const int64_t off_merge = off_split + batch + 1;
+    const int64_t need = off_merge + n_merge;
     if (need > plan_cap) return fail(ASV_ERR_INVALID, "plan buffer too small: need " + std::to_string(need));
 
     asv_attn_plan pl{};
@@ -180,7 +179,12 @@ int asv_attn_plan_build(const asv_attn_shape* shape, int32_t batch, const int32_
     pl.num_workers = num_workers;
     pl.off_desc = static_cast<int32_t>(off_desc);
     pl.off_split_base = static_cast<int32_t>(off_split);
+    pl.off_merge = static_cast<int32_t>(off_merge);
+    pl.n_merge = n_merge;
     pl.total_int32 = static_cast<int32_t>(need);
+    for (int r = 0, k = 0; r < batch; ++r) {
+        if (best_ns[static_cast<size_t>(r)] > 1) plan_buf[off_merge + k++] = r;
+    }
     pl.max_item_pages = 0;
 
     // split_base: partial slots are request-major (the merge walks them)
@@ -271,6 +275,14 @@ int asv_decode_attention(const asv_attn_shape* shape, const asv_attn_args* a, vo
     L.gdesc = a->plan_dev + pl.off_desc;
     L.split_base = a->plan_dev + pl.off_split_base;
     L.pdl = a->pdl != 0;
+    L.merge_reqs = a->plan_dev + pl.off_merge;
+    L.n_merge = pl.n_merge;
+    {
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        L.sms = sms > 0 ? sms : 148;
+    }
     L.num_items = pl.num_items;
     L.n_kv = n_kv;
     L.n_q = n_q;

@@ -19,9 +19,9 @@
 //    fma.rn.f32.bf16 (one FHFMA per MAC, no converts), warp-shuffle softmax;
 //  * GQA (group 2..8): mma.sync.m16n8k16 bf16 on the query group (rows = heads),
 //    S fragment reused in registers as the PV A operand;
-//  * split partials merge in-kernel: a warp publishes its partial, announces it
-//    with a release atomic one page later (so the store round trip is hidden),
-//    and the last arrival per (request, kv head) merges (log-sum-exp);
+//  * split requests publish (o, m, l) partials; a small merge kernel (K2), chained
+//    with programmatic dependent launch, combines them (log-sum-exp) — the
+//    streaming kernel itself carries no fences or semaphores;
 //  * the owner of a request's last split appends the step's K/V row at position
 //    seq_len (prefix_len += 1, cluster_sim.hpp:443-447);
 //  * programmatic dependent launch: the KV prefetch of layer l+1 overlaps layer
@@ -222,49 +222,6 @@ __device__ __forceinline__ void write_final_row(const Params& p, int r, int qh, 
     }
 }
 
-// Merge all split partials of (r, qh); every lane owns dims 4*lane .. 4*lane+3.
-__device__ __forceinline__ void merge_row(const Params& p, int r, int qh, int lane) {
-    const int s0 = __ldg(p.split_base + r);
-    const int ns = __ldg(p.split_base + r + 1) - s0;
-    float M = -INFINITY;
-    for (int s = 0; s < ns; ++s) {
-        const float2 ml = __ldcg(p.part_ml + static_cast<int64_t>(s0 + s) * p.n_q + qh);
-        M = fmaxf(M, ml.x);
-    }
-    float o[4] = {0.f, 0.f, 0.f, 0.f};
-    float L = 0.f;
-    for (int s = 0; s < ns; ++s) {
-        const int64_t slot = static_cast<int64_t>(s0 + s) * p.n_q + qh;
-        const float2 ml = __ldcg(p.part_ml + slot);
-        const float w = (ml.x == -INFINITY) ? 0.f : exp2f(ml.x - M);
-        const float4 v = __ldcg(reinterpret_cast<const float4*>(p.part_o + slot * kD) + lane);
-        o[0] += w * v.x;
-        o[1] += w * v.y;
-        o[2] += w * v.z;
-        o[3] += w * v.w;
-        L += w * ml.y;
-    }
-    write_final_row(p, r, qh, lane, o, M, L);
-}
-
-// Announce a published partial (release) and, on the last arrival for this
-// (request, kv head), merge every query head of the group.
-template <int GROUP>
-__device__ __forceinline__ void announce(const Params& p, int r, int head, int nsplit, int lane) {
-    __syncwarp();
-    int prev = 0;
-    if (lane == 0) {
-        int32_t* s = p.sem + static_cast<int64_t>(r) * p.n_kv + head;
-        asm volatile("atom.release.gpu.global.add.s32 %0, [%1], 1;" : "=r"(prev) : "l"(s) : "memory");
-        if (prev == nsplit - 1) *s = 0;  // re-arm for the next launch (stream-ordered)
-    }
-    prev = __shfl_sync(0xffffffffu, prev, 0);
-    if (prev == nsplit - 1) {
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        for (int gh = 0; gh < GROUP; ++gh) merge_row(p, r, head * GROUP + gh, lane);
-    }
-}
-
 // KV append (K3): lanes 0-15 write the K row, 16-31 the V row (16 B each, swizzled).
 __device__ __forceinline__ void append_row(const Params& p, const Desc& d, int lane) {
     if (p.k_new == nullptr || d.append_phys < 0) return;
@@ -408,7 +365,7 @@ struct Acc<1> {
             }
         }
     }
-    // returns true when a partial was published (announce pending)
+    // returns true when a partial was published for the merge kernel
     __device__ __forceinline__ bool finish(const Params& p, const Desc& d, int lane) {
         float lt = l;
 #pragma unroll
@@ -616,9 +573,6 @@ decode_attn_kernel(const Params p) {
     bool qn_ready = false;
     Desc cd;            // consumer's current item
     int cpage = 0;
-    // deferred partial announcement
-    bool pend = false;
-    int pend_r = 0, pend_head = 0, pend_ns = 0;
 
     while (citem < pushed) {
         // ---- start the next item (the producer pushed it >= 1 page ago or just now)
@@ -644,23 +598,13 @@ decode_attn_kernel(const Params p) {
                 issue(slot);
                 ++issued;
             }
-            if (pend) {  // the partial's stores have had a page to drain
-                announce<GROUP>(p, pend_r, pend_head, pend_ns, lane);
-                pend = false;
-            }
             if (!qn_ready && citem < pushed) {  // prefetch the next item's q
                 qn.load(p, ring[citem % kRing], lane);
                 qn_ready = true;
             }
         }
-        if (acc.finish(p, cd, lane)) {
-            pend = true;
-            pend_r = cd.r;
-            pend_head = cd.head;
-            pend_ns = cd.nsplit;
-        }
+        acc.finish(p, cd, lane);  // final row (single split) or partial for the merge kernel
     }
-    if (pend) announce<GROUP>(p, pend_r, pend_head, pend_ns, lane);
 
     // last warp out re-arms the work counters of this launch parity
     if (lane == 0) {
@@ -669,6 +613,55 @@ decode_attn_kernel(const Params p) {
             p.work[0] = 0u;
             p.work[1] = 0u;
         }
+    }
+}
+
+// ============================================================ split merge (K2)
+// One warp per (request, query head) of every split request: log-sum-exp merge
+// of the partials the streaming kernel published.  Chained with PDL: the warps
+// park on griddepcontrol.wait until the streaming grid has completed (which
+// also makes its partial stores visible), so no fences or semaphores are needed.
+constexpr int kMergeWarps = 4;
+
+__global__ void __launch_bounds__(kMergeWarps * 32)
+merge_splits_kernel(const Params p, const int32_t* __restrict__ merge_reqs, int32_t rows) {
+    // let the next layer's streaming kernel start prefetching as soon as SMs free
+    // up; it cannot pass its own wait before this grid completes
+    grid_dep_launch();
+    grid_dep_wait();
+    const int lane = threadIdx.x & 31;
+    for (int row = blockIdx.x * kMergeWarps + (threadIdx.x >> 5); row < rows; row += gridDim.x * kMergeWarps) {
+        const int r = __ldg(merge_reqs + row / p.n_q);
+        const int qh = row % p.n_q;
+        const int s0 = __ldg(p.split_base + r);
+        const int ns = __ldg(p.split_base + r + 1) - s0;
+        const float2* ml = p.part_ml + static_cast<int64_t>(s0) * p.n_q + qh;
+        // max over splits, lane-parallel
+        float M = -INFINITY;
+        for (int s = lane; s < ns; s += 32) M = fmaxf(M, ml[static_cast<int64_t>(s) * p.n_q].x);
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+        float L = 0.f;
+        for (int s = lane; s < ns; s += 32) {
+            const float2 v = ml[static_cast<int64_t>(s) * p.n_q];
+            L += (v.x == -INFINITY) ? 0.f : exp2f(v.x - M) * v.y;
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
+        float o[4] = {0.f, 0.f, 0.f, 0.f};
+        const float4* po = reinterpret_cast<const float4*>(p.part_o + (static_cast<int64_t>(s0) * p.n_q + qh) * kD) + lane;
+        const int64_t stride4 = static_cast<int64_t>(p.n_q) * (kD / 4);
+#pragma unroll 4
+        for (int s = 0; s < ns; ++s) {
+            const float mx = ml[static_cast<int64_t>(s) * p.n_q].x;
+            const float w = (mx == -INFINITY) ? 0.f : exp2f(mx - M);
+            const float4 v = po[s * stride4];
+            o[0] += w * v.x;
+            o[1] += w * v.y;
+            o[2] += w * v.z;
+            o[3] += w * v.w;
+        }
+        write_final_row(p, r, qh, lane, o, M, L);
     }
 }
 
@@ -734,6 +727,24 @@ cudaError_t attn_occupancy(int group, int* blocks_per_sm) {
     return dispatch(group, true, blocks_per_sm, nullptr, 0, false, nullptr);
 }
 
+cudaError_t merge_launch(const Params& p, const int32_t* merge_reqs, int32_t n_merge, int sms, bool pdl,
+                         cudaStream_t st) {
+    const int32_t rows = n_merge * p.n_q;
+    if (rows <= 0) return cudaSuccess;
+    const int blocks = min((rows + kMergeWarps - 1) / kMergeWarps, 2 * sms);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(kMergeWarps * 32);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, merge_splits_kernel, p, merge_reqs, rows);
+}
+
 cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st) {
     Params p;
     p.q = static_cast<const __nv_bfloat16*>(a.q);
@@ -758,7 +769,9 @@ cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st) {
     p.work = a.work;
     p.scale_log2 = a.sm_scale * kLog2e;
     if (p.num_items <= 0) return cudaSuccess;
-    return dispatch(a.group, false, nullptr, &p, a.grid, a.pdl, st);
+    cudaError_t e = dispatch(a.group, false, nullptr, &p, a.grid, a.pdl, st);
+    if (e != cudaSuccess) return e;
+    return merge_launch(p, a.merge_reqs, a.n_merge, a.sms, a.pdl, st);
 }
 
 }  // namespace asv

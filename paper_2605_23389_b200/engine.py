@@ -1,0 +1,47 @@
+"""Python face of the host-side decision path (C++ behind include/asv.h).
+
+Mirrors the reference's entry points on the decode path:
+  * run_config_jsonl  ~ `prefixsim run --config X` (experiment_from_json ->
+    run_experiment -> log_to_jsonl; reference prefixsim_main.cpp:66-111,
+    io.hpp:184-254, io.hpp:279-323), virtual-clock mode;
+  * dfs_batch         ~ density_first_search on a pool snapshot
+    (reference batch_gen.hpp:126-210); member order = page-table order.
+Errors map to the reference's exception types: ValueError for
+std::invalid_argument, AssertionError for std::logic_error, RuntimeError for
+std::runtime_error, with the same messages.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+
+import numpy as np
+
+from . import _lib
+
+
+def run_config_jsonl(config, policy: str | None = None) -> str:
+    """Run one experiment config (dict or JSON text) and return the schema-1 JSONL log."""
+    text = config if isinstance(config, str) else json.dumps(config)
+    out = C.c_void_p()
+    n = C.c_int64(0)
+    h = _lib.lib()
+    _lib.check(h.asv_run_config_jsonl(text.encode(), policy.encode() if policy else None,
+                                      C.byref(out), C.byref(n)))
+    try:
+        return C.string_at(out.value, n.value).decode()
+    finally:
+        h.asv_free(out)
+
+
+def dfs_batch(residents, b_max: int, k_min: int):
+    """residents: [(id, prefix_len, kv_blocks)] in insertion order -> (member ids, total_blocks)."""
+    arr = np.ascontiguousarray(np.asarray(residents, dtype=np.int64).reshape(-1, 3))
+    n = arr.shape[0]
+    ids = np.zeros(max(n, 1), dtype=np.int64)
+    cnt = C.c_int64(0)
+    tot = C.c_int64(0)
+    p64 = lambda a: a.ctypes.data_as(C.POINTER(C.c_int64))  # noqa: E731
+    _lib.check(_lib.lib().asv_dfs_batch(p64(arr), n, int(b_max), int(k_min), p64(ids),
+                                         C.byref(cnt), C.byref(tot)))
+    return ids[:cnt.value].tolist(), int(tot.value)

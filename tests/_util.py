@@ -143,3 +143,50 @@ def numpy_attention(n_q, n_kv, num_layers, layer, q_bits, pool, seq_lens, indptr
                 out[r, h] = p @ V / p.sum()
                 lse[r, h] = m + np.log(p.sum())
     return out, lse
+
+
+class RefEngine:
+    """The UNMODIFIED reference decision path (oracle/_ref, built from /root/reference) — checker only."""
+
+    def __init__(self):
+        if not os.path.exists(REF_SO):
+            raise RuntimeError("oracle/_ref/libprefixsim_ref.so missing (reference not built)")
+        self.h = C.CDLL(REF_SO)
+        self.h.ref_run_config_jsonl.restype = C.c_int
+        self.h.ref_run_config_jsonl.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p),
+                                                C.POINTER(C.c_longlong), C.POINTER(C.c_double),
+                                                C.POINTER(C.c_longlong)]
+        for fn in ("ref_dfs_batch", "ref_dfs_flat_oracle"):
+            f = getattr(self.h, fn)
+            f.restype = C.c_int
+            f.argtypes = [C.POINTER(C.c_longlong), C.c_longlong, C.c_longlong, C.c_longlong,
+                          C.POINTER(C.c_longlong), C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]
+        self.h.ref_free.argtypes = [C.c_void_p]
+        self.h.ref_last_error.restype = C.c_char_p
+
+    def run_config_jsonl(self, config, policy=None):
+        import json as _json
+        text = config if isinstance(config, str) else _json.dumps(config)
+        out = C.c_void_p()
+        n = C.c_longlong(0)
+        secs = C.c_double(0)
+        its = C.c_longlong(0)
+        rc = self.h.ref_run_config_jsonl(text.encode(), policy.encode() if policy else None,
+                                         C.byref(out), C.byref(n), C.byref(secs), C.byref(its))
+        if rc != 0:
+            raise RuntimeError(self.h.ref_last_error().decode())
+        try:
+            return C.string_at(out.value, n.value).decode(), secs.value, its.value
+        finally:
+            self.h.ref_free(out)
+
+    def dfs(self, residents, b_max, k_min, flat_oracle=False):
+        arr = np.ascontiguousarray(np.asarray(residents, dtype=np.int64).reshape(-1, 3))
+        n = arr.shape[0]
+        ids = np.zeros(max(n, 1), dtype=np.int64)
+        cnt = C.c_longlong(0)
+        tot = C.c_longlong(0)
+        p = lambda a: a.ctypes.data_as(C.POINTER(C.c_longlong))  # noqa: E731
+        f = self.h.ref_dfs_flat_oracle if flat_oracle else self.h.ref_dfs_batch
+        assert f(p(arr), n, int(b_max), int(k_min), p(ids), C.byref(cnt), C.byref(tot)) == 0
+        return ids[:cnt.value].tolist(), int(tot.value)
