@@ -138,6 +138,69 @@ int asv_run_config_jsonl(const char* config_json, const char* policy_override, c
                          int64_t* out_len);
 void asv_free(void* p);
 
+/* ------------------------------------------------------------------------ */
+/* Decode engine on the GPU: the reference engine's decisions (virtual clock, */
+/* bit-exact) executed for real — KV moves as copies, every iteration as      */
+/* page-table build + L decode-attention launches — with measured times.      */
+/* Replaces Simulation::run's priced path (cluster_sim.hpp:131-160, 437-569). */
+/* ------------------------------------------------------------------------ */
+typedef struct asv_engine_opts {
+    int32_t decode_device;      /* CUDA device of the decode GPU */
+    int32_t prefetch_device;    /* partner holding the candidate buffers; == decode_device: single GPU */
+    int32_t num_q_heads;        /* attention shape; num_kv_heads*128*2*2*num_layers must equal */
+    int32_t num_kv_heads;       /* the config model's kv_bytes_per_token (bytes moved == reference) */
+    int32_t num_layers;
+    int32_t execute_transfers;  /* 1: real KV moves from/to the pinned host pool (e2e); 0: KV resident */
+    int64_t host_pool_bytes;    /* pinned host arena; request KV pages alias into it (synthetic data) */
+    int64_t exec_begin;         /* first iteration executed on the GPU (earlier: decisions only) */
+    int64_t exec_end;           /* one past the last executed iteration (-1: all) */
+    int64_t timed_begin;        /* first iteration of the timed window (>= exec_begin) */
+    int32_t shard_index;        /* data-parallel shard of the trace: requests i with */
+    int32_t shard_count;        /* i % shard_count == shard_index (1: whole trace) */
+    int32_t pdl;                /* programmatic dependent launch between layer kernels */
+    int32_t run_ahead;          /* max iterations the host may run ahead of the GPU (ring depth) */
+    int64_t copy_begin;         /* first iteration whose boundary KV moves are executed (<= exec_begin:
+                                   lets prefetches issued before the executed span reach steady state) */
+} asv_engine_opts;
+
+/* transfer kinds for the per-kind byte counters */
+#define ASV_XFER_PREFILL_OFFLOAD 0
+#define ASV_XFER_BATCH_PREFETCH 1
+#define ASV_XFER_STRAY_PREFETCH 2
+#define ASV_XFER_ADMIT 3
+#define ASV_XFER_EVICT 4
+#define ASV_XFER_SPILL 5
+#define ASV_XFER_FLUSH 6
+#define ASV_XFER_KINDS 7
+
+typedef struct asv_engine_stats {
+    int64_t iterations_total;     /* decode iterations of the whole run (log) */
+    int64_t iterations_timed;     /* iterations inside the timed window */
+    int64_t tokens_timed;         /* sum of batch sizes inside the window */
+    double window_ms;             /* GPU time of the window (CUDA events, compute stream) */
+    double attn_ms;               /* sum of attention-kernel time inside the window */
+    int64_t attn_bytes;           /* algorithmic K/V + q + out + index bytes inside the window */
+    int64_t attn_launches;        /* kernel launches inside the window */
+    int64_t h2d_bytes;            /* physical bytes moved inside the window */
+    int64_t d2h_bytes;
+    int64_t p2p_bytes;
+    double h2d_busy_ms;           /* copy-engine busy time of those moves (events) */
+    double p2p_busy_ms;
+    int64_t logical_bytes[ASV_XFER_KINDS]; /* whole run, == sum of the reference's TransferRecord.bytes */
+    int64_t logical_count[ASV_XFER_KINDS];
+    double virtual_decode_tok_s;  /* decode_throughput of the virtual-clock log */
+    double host_decide_ms;        /* host time spent in the decision path (engine + planning) */
+    int64_t max_batch;
+    int64_t pages_decode;         /* physical page pools */
+    int64_t pages_prefetch;
+    double bubble_ms_timed;       /* sum of per-iteration bubble (virtual) inside the window */
+    int64_t kernel_launches_timed;/* our kernels launched inside the window (attention + merge) */
+    double virtual_window_ms;     /* reference-clock duration of the same window */
+} asv_engine_stats;
+
+int asv_engine_run(const char* config_json, const char* policy_override, const asv_engine_opts* opts,
+                   asv_engine_stats* stats);
+
 /* Density-first search on a pool snapshot (batch_gen.hpp:126-210).
  * residents: n x {id, prefix_len, kv_blocks} in insertion order (all inserted at t=0).
  * Writes the batch member ids in page-table order; returns count via *n_out (0 = no batch). */

@@ -60,6 +60,65 @@ class AttnArgs(C.Structure):
     ]
 
 
+class EngineOpts(C.Structure):
+    _fields_ = [
+        ("decode_device", C.c_int32),
+        ("prefetch_device", C.c_int32),
+        ("num_q_heads", C.c_int32),
+        ("num_kv_heads", C.c_int32),
+        ("num_layers", C.c_int32),
+        ("execute_transfers", C.c_int32),
+        ("host_pool_bytes", C.c_int64),
+        ("exec_begin", C.c_int64),
+        ("exec_end", C.c_int64),
+        ("timed_begin", C.c_int64),
+        ("shard_index", C.c_int32),
+        ("shard_count", C.c_int32),
+        ("pdl", C.c_int32),
+        ("run_ahead", C.c_int32),
+        ("copy_begin", C.c_int64),
+    ]
+
+
+XFER_KINDS = ["prefill_offload", "batch_prefetch", "stray_prefetch", "admit", "evict", "spill", "flush"]
+
+
+class EngineStats(C.Structure):
+    _fields_ = [
+        ("iterations_total", C.c_int64),
+        ("iterations_timed", C.c_int64),
+        ("tokens_timed", C.c_int64),
+        ("window_ms", C.c_double),
+        ("attn_ms", C.c_double),
+        ("attn_bytes", C.c_int64),
+        ("attn_launches", C.c_int64),
+        ("h2d_bytes", C.c_int64),
+        ("d2h_bytes", C.c_int64),
+        ("p2p_bytes", C.c_int64),
+        ("h2d_busy_ms", C.c_double),
+        ("p2p_busy_ms", C.c_double),
+        ("logical_bytes", C.c_int64 * 7),
+        ("logical_count", C.c_int64 * 7),
+        ("virtual_decode_tok_s", C.c_double),
+        ("host_decide_ms", C.c_double),
+        ("max_batch", C.c_int64),
+        ("pages_decode", C.c_int64),
+        ("pages_prefetch", C.c_int64),
+        ("bubble_ms_timed", C.c_double),
+        ("kernel_launches_timed", C.c_int64),
+        ("virtual_window_ms", C.c_double),
+    ]
+
+    def as_dict(self):
+        d = {}
+        for name, _ in self._fields_:
+            v = getattr(self, name)
+            if name in ("logical_bytes", "logical_count"):
+                v = {k: int(v[i]) for i, k in enumerate(XFER_KINDS)}
+            d[name] = v
+        return d
+
+
 # (name, restype, argtypes) for every symbol include/asv.h declares
 SIGNATURES = [
     ("asv_last_error", C.c_char_p, []),
@@ -77,6 +136,8 @@ SIGNATURES = [
     ("asv_decode_attention", C.c_int, [C.POINTER(AttnShape), C.POINTER(AttnArgs), C.c_void_p]),
     ("asv_run_config_jsonl", C.c_int,
      [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
+    ("asv_engine_run", C.c_int,
+     [C.c_char_p, C.c_char_p, C.POINTER(EngineOpts), C.POINTER(EngineStats)]),
     ("asv_dfs_batch", C.c_int,
      [C.POINTER(C.c_int64), C.c_int64, C.c_int64, C.c_int64, C.POINTER(C.c_int64),
       C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),

@@ -45,3 +45,39 @@ def dfs_batch(residents, b_max: int, k_min: int):
     _lib.check(_lib.lib().asv_dfs_batch(p64(arr), n, int(b_max), int(k_min), p64(ids),
                                          C.byref(cnt), C.byref(tot)))
     return ids[:cnt.value].tolist(), int(tot.value)
+
+
+def load_config(path: str, root: str | None = None) -> dict:
+    """Read a config JSON; trace paths are resolved against `root` (default: the repo root)."""
+    import os
+    root = root or os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with open(path) as f:
+        cfg = json.load(f)
+    wl = cfg.get("workload", {})
+    if wl.get("kind") == "trace" and not os.path.isabs(wl.get("path", "")):
+        wl["path"] = os.path.join(root, wl["path"])
+    return cfg
+
+
+def engine_run(config, *, device: int = 0, prefetch_device: int | None = None,
+               num_q_heads: int, num_kv_heads: int, num_layers: int, execute_transfers: bool,
+               exec_begin: int = 0, exec_end: int = -1, timed_begin: int = 0, copy_begin: int | None = None,
+               host_pool_bytes: int = 8 << 30, shard_index: int = 0, shard_count: int = 1,
+               pdl: bool = True, run_ahead: int = 16, policy: str | None = None) -> dict:
+    """Run the decode engine on the GPU (asv_engine_run): reference decisions executed for real."""
+    text = config if isinstance(config, str) else json.dumps(config)
+    o = _lib.EngineOpts()
+    o.decode_device = device
+    o.prefetch_device = device if prefetch_device is None else prefetch_device
+    o.num_q_heads, o.num_kv_heads, o.num_layers = num_q_heads, num_kv_heads, num_layers
+    o.execute_transfers = 1 if execute_transfers else 0
+    o.host_pool_bytes = host_pool_bytes
+    o.exec_begin, o.exec_end, o.timed_begin = exec_begin, exec_end, timed_begin
+    o.copy_begin = exec_begin if copy_begin is None else copy_begin
+    o.shard_index, o.shard_count = shard_index, shard_count
+    o.pdl = 1 if pdl else 0
+    o.run_ahead = run_ahead
+    st = _lib.EngineStats()
+    _lib.check(_lib.lib().asv_engine_run(text.encode(), policy.encode() if policy else None,
+                                          C.byref(o), C.byref(st)))
+    return st.as_dict()
