@@ -138,6 +138,12 @@ int asv_run_config_jsonl(const char* config_json, const char* policy_override, c
                          int64_t* out_len);
 void asv_free(void* p);
 
+/* Same, for data-parallel shard `shard_index` of `shard_count` (request i of the
+ * trace belongs to shard i % shard_count) — what each rank of a multi-GPU run
+ * decides; no cross-shard communication exists on the decision path. */
+int asv_run_config_jsonl_shard(const char* config_json, const char* policy_override, int32_t shard_index,
+                               int32_t shard_count, char** out, int64_t* out_len);
+
 /* ------------------------------------------------------------------------ */
 /* Decode engine on the GPU: the reference engine's decisions (virtual clock, */
 /* bit-exact) executed for real — KV moves as copies, every iteration as      */

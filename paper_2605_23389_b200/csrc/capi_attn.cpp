@@ -38,17 +38,6 @@ int check_shape(const asv_attn_shape* s) {
     return ASV_OK;
 }
 
-// Split count so that ceil(n / ceil(n / ns)) == ns: every split non-empty.
-int normalize_splits(int n, int ns) {
-    ns = std::max(1, std::min(ns, n));
-    for (;;) {
-        const int chunk = (n + ns - 1) / ns;
-        const int ns2 = (n + chunk - 1) / chunk;
-        if (ns2 == ns) return ns;
-        ns = ns2;
-    }
-}
-
 struct OccCache {
     std::mutex mu;
     int dev[64][9] = {};
@@ -146,7 +135,7 @@ int asv_attn_plan_build(const asv_attn_shape* shape, int32_t batch, const int32_
         int max_item = 0;
         for (int r = 0; r < batch; ++r) {
             const int n = npages[static_cast<size_t>(r)];
-            const int k = normalize_splits(n, (n + c - 1) / c);
+            const int k = (n + c - 1) / c;  // balanced: every split gets floor/ceil(n/k) pages
             ns[static_cast<size_t>(r)] = k;
             const int chunk = (n + k - 1) / k;
             max_item = std::max(max_item, chunk);
@@ -193,10 +182,13 @@ int asv_attn_plan_build(const asv_attn_shape* shape, int32_t batch, const int32_
     for (int r = 0; r < batch; ++r) sb[r + 1] = sb[r] + best_ns[static_cast<size_t>(r)];
     // descriptors, counting-sorted by item size descending (stable: request, split)
     std::vector<int32_t> bucket(kMaxItemPages + 2, 0);
+    const auto span_of = [](int n, int k, int s) { return std::pair<int, int>{s * n / k, (s + 1) * n / k}; };
     for (int r = 0; r < batch; ++r) {
         const int n = npages[static_cast<size_t>(r)], k = best_ns[static_cast<size_t>(r)];
-        const int chunk = (n + k - 1) / k;
-        for (int s = 0; s < k; ++s) bucket[static_cast<size_t>(std::min(n, (s + 1) * chunk) - s * chunk)]++;
+        for (int s = 0; s < k; ++s) {
+            const auto [pb, pe] = span_of(n, k, s);
+            bucket[static_cast<size_t>(pe - pb)]++;
+        }
     }
     std::vector<int64_t> pos(kMaxItemPages + 2, 0);
     for (int sz = kMaxItemPages, acc = 0; sz >= 1; --sz) {
@@ -205,12 +197,11 @@ int asv_attn_plan_build(const asv_attn_shape* shape, int32_t batch, const int32_
     }
     for (int r = 0; r < batch; ++r) {
         const int n = npages[static_cast<size_t>(r)], k = best_ns[static_cast<size_t>(r)];
-        const int chunk = (n + k - 1) / k;
         const int32_t* pages = page_indices + page_indptr[r];
         const int32_t owned = page_indptr[r + 1] - page_indptr[r];
         const int app = seq_lens[r] / 16;
         for (int s = 0; s < k; ++s) {
-            const int pb = s * chunk, pe = std::min(n, pb + chunk);
+            const auto [pb, pe] = span_of(n, k, s);
             int32_t* d = plan_buf + off_desc + pos[static_cast<size_t>(pe - pb)]++ * kDescWords;
             d[0] = r;
             d[1] = sb[r] + s;

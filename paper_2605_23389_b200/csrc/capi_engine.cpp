@@ -14,6 +14,7 @@
 
 #include "../../include/asv.h"
 #include "asv_internal.h"
+#include "engine_internal.h"
 
 namespace asv {
 
@@ -39,6 +40,25 @@ char* dup_string(const std::string& s, int64_t* len) {
     return p;
 }
 
+std::vector<prefixsim::Request> load_workload(const prefixsim::ExperimentConfig& cfg) {
+    return cfg.workload.kind == prefixsim::WorkloadSpec::Kind::kTrace
+               ? prefixsim::ingest_trace(cfg.workload.trace_path, cfg.workload.trace_format).requests
+               : prefixsim::generate_synthetic(cfg.workload);
+}
+
+// Data-parallel shard of a trace: request i goes to shard i % count (arrival
+// times and order preserved; Simulation::run re-numbers ids to local indices,
+// cluster_sim.hpp:137-139, so global id = local * count + index).
+void shard_requests(std::vector<prefixsim::Request>& reqs, int32_t index, int32_t count) {
+    if (count < 1 || index < 0 || index >= count) throw std::invalid_argument("bad shard index/count");
+    if (count == 1) return;
+    std::vector<prefixsim::Request> mine;
+    for (std::size_t i = static_cast<std::size_t>(index); i < reqs.size(); i += static_cast<std::size_t>(count)) {
+        mine.push_back(reqs[i]);
+    }
+    reqs.swap(mine);
+}
+
 }  // namespace asv
 
 using namespace asv;
@@ -52,6 +72,23 @@ int asv_run_config_jsonl(const char* config_json, const char* policy_override, c
         if (policy_override != nullptr) cfg.sim.policy = prefixsim::policy_from_string(policy_override);
         const prefixsim::ExperimentResult r = prefixsim::run_experiment(cfg);
         *out = dup_string(prefixsim::log_to_jsonl(r.log), out_len);
+        return ASV_OK;
+    });
+}
+
+int asv_run_config_jsonl_shard(const char* config_json, const char* policy_override, int32_t shard_index,
+                               int32_t shard_count, char** out, int64_t* out_len) {
+    return guarded([&] {
+        if (config_json == nullptr || out == nullptr) throw std::invalid_argument("null config/out");
+        prefixsim::ExperimentConfig cfg = prefixsim::experiment_from_json(prefixsim::json::parse(config_json));
+        if (policy_override != nullptr) cfg.sim.policy = prefixsim::policy_from_string(policy_override);
+        std::vector<prefixsim::Request> reqs = load_workload(cfg);
+        shard_requests(reqs, shard_index, shard_count);
+        const prefixsim::CalibratedCostModel model =
+            cfg.has_calibration ? cfg.calibration
+                                : prefixsim::calibrate(prefixsim::reference_mixed_batch_anchors(), cfg.model).model;
+        const prefixsim::MetricsLog log = prefixsim::run(cfg.sim, std::move(reqs), model);
+        *out = dup_string(prefixsim::log_to_jsonl(log), out_len);
         return ASV_OK;
     });
 }

@@ -38,6 +38,7 @@
 
 #include "../../include/asv.h"
 #include "asv_internal.h"
+#include "engine_internal.h"
 
 namespace asv {
 
@@ -808,19 +809,8 @@ int engine_run(const char* config_json, const char* policy_override, const asv_e
         const prefixsim::CalibratedCostModel model =
             cfg.has_calibration ? cfg.calibration
                                 : prefixsim::calibrate(prefixsim::reference_mixed_batch_anchors(), cfg.model).model;
-        std::vector<prefixsim::Request> reqs =
-            cfg.workload.kind == prefixsim::WorkloadSpec::Kind::kTrace
-                ? prefixsim::ingest_trace(cfg.workload.trace_path, cfg.workload.trace_format).requests
-                : prefixsim::generate_synthetic(cfg.workload);
-        if (opts->shard_count > 1) {
-            std::vector<prefixsim::Request> mine;
-            for (std::size_t i = 0; i < reqs.size(); ++i) {
-                if (static_cast<int32_t>(i % static_cast<std::size_t>(opts->shard_count)) == opts->shard_index) {
-                    mine.push_back(reqs[i]);
-                }
-            }
-            reqs.swap(mine);
-        }
+        std::vector<prefixsim::Request> reqs = load_workload(cfg);
+        shard_requests(reqs, opts->shard_index, std::max(1, opts->shard_count));
         if (reqs.empty()) return fail(ASV_ERR_INVALID, "empty shard");
         prefixsim::Simulation sim(cfg.sim, model, reqs);
         GpuExecutor ex(*opts, cfg.sim, model.spec, reqs.size());

@@ -34,6 +34,20 @@ def run_config_jsonl(config, policy: str | None = None) -> str:
         h.asv_free(out)
 
 
+def run_config_jsonl_shard(config, shard_index: int, shard_count: int, policy: str | None = None) -> str:
+    """Schema-1 log of one data-parallel shard (request i -> shard i % shard_count)."""
+    text = config if isinstance(config, str) else json.dumps(config)
+    out = C.c_void_p()
+    n = C.c_int64(0)
+    h = _lib.lib()
+    _lib.check(h.asv_run_config_jsonl_shard(text.encode(), policy.encode() if policy else None,
+                                            int(shard_index), int(shard_count), C.byref(out), C.byref(n)))
+    try:
+        return C.string_at(out.value, n.value).decode()
+    finally:
+        h.asv_free(out)
+
+
 def dfs_batch(residents, b_max: int, k_min: int):
     """residents: [(id, prefix_len, kv_blocks)] in insertion order -> (member ids, total_blocks)."""
     arr = np.ascontiguousarray(np.asarray(residents, dtype=np.int64).reshape(-1, 3))
