@@ -8,8 +8,8 @@ lengths 1K-16K, bf16 KV, 1 B200") = configs/c2_7b_1024req.json.
 
 A step is one decode iteration of the engine: the reference-API scheduler's
 boundary decisions (virtual clock, bit-exact with the reference), the page-table
-build + upload, and attention over all 32 layers (one sm_100a decode kernel per
-layer, PDL-chained, plus the split-merge kernel).  Iterations [S, S+W) are
+build + upload, and attention over all 32 layers (one persistent sm_100a decode
+kernel per layer, PDL-chained; split merges happen in-kernel after a grid barrier).  Iterations [S, S+W) are
 warm-up, [S+W, S+W+K) are timed with CUDA events on the compute stream; S is a
 steady-state point of the trace (earlier iterations run decisions only).
 
@@ -272,9 +272,9 @@ def main():
         ewin = d.reduce([e2e["window_ms"]], "MAX")[0]
         etok = d.reduce([float(e2e["tokens_timed"])], "SUM")[0]
         e2e_obj = {"value": etok / (ewin / 1e3) if ewin > 0 else 0.0, "unit": "tokens/s",
-                   "h2d_bytes_per_step": int(e2e["h2d_bytes"] / max(1, e2e["iterations_timed"])),
-                   "d2h_bytes_per_step": int(e2e["d2h_bytes"] / max(1, e2e["iterations_timed"])),
-                   "p2p_bytes_per_step": int(e2e["p2p_bytes"] / max(1, e2e["iterations_timed"])),
+                   "h2d_bytes_per_step": int(e2e["h2d_bytes_window"] / max(1, e2e["iterations_timed"])),
+                   "d2h_bytes_per_step": int(e2e["d2h_bytes_window"] / max(1, e2e["iterations_timed"])),
+                   "p2p_bytes_per_step": int(e2e["p2p_bytes_window"] / max(1, e2e["iterations_timed"])),
                    "ms_per_step": ewin / max(1, e2e["iterations_timed"]),
                    "path": "asv_engine_run (C ABI) with KV moves from/to the pinned host pool"}
 
@@ -283,14 +283,15 @@ def main():
     launches = max(1, res["attn_launches"])
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": ncu_traffic(), "peak_source": peak_src,
-                "kernel": "decode_attn_kernel (+ merge_splits_kernel), per-layer launches",
+                "kernel": "decode_attn_kernel (split-KV + in-kernel merge), one launch per layer",
                 "alg_bytes_per_launch": res["attn_bytes"] / launches,
                 "avg_launch_us": res["attn_ms"] * 1e3 / launches,
                 "frac_of_8TBps": achieved / 8000.0}
     prefetch = None
     if e2e is not None:
-        h2d_gbps = e2e["h2d_bytes"] / (e2e["h2d_busy_ms"] * 1e-3) / 1e9 if e2e["h2d_busy_ms"] > 0 else None
-        p2p_gbps = e2e["p2p_bytes"] / (e2e["p2p_busy_ms"] * 1e-3) / 1e9 if e2e["p2p_busy_ms"] > 0 else None
+        h2d_gbps = ((e2e["h2d_bytes_window"] + e2e["d2h_bytes_window"]) / (e2e["h2d_busy_ms"] * 1e-3) / 1e9
+                    if e2e["h2d_busy_ms"] > 0 else None)
+        p2p_gbps = e2e["p2p_bytes_window"] / (e2e["p2p_busy_ms"] * 1e-3) / 1e9 if e2e["p2p_busy_ms"] > 0 else None
         prefetch = {"h2d_gbps": h2d_gbps, "h2d_roofline_gbps": 64.0, "p2p_gbps": p2p_gbps,
                     "p2p_roofline_gbps": 770.0, "h2d_busy_ms": e2e["h2d_busy_ms"],
                     "window_ms": e2e["window_ms"],
@@ -320,6 +321,9 @@ def main():
             "decode_attn_hbm_gbps": achieved, "kv_prefetch": prefetch,
             "virtual_clock_tok_s": res["virtual_decode_tok_s"],
             "bubble_ms_per_step_virtual": res["bubble_ms_timed"] / max(1, res["iterations_timed"]),
+            "bubble_measured": {"idle_frac": res["measured_idle_frac"],
+                                "ms_per_step": res["measured_bubble_ms"] / max(1, res["iterations_timed"]),
+                                "probe": "per-warp %globaltimer start/end of each step's layer-0 launch"},
             "host_decide_ms": res["host_decide_ms"],
             "logical_bytes_moved": res["logical_bytes"],
         }

@@ -117,6 +117,8 @@ typedef struct asv_attn_args {
     float sm_scale;         /* 1/sqrt(128) for the paper's Eq. 2 */
     uint32_t launch_index;  /* consecutive launches on one workspace must alternate parity */
     int32_t pdl;            /* 1: programmatic dependent launch (overlap with the previous kernel) */
+    uint64_t* warp_timestamps; /* optional [workers][2] device buffer: %globaltimer at each persistent
+                                  warp's start and end — the measured intra-iteration bubble */
 } asv_attn_args;
 
 /* K1+K2+K3: paged split-KV decode attention with fused KV append (K1+K3), then the
@@ -167,6 +169,8 @@ typedef struct asv_engine_opts {
     int32_t run_ahead;          /* max iterations the host may run ahead of the GPU (ring depth) */
     int64_t copy_begin;         /* first iteration whose boundary KV moves are executed (<= exec_begin:
                                    lets prefetches issued before the executed span reach steady state) */
+    int32_t pair_mode;          /* 1: separate candidate-buffer pool even when prefetch_device ==
+                                   decode_device (exercises the admit/evict copy path on one GPU) */
 } asv_engine_opts;
 
 /* transfer kinds for the per-kind byte counters */
@@ -187,7 +191,7 @@ typedef struct asv_engine_stats {
     double attn_ms;               /* sum of attention-kernel time inside the window */
     int64_t attn_bytes;           /* algorithmic K/V + q + out + index bytes inside the window */
     int64_t attn_launches;        /* kernel launches inside the window */
-    int64_t h2d_bytes;            /* physical bytes moved inside the window */
+    int64_t h2d_bytes;            /* physical bytes moved over the executed span */
     int64_t d2h_bytes;
     int64_t p2p_bytes;
     double h2d_busy_ms;           /* copy-engine busy time of those moves (events) */
@@ -202,6 +206,12 @@ typedef struct asv_engine_stats {
     double bubble_ms_timed;       /* sum of per-iteration bubble (virtual) inside the window */
     int64_t kernel_launches_timed;/* our kernels launched inside the window (attention + merge) */
     double virtual_window_ms;     /* reference-clock duration of the same window */
+    int64_t h2d_bytes_window;     /* the physical moves above restricted to the timed window */
+    int64_t d2h_bytes_window;
+    int64_t p2p_bytes_window;
+    double measured_idle_frac;    /* 1 - sum(warp busy) / (warps x launch span), layer-0 launch of each
+                                     timed iteration, from per-warp %globaltimer */
+    double measured_bubble_ms;    /* sum over timed iterations of the mean idle time per warp x layers */
 } asv_engine_stats;
 
 int asv_engine_run(const char* config_json, const char* policy_override, const asv_engine_opts* opts,

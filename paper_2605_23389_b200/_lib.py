@@ -57,6 +57,7 @@ class AttnArgs(C.Structure):
         ("sm_scale", C.c_float),
         ("launch_index", C.c_uint32),
         ("pdl", C.c_int32),
+        ("warp_timestamps", C.c_void_p),
     ]
 
 
@@ -77,6 +78,7 @@ class EngineOpts(C.Structure):
         ("pdl", C.c_int32),
         ("run_ahead", C.c_int32),
         ("copy_begin", C.c_int64),
+        ("pair_mode", C.c_int32),
     ]
 
 
@@ -107,6 +109,11 @@ class EngineStats(C.Structure):
         ("bubble_ms_timed", C.c_double),
         ("kernel_launches_timed", C.c_int64),
         ("virtual_window_ms", C.c_double),
+        ("h2d_bytes_window", C.c_int64),
+        ("d2h_bytes_window", C.c_int64),
+        ("p2p_bytes_window", C.c_int64),
+        ("measured_idle_frac", C.c_double),
+        ("measured_bubble_ms", C.c_double),
     ]
 
     def as_dict(self):

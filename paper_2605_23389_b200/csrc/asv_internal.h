@@ -41,9 +41,10 @@ struct AttnLaunch {
     int32_t n_merge;
     int sms;
     float sm_scale;
+    unsigned long long* warp_ts;  // optional per-warp %globaltimer (start, end)
 };
 
-int attn_warps_per_cta();
+int attn_warps_per_cta(int group);
 cudaError_t attn_occupancy(int group, int* blocks_per_sm);
 cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st);
 

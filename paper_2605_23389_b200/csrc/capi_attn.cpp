@@ -99,7 +99,7 @@ int asv_attn_num_workers(const asv_attn_shape* shape, int device, int32_t* worke
         }
         blocks = cached;
     }
-    *workers_out = sms * blocks * attn_warps_per_cta();
+    *workers_out = sms * blocks * attn_warps_per_cta(g);
     return ASV_OK;
 }
 
@@ -251,13 +251,21 @@ int asv_decode_attention(const asv_attn_shape* shape, const asv_attn_args* a, vo
     const int64_t need = kHeadBytes + static_cast<int64_t>(pl.total_splits) * n_q * (128 * 4 + 8);
     if (a->workspace == nullptr || static_cast<int64_t>(a->workspace_bytes) < need)
         return fail(ASV_ERR_INVALID, "workspace too small for plan: need " + std::to_string(need));
-    const int nw = attn_warps_per_cta();
+    const int nw = attn_warps_per_cta(n_q / n_kv);
     if (pl.num_workers < nw || pl.num_workers % nw != 0)
         return fail(ASV_ERR_INVALID, "plan num_workers must be a multiple of the CTA warp count");
 
     AttnLaunch L{};
     L.group = n_q / n_kv;
     L.grid = pl.num_workers / nw;
+    {
+        // the in-kernel merge uses a grid-wide barrier: never exceed co-residency
+        int dev = 0;
+        cudaGetDevice(&dev);
+        int32_t resident = 0;
+        if (int rc = asv_attn_num_workers(shape, dev, &resident)) return rc;
+        L.grid = std::max(1, std::min(L.grid, resident / nw));
+    }
     L.q = a->q;
     L.pool = a->kv_pool;
     L.page_bytes = static_cast<int64_t>(shape->num_layers) * 2 * n_kv * kBlockBytes;
@@ -288,6 +296,7 @@ int asv_decode_attention(const asv_attn_shape* shape, const asv_attn_args* a, vo
     L.part_o = reinterpret_cast<float*>(ws + kHeadBytes);
     L.part_ml = reinterpret_cast<float*>(ws + kHeadBytes + static_cast<int64_t>(pl.total_splits) * n_q * 512);
     L.sm_scale = a->sm_scale;
+    L.warp_ts = reinterpret_cast<unsigned long long*>(a->warp_timestamps);
     cudaError_t e = attn_launch(L, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "decode attention launch");
     return ASV_OK;

@@ -19,9 +19,10 @@
 //    fma.rn.f32.bf16 (one FHFMA per MAC, no converts), warp-shuffle softmax;
 //  * GQA (group 2..8): mma.sync.m16n8k16 bf16 on the query group (rows = heads),
 //    S fragment reused in registers as the PV A operand;
-//  * split requests publish (o, m, l) partials; a small merge kernel (K2), chained
-//    with programmatic dependent launch, combines them (log-sum-exp) — the
-//    streaming kernel itself carries no fences or semaphores;
+//  * split requests publish (o, m, l) partials; a warp announces its partials in
+//    batches (one fence per batch, relaxed per-(request, kv head) counters) and
+//    the last arrival merges the rows (log-sum-exp, K2) — no per-item fences and
+//    no grid barrier, so finished CTAs free their SM for the next layer;
 //  * the owner of a request's last split appends the step's K/V row at position
 //    seq_len (prefix_len += 1, cluster_sim.hpp:443-447);
 //  * programmatic dependent launch: the KV prefetch of layer l+1 overlaps layer
@@ -29,6 +30,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "asv_internal.h"
 
@@ -40,7 +43,8 @@ constexpr int kPage = 16;
 constexpr int kRowBytes = kD * 2;               // 256
 constexpr int kBlockBytes = kPage * kRowBytes;  // 4096: one (page, layer, K|V, head) block
 constexpr int kStageBytes = 2 * kBlockBytes;    // K + V
-constexpr int kRing = 4;                        // descriptor ring depth (>= stages + 1)
+constexpr int kWarpExtra = 1024;                // per warp: mbarriers, p scratch, desc ring, split list
+constexpr int kPendMax = 64;                    // split items a warp publishes before announcing them
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct Params {
@@ -63,8 +67,11 @@ struct Params {
     float* part_o;    // [slots * n_q][128]
     float2* part_ml;  // [slots * n_q]
     int32_t* sem;     // [b * n_kv]
-    uint32_t* work;   // [2]: grab counter, finished warps (this launch parity)
+    uint32_t* work;   // [3]: grab counter, arrived warps, exited warps (this launch parity)
+    const int32_t* merge_reqs;  // requests split more than once
+    int32_t merge_rows;         // merge_reqs count * n_q
     float scale_log2;
+    unsigned long long* warp_ts;  // optional [total_warps][2] %globaltimer start/end (bubble probe, I1)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -222,6 +229,105 @@ __device__ __forceinline__ void write_final_row(const Params& p, int r, int qh, 
     }
 }
 
+// Log-sum-exp merge of the split partials of (request r, query head qh).
+// Few splits: every lane owns dims 4*lane..4*lane+3 and walks the splits, 8
+// loads in flight.  Many splits (long contexts): every lane owns a subset of the
+// SPLITS and all 128 dims, then the 32 lane sums are reduced through the warp's
+// (drained) shared-memory stage area `red` (>= 16 KiB).
+__device__ __forceinline__ void merge_row(const Params& p, int r, int qh, int lane, float* red) {
+    const int s0 = __ldg(p.split_base + r);
+    const int ns = __ldg(p.split_base + r + 1) - s0;
+    const float2* ml = p.part_ml + static_cast<int64_t>(s0) * p.n_q + qh;
+    const int64_t mstride = p.n_q;
+    if (ns > 24 && red != nullptr) {
+        float M = -INFINITY;
+        for (int s = lane; s < ns; s += 32) M = fmaxf(M, __ldcg(ml + s * mstride).x);
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+        float L = 0.f;
+        for (int s = lane; s < ns; s += 32) {
+            const float2 v = __ldcg(ml + s * mstride);
+            L += (v.x == -INFINITY) ? 0.f : exp2f(v.x - M) * v.y;
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
+        float o[4] = {0.f, 0.f, 0.f, 0.f};
+        // two passes of 64 dims keep the per-lane accumulator at 64 registers
+#pragma unroll 1
+        for (int half = 0; half < 2; ++half) {
+            float acc[64];
+#pragma unroll
+            for (int d = 0; d < 64; ++d) acc[d] = 0.f;
+            for (int s = lane; s < ns; s += 32) {
+                const float mx = __ldcg(ml + s * mstride).x;
+                const float w = (mx == -INFINITY) ? 0.f : exp2f(mx - M);
+                const float4* src = reinterpret_cast<const float4*>(
+                                        p.part_o + (static_cast<int64_t>(s0 + s) * p.n_q + qh) * kD) + half * 16;
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                    const float4 x = __ldcg(src + c);
+                    acc[4 * c + 0] += w * x.x;
+                    acc[4 * c + 1] += w * x.y;
+                    acc[4 * c + 2] += w * x.z;
+                    acc[4 * c + 3] += w * x.w;
+                }
+            }
+            // transpose-reduce through red[lane][64] (pitch 65: conflict-free columns)
+#pragma unroll
+            for (int d = 0; d < 64; ++d) red[lane * 65 + d] = acc[d];
+            __syncwarp();
+            if ((lane >> 4) == half) {
+                const int c = (lane & 15) * 4;
+                for (int l2 = 0; l2 < 32; ++l2) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) o[e] += red[l2 * 65 + c + e];
+                }
+            }
+            __syncwarp();
+        }
+        write_final_row(p, r, qh, lane, o, M, L);
+        return;
+    }
+    float M = -INFINITY;
+    for (int s = lane; s < ns; s += 32) M = fmaxf(M, __ldcg(ml + s * mstride).x);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+    float L = 0.f;
+    for (int s = lane; s < ns; s += 32) {
+        const float2 v = __ldcg(ml + s * mstride);
+        L += (v.x == -INFINITY) ? 0.f : exp2f(v.x - M) * v.y;
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
+    const float4* po = reinterpret_cast<const float4*>(p.part_o + (static_cast<int64_t>(s0) * p.n_q + qh) * kD) + lane;
+    const int64_t ostride = static_cast<int64_t>(p.n_q) * (kD / 4);
+    float o[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int base = 0; base < ns; base += 8) {
+        float4 v[8];
+        float w[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int s = base + j;
+            if (s < ns) {
+                v[j] = __ldcg(po + s * ostride);
+                const float mx = __ldcg(ml + s * mstride).x;
+                w[j] = (mx == -INFINITY) ? 0.f : exp2f(mx - M);
+            } else {
+                v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+                w[j] = 0.f;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            o[0] += w[j] * v[j].x;
+            o[1] += w[j] * v[j].y;
+            o[2] += w[j] * v[j].z;
+            o[3] += w[j] * v[j].w;
+        }
+    }
+    write_final_row(p, r, qh, lane, o, M, L);
+}
+
 // KV append (K3): lanes 0-15 write the K row, 16-31 the V row (16 B each, swizzled).
 __device__ __forceinline__ void append_row(const Params& p, const Desc& d, int lane) {
     if (p.k_new == nullptr || d.append_phys < 0) return;
@@ -233,6 +339,41 @@ __device__ __forceinline__ void append_row(const Params& p, const Desc& d, int l
     char* dst = p.pool_w + static_cast<int64_t>(d.append_phys) * p.page_bytes + p.layer_off +
                 (is_v ? p.v_off : 0) + static_cast<int64_t>(d.head) * kBlockBytes + swz(t, c);
     *reinterpret_cast<uint4*>(dst) = __ldg(reinterpret_cast<const uint4*>(src));
+}
+
+// Announce this warp's published split partials: one fence for the whole list
+// (release), then one relaxed counter bump per item; for every (request, kv
+// head) whose count completes here, this warp merges its GROUP query heads.
+// `pend` holds (request | head << 16, nsplit) pairs; `red` is a drained stage
+// area for wide merges (nullptr mid-kernel).
+template <int GROUP>
+__device__ __forceinline__ void announce_splits(const Params& p, const int2* pend, int n, int lane, float* red) {
+    __syncwarp();
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    for (int base = 0; base < n; base += 32) {
+        int r = 0, head = 0;
+        bool last = false;
+        if (base + lane < n) {
+            const int2 e = pend[base + lane];
+            r = e.x & 0xffff;
+            head = e.x >> 16;
+            int32_t* sem = p.sem + static_cast<int64_t>(r) * p.n_kv + head;
+            const int prev = atomicAdd(sem, 1);
+            last = prev == e.y - 1;
+            if (last) *sem = 0;  // re-arm for the next launch (stream-ordered)
+        }
+        unsigned mask = __ballot_sync(0xffffffffu, last);
+        if (mask != 0u) {
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire the other splits
+            while (mask != 0u) {
+                const int j = __ffs(mask) - 1;
+                mask &= mask - 1u;
+                const int rj = __shfl_sync(0xffffffffu, r, j);
+                const int hj = __shfl_sync(0xffffffffu, head, j);
+                for (int g = 0; g < GROUP; ++g) merge_row(p, rj, hj * GROUP + g, lane, red);
+            }
+        }
+    }
 }
 
 // ------------------------------------------------------------- q staging
@@ -313,16 +454,19 @@ struct Acc<1> {
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
         const float m_new = fmaxf(m, mx);
-        const float alpha = exp2f(m - m_new);
+        if (m_new > m) {  // warp-uniform: the running max moved
+            const float alpha = exp2f(m - m_new);
+            l *= alpha;
+            o[0] *= alpha;
+            o[1] *= alpha;
+            o[2] *= alpha;
+            o[3] *= alpha;
+        }
         m = m_new;
         // P rounded to bf16 for the PV product (FA2/FA3 convention); l sums the
         // rounded weights so O / l stays an exact convex combination of V rows.
         const __nv_bfloat16 pb = __float2bfloat16_rn(exp2f(s - m_new));
-        l = l * alpha + ((half == 0) ? __bfloat162float(pb) : 0.f);
-        o[0] *= alpha;
-        o[1] *= alpha;
-        o[2] *= alpha;
-        o[3] *= alpha;
+        l += (half == 0) ? __bfloat162float(pb) : 0.f;
         if (half == 0) scratch[t] = pb;
         __syncwarp();
         const uint4 p0 = lds128(sp);
@@ -384,27 +528,47 @@ struct Acc<1> {
 template <int GROUP>
 struct Acc {
     float m, l;
-    float o[16][2];  // C rows 0-7 (query heads), 16 n-tiles of 8 dims
+    float o[16][4];  // full C fragments; rows 8-15 (padding heads) stay exactly 0
     __device__ __forceinline__ void reset() {
         m = -INFINITY;
         l = 0.f;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = 0.f;
+        for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    }
+    template <bool PARTIAL>
+    __device__ __forceinline__ void pv(const uint32_t* pa, uint32_t vs, int valid, int lane) {
+        const int qcol = (lane & 3) * 2;
+        const int trow = (lane & 7) + ((lane >> 3) & 1) * 8;
+#pragma unroll
+        for (int dn = 0; dn < 16; dn += 2) {
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4_t(vs + swz(trow, dn + (lane >> 4)), b0, b1, b2, b3);
+            if constexpr (PARTIAL) {
+                // rows >= valid may hold stale data: P is 0 there but 0 * NaN = NaN
+                b0 = mask_tokens(b0, qcol, valid);
+                b2 = mask_tokens(b2, qcol, valid);
+                b1 = mask_tokens(b1, qcol + 8, valid);
+                b3 = mask_tokens(b3, qcol + 8, valid);
+            }
+            mma_bf16(o[dn], pa[0], pa[1], b0, b1);
+            mma_bf16(o[dn + 1], pa[0], pa[1], b2, b3);
+        }
     }
     __device__ __forceinline__ void page(const QRegs<GROUP>& q, uint32_t ks, uint32_t vs, uint32_t,
                                          __nv_bfloat16*, int valid, float scale, int lane) {
         const int qcol = (lane & 3) * 2;
-        // S = Q K^T: two n-tiles of 8 tokens, 8 k-steps of 16 dims
-        float sacc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+        // S = Q K^T: two n-tiles of 8 tokens; even/odd k-steps accumulate in
+        // separate fragments so the HMMA dependency chains are 4 deep, not 8
+        float sa[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+        float sb[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-            const int trow = nt * 8 + (lane & 7);
+        for (int kk = 0; kk < 8; kk += 2) {
 #pragma unroll
-            for (int kk = 0; kk < 8; kk += 2) {
+            for (int nt = 0; nt < 2; ++nt) {
                 uint32_t b0, b1, b2, b3;
-                ldsm_x4(ks + swz(trow, 2 * kk + (lane >> 3)), b0, b1, b2, b3);
-                mma_bf16(sacc[nt], q.v[2 * kk], q.v[2 * kk + 1], b0, b1);
-                mma_bf16(sacc[nt], q.v[2 * kk + 2], q.v[2 * kk + 3], b2, b3);
+                ldsm_x4(ks + swz(nt * 8 + (lane & 7), 2 * kk + (lane >> 3)), b0, b1, b2, b3);
+                mma_bf16(sa[nt], q.v[2 * kk], q.v[2 * kk + 1], b0, b1);
+                mma_bf16(sb[nt], q.v[2 * kk + 2], q.v[2 * kk + 3], b2, b3);
             }
         }
         float sv[4];
@@ -413,14 +577,23 @@ struct Acc {
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int tok = nt * 8 + qcol + e;
-                sv[nt * 2 + e] = (tok < valid) ? sacc[nt][e] * scale : -INFINITY;
+                sv[nt * 2 + e] = (tok < valid) ? (sa[nt][e] + sb[nt][e]) * scale : -INFINITY;
             }
         }
         float mx = fmaxf(fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3]));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
         const float m_new = fmaxf(m, mx);
-        const float alpha = exp2f(m - m_new);
+        // rescale only when some row's running max moved (rare after the first pages)
+        if (__any_sync(0xffffffffu, m_new > m)) {
+            const float alpha = exp2f(m - m_new);
+            l *= alpha;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                o[i][0] *= alpha;
+                o[i][1] *= alpha;
+            }
+        }
         m = m_new;
         uint32_t pa[2];
         float psum = 0.f;
@@ -429,32 +602,12 @@ struct Acc {
             pa[nt] = pack_bf16(exp2f(sv[nt * 2] - m_new), exp2f(sv[nt * 2 + 1] - m_new));
             psum += bf16_lo(pa[nt]) + bf16_hi(pa[nt]);
         }
-        l = l * alpha + psum;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            o[i][0] *= alpha;
-            o[i][1] *= alpha;
-        }
+        l += psum;
         // O += P V: A = P (the S fragments, bf16), B = V tile via ldmatrix.trans
-        const int trow = (lane & 7) + ((lane >> 3) & 1) * 8;
-#pragma unroll
-        for (int dn = 0; dn < 16; dn += 2) {
-            uint32_t b0, b1, b2, b3;
-            ldsm_x4_t(vs + swz(trow, dn + (lane >> 4)), b0, b1, b2, b3);
-            if (valid < kPage) {
-                b0 = mask_tokens(b0, qcol, valid);
-                b2 = mask_tokens(b2, qcol, valid);
-                b1 = mask_tokens(b1, qcol + 8, valid);
-                b3 = mask_tokens(b3, qcol + 8, valid);
-            }
-            float c0[4] = {o[dn][0], o[dn][1], 0.f, 0.f};
-            float c1[4] = {o[dn + 1][0], o[dn + 1][1], 0.f, 0.f};
-            mma_bf16(c0, pa[0], pa[1], b0, b1);
-            mma_bf16(c1, pa[0], pa[1], b2, b3);
-            o[dn][0] = c0[0];
-            o[dn][1] = c0[1];
-            o[dn + 1][0] = c1[0];
-            o[dn + 1][1] = c1[1];
+        if (valid == kPage) {
+            pv<false>(pa, vs, valid, lane);
+        } else {
+            pv<true>(pa, vs, valid, lane);
         }
     }
     __device__ __forceinline__ bool finish(const Params& p, const Desc& d, int lane) {
@@ -494,26 +647,31 @@ struct Acc {
 
 // ============================================================ the kernel
 template <int NW, int S, int GROUP>
-__global__ void __launch_bounds__(NW * 32)
+__global__ void __launch_bounds__(NW * 32, (NW == 2 ? 4 : 2))
 decode_attn_kernel(const Params p) {
-    static_assert(kRing >= S + 1, "descriptor ring must cover the TMA lookahead");
+    constexpr int kRing = S + 1;  // descriptor ring must cover the TMA lookahead
+    static_assert(S <= 8, "mbarrier area holds 8 stages");
     extern __shared__ __align__(1024) char smem_raw[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    // per warp: S stages (8 KiB) | S mbarriers (64 B) | p scratch (64 B) | desc ring (128 B)
-    constexpr int kWarpBytes = S * kStageBytes + 256;
+    // per warp: S stages (8 KiB) | S mbarriers (64 B) | p scratch (64 B) | desc ring
+    constexpr int kWarpBytes = S * kStageBytes + kWarpExtra;
     char* wbase = smem_raw + warp * kWarpBytes;
     const uint32_t stage0 = smem_u32(wbase);
     const uint32_t bar0 = smem_u32(wbase + S * kStageBytes);
     __nv_bfloat16* scratch = reinterpret_cast<__nv_bfloat16*>(wbase + S * kStageBytes + 64);
     const uint32_t sp = smem_u32(scratch);
     Desc* ring = reinterpret_cast<Desc*>(wbase + S * kStageBytes + 128);
+    int2* pend = reinterpret_cast<int2*>(wbase + S * kStageBytes + 512);
+    int npend = 0;
 
     if (lane == 0) {
         for (int s = 0; s < S; ++s) mbar_init(bar0 + 8 * s, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     const uint64_t pol = evict_first_policy();
+    unsigned long long ts_begin = 0;
+    if (p.warp_ts != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts_begin));
 
     // ---- producer state: current item (descriptor + lane-distributed page ids),
     // next item (loads in flight), and the id after that (atomic in flight)
@@ -603,10 +761,29 @@ decode_attn_kernel(const Params p) {
                 qn_ready = true;
             }
         }
-        acc.finish(p, cd, lane);  // final row (single split) or partial for the merge kernel
+        if (acc.finish(p, cd, lane)) {  // published a split partial: remember it
+            if (lane == 0) pend[npend] = make_int2(cd.r | (cd.head << 16), cd.nsplit);
+            if (++npend == kPendMax) {
+                announce_splits<GROUP>(p, pend, npend, lane, nullptr);
+                npend = 0;
+            }
+        }
     }
 
-    // last warp out re-arms the work counters of this launch parity
+    // ---- K2: announce the remaining split partials; last arrivals merge.  Warps
+    // with nothing left exit at once, so the next layer's CTAs can take their SM.
+    if (npend > 0) {
+        float* red = S * kStageBytes >= 32 * 65 * 4 ? reinterpret_cast<float*>(wbase) : nullptr;  // drained
+        announce_splits<GROUP>(p, pend, npend, lane, red);
+    }
+    if (p.warp_ts != nullptr && lane == 0) {
+        unsigned long long ts_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts_end));
+        const int64_t w = static_cast<int64_t>(blockIdx.x) * NW + warp;
+        p.warp_ts[2 * w] = ts_begin;
+        p.warp_ts[2 * w + 1] = ts_end;
+    }
+    // last warp out re-arms the counters of this launch parity
     if (lane == 0) {
         const uint32_t done = atomicAdd(p.work + 1, 1u);
         if (done == static_cast<uint32_t>(p.total_warps) - 1u) {
@@ -616,74 +793,23 @@ decode_attn_kernel(const Params p) {
     }
 }
 
-// ============================================================ split merge (K2)
-// One warp per (request, query head) of every split request: log-sum-exp merge
-// of the partials the streaming kernel published.  Chained with PDL: the warps
-// park on griddepcontrol.wait until the streaming grid has completed (which
-// also makes its partial stores visible), so no fences or semaphores are needed.
-constexpr int kMergeWarps = 4;
-
-__global__ void __launch_bounds__(kMergeWarps * 32)
-merge_splits_kernel(const Params p, const int32_t* __restrict__ merge_reqs, int32_t rows) {
-    // let the next layer's streaming kernel start prefetching as soon as SMs free
-    // up; it cannot pass its own wait before this grid completes
-    grid_dep_launch();
-    grid_dep_wait();
-    const int lane = threadIdx.x & 31;
-    for (int row = blockIdx.x * kMergeWarps + (threadIdx.x >> 5); row < rows; row += gridDim.x * kMergeWarps) {
-        const int r = __ldg(merge_reqs + row / p.n_q);
-        const int qh = row % p.n_q;
-        const int s0 = __ldg(p.split_base + r);
-        const int ns = __ldg(p.split_base + r + 1) - s0;
-        const float2* ml = p.part_ml + static_cast<int64_t>(s0) * p.n_q + qh;
-        // max over splits, lane-parallel
-        float M = -INFINITY;
-        for (int s = lane; s < ns; s += 32) M = fmaxf(M, ml[static_cast<int64_t>(s) * p.n_q].x);
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-        float L = 0.f;
-        for (int s = lane; s < ns; s += 32) {
-            const float2 v = ml[static_cast<int64_t>(s) * p.n_q];
-            L += (v.x == -INFINITY) ? 0.f : exp2f(v.x - M) * v.y;
-        }
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
-        float o[4] = {0.f, 0.f, 0.f, 0.f};
-        const float4* po = reinterpret_cast<const float4*>(p.part_o + (static_cast<int64_t>(s0) * p.n_q + qh) * kD) + lane;
-        const int64_t stride4 = static_cast<int64_t>(p.n_q) * (kD / 4);
-#pragma unroll 4
-        for (int s = 0; s < ns; ++s) {
-            const float mx = ml[static_cast<int64_t>(s) * p.n_q].x;
-            const float w = (mx == -INFINITY) ? 0.f : exp2f(mx - M);
-            const float4 v = po[s * stride4];
-            o[0] += w * v.x;
-            o[1] += w * v.y;
-            o[2] += w * v.z;
-            o[3] += w * v.w;
-        }
-        write_final_row(p, r, qh, lane, o, M, L);
-    }
-}
-
 // ------------------------------------------------------------- launcher
-constexpr int kNW = 4;
-constexpr int kStages = 3;
-
-template <int GROUP>
+// (warps per CTA, TMA stages per warp) variants; the default is chosen per group
+// from B200 measurements, ASV_ATTN_VARIANT=<NW>x<S> overrides it (tuning only).
+template <int NW, int S, int GROUP>
 struct Launch {
-    static constexpr int kSmem = kNW * (kStages * kStageBytes + 256);
+    static constexpr int kSmem = NW * (S * kStageBytes + kWarpExtra);
     static cudaError_t configure() {
-        return cudaFuncSetAttribute(decode_attn_kernel<kNW, kStages, GROUP>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        return cudaFuncSetAttribute(decode_attn_kernel<NW, S, GROUP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kSmem);
     }
     static cudaError_t occupancy(int* blocks) {
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, decode_attn_kernel<kNW, kStages, GROUP>,
-                                                             kNW * 32, kSmem);
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, decode_attn_kernel<NW, S, GROUP>, NW * 32, kSmem);
     }
     static cudaError_t run(const Params& p, int grid, bool pdl, cudaStream_t st) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(grid);
-        cfg.blockDim = dim3(kNW * 32);
+        cfg.blockDim = dim3(NW * 32);
         cfg.dynamicSmemBytes = kSmem;
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
@@ -691,20 +817,58 @@ struct Launch {
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = pdl ? 1 : 0;
-        return cudaLaunchKernelEx(&cfg, decode_attn_kernel<kNW, kStages, GROUP>, p);
+        return cudaLaunchKernelEx(&cfg, decode_attn_kernel<NW, S, GROUP>, p);
     }
 };
 
-template <int GROUP>
-cudaError_t dispatch_group(bool query, int* blocks, const Params* p, int grid, bool pdl, cudaStream_t st) {
+template <int NW, int S, int GROUP>
+cudaError_t dispatch_variant(bool query, int* blocks, const Params* p, int grid, bool pdl, cudaStream_t st) {
+    using L = Launch<NW, S, GROUP>;
     static bool configured = false;  // attribute set is idempotent; a race is harmless
     if (!configured) {
-        cudaError_t e = Launch<GROUP>::configure();
+        cudaError_t e = L::configure();
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    if (query) return Launch<GROUP>::occupancy(blocks);
-    return Launch<GROUP>::run(*p, grid, pdl, st);
+    if (query) return L::occupancy(blocks);
+    return L::run(*p, grid, pdl, st);
+}
+
+struct Variant {
+    int nw, stages;
+};
+
+Variant default_variant(int group) {
+    (void)group;
+    return Variant{4, 3};
+}
+
+Variant selected_variant(int group) {
+    static const char* env = getenv("ASV_ATTN_VARIANT");
+    if (env != nullptr) {
+        int nw = 0, st = 0;
+        if (sscanf(env, "%dx%d", &nw, &st) == 2) return Variant{nw, st};
+    }
+    return default_variant(group);
+}
+
+template <int GROUP>
+cudaError_t dispatch_group(bool query, int* blocks, const Params* p, int grid, bool pdl, cudaStream_t st) {
+    const Variant v = selected_variant(GROUP);
+    if (v.nw == 4 && v.stages == 3) return dispatch_variant<4, 3, GROUP>(query, blocks, p, grid, pdl, st);
+    if constexpr (GROUP == 1 || GROUP == 5 || GROUP == 4) {
+        if (v.nw == 4 && v.stages == 4) return dispatch_variant<4, 4, GROUP>(query, blocks, p, grid, pdl, st);
+        if (v.nw == 2 && v.stages == 6) return dispatch_variant<2, 6, GROUP>(query, blocks, p, grid, pdl, st);
+        if (v.nw == 4 && v.stages == 2) return dispatch_variant<4, 2, GROUP>(query, blocks, p, grid, pdl, st);
+        if (v.nw == 2 && v.stages == 4) return dispatch_variant<2, 4, GROUP>(query, blocks, p, grid, pdl, st);
+    }
+    return dispatch_variant<4, 3, GROUP>(query, blocks, p, grid, pdl, st);
+}
+
+bool variant_available(int group, Variant v) {
+    if (v.nw == 4 && v.stages == 3) return true;
+    if (group != 1 && group != 4 && group != 5) return false;
+    return (v.nw == 4 && (v.stages == 4 || v.stages == 2)) || (v.nw == 2 && (v.stages == 6 || v.stages == 4));
 }
 
 cudaError_t dispatch(int group, bool query, int* blocks, const Params* p, int grid, bool pdl,
@@ -721,28 +885,13 @@ cudaError_t dispatch(int group, bool query, int* blocks, const Params* p, int gr
 
 }  // namespace
 
-int attn_warps_per_cta() { return kNW; }
+int attn_warps_per_cta(int group) {
+    const Variant v = selected_variant(group);
+    return variant_available(group, v) ? v.nw : 4;
+}
 
 cudaError_t attn_occupancy(int group, int* blocks_per_sm) {
     return dispatch(group, true, blocks_per_sm, nullptr, 0, false, nullptr);
-}
-
-cudaError_t merge_launch(const Params& p, const int32_t* merge_reqs, int32_t n_merge, int sms, bool pdl,
-                         cudaStream_t st) {
-    const int32_t rows = n_merge * p.n_q;
-    if (rows <= 0) return cudaSuccess;
-    const int blocks = min((rows + kMergeWarps - 1) / kMergeWarps, 2 * sms);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(blocks);
-    cfg.blockDim = dim3(kMergeWarps * 32);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, merge_splits_kernel, p, merge_reqs, rows);
 }
 
 cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st) {
@@ -758,7 +907,7 @@ cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st) {
     p.num_items = a.num_items;
     p.n_kv = a.n_kv;
     p.n_q = a.n_q;
-    p.total_warps = a.grid * kNW;
+    p.total_warps = a.grid * attn_warps_per_cta(a.group);
     p.k_new = static_cast<const __nv_bfloat16*>(a.k_new);
     p.v_new = static_cast<const __nv_bfloat16*>(a.v_new);
     p.out = static_cast<__nv_bfloat16*>(a.out);
@@ -767,11 +916,12 @@ cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st) {
     p.part_ml = reinterpret_cast<float2*>(a.part_ml);
     p.sem = a.sem;
     p.work = a.work;
+    p.merge_reqs = a.merge_reqs;
+    p.merge_rows = a.n_merge * a.n_q;
     p.scale_log2 = a.sm_scale * kLog2e;
+    p.warp_ts = a.warp_ts;
     if (p.num_items <= 0) return cudaSuccess;
-    cudaError_t e = dispatch(a.group, false, nullptr, &p, a.grid, a.pdl, st);
-    if (e != cudaSuccess) return e;
-    return merge_launch(p, a.merge_reqs, a.n_merge, a.sms, a.pdl, st);
+    return dispatch(a.group, false, nullptr, &p, a.grid, a.pdl, st);
 }
 
 }  // namespace asv

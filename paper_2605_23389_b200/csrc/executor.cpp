@@ -172,7 +172,8 @@ class GpuExecutor : public prefixsim::EngineObserver {
                                         std::to_string(row_bytes_all_) + " vs " +
                                         std::to_string(spec.kv_bytes_per_token()) + ")");
         }
-        pair_ = o.prefetch_device != o.decode_device;
+        pair_ = o.prefetch_device != o.decode_device || o.pair_mode != 0;
+        const bool peer = o.prefetch_device != o.decode_device;
         const int64_t bmax = sim.b_max_blocks(), crb = sim.crb_capacity_blocks();
         dec_pages_ = sim.cluster.decode_hbm_blocks + (pair_ ? 0 : bmax + crb) + 64;
         pre_pages_ = pair_ ? bmax + crb + 64 : 0;
@@ -186,7 +187,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
                                         std::to_string(fr) + " B)");
         }
         dec_.init(o.decode_device, dec_pages_, page_bytes_);
-        if (pair_) {
+        if (pair_ && peer) {
             ASV_CUDA(cudaSetDevice(o.decode_device));
             int can = 0;
             ASV_CUDA(cudaDeviceCanAccessPeer(&can, o.decode_device, o.prefetch_device));
@@ -198,15 +199,17 @@ class GpuExecutor : public prefixsim::EngineObserver {
             e = cudaDeviceEnablePeerAccess(o.decode_device, 0);
             if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) ASV_CUDA(e);
             cudaGetLastError();
-            pre_.init(o.prefetch_device, pre_pages_, page_bytes_);
         }
+        if (pair_) pre_.init(o.prefetch_device, pre_pages_, page_bytes_);
         // streams
         ASV_CUDA(cudaSetDevice(o.decode_device));
         ASV_CUDA(cudaStreamCreateWithFlags(&compute_, cudaStreamNonBlocking));
         ASV_CUDA(cudaStreamCreateWithFlags(&p2p_, cudaStreamNonBlocking));
         ASV_CUDA(cudaSetDevice(xfer_device()));
         ASV_CUDA(cudaStreamCreateWithFlags(&xfer_, cudaStreamNonBlocking));
+        ASV_CUDA(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));  // other PCIe direction
         xfer_ev_.init(xfer_device(), 4096);
+        d2h_ev_.init(xfer_device(), 4096);
         ASV_CUDA(cudaSetDevice(o.decode_device));
         p2p_ev_.init(o.decode_device, 4096);
         // host pool
@@ -240,6 +243,8 @@ class GpuExecutor : public prefixsim::EngineObserver {
         att_beg_.resize(static_cast<size_t>(ring_));
         att_end_.resize(static_cast<size_t>(ring_));
         slot_timed_.assign(static_cast<size_t>(ring_), 0);
+        ts_dev_.resize(static_cast<size_t>(ring_));
+        ts_host_.resize(static_cast<size_t>(2 * workers_));
         for (int i = 0; i < ring_; ++i) {
             ASV_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&plan_host_[static_cast<size_t>(i)]),
                                    static_cast<size_t>(plan_cap_) * 4, cudaHostAllocDefault));
@@ -247,6 +252,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
             ASV_CUDA(cudaEventCreateWithFlags(&it_end_[static_cast<size_t>(i)], cudaEventDisableTiming));
             ASV_CUDA(cudaEventCreate(&att_beg_[static_cast<size_t>(i)]));
             ASV_CUDA(cudaEventCreate(&att_end_[static_cast<size_t>(i)]));
+            ASV_CUDA(cudaMalloc(&ts_dev_[static_cast<size_t>(i)], static_cast<size_t>(workers_) * 16));
         }
         ws_splits_ = static_cast<int32_t>(dec_pages_ / 2 + max_rows_ + 1);
         ws_bytes_ = asv_attn_workspace_bytes(&shape_, 0, ws_splits_);
@@ -272,6 +278,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
         for (auto e : it_end_) cudaEventDestroy(e);
         for (auto e : att_beg_) cudaEventDestroy(e);
         for (auto e : att_end_) cudaEventDestroy(e);
+        for (auto p : ts_dev_) cudaFree(p);
         for (auto& pr : copy_timers_) {
             cudaEventDestroy(pr.a);
             cudaEventDestroy(pr.b);
@@ -287,6 +294,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
         cudaStreamDestroy(compute_);
         cudaStreamDestroy(p2p_);
         cudaStreamDestroy(xfer_);
+        cudaStreamDestroy(d2h_);
     }
 
     // ---------------------------------------------------------- observer
@@ -351,7 +359,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
                 break;
             case ASV_XFER_EVICT:
                 if (!aligned_) {
-                    begin_xfer_group();
+                    begin_xfer_group(true);
                     write_back_to_host(t.request_id);
                     end_xfer_group();
                 } else {
@@ -360,7 +368,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
                 break;
             case ASV_XFER_SPILL:
             case ASV_XFER_FLUSH:
-                begin_xfer_group();
+                begin_xfer_group(true);
                 write_back_to_host(t.request_id);
                 end_xfer_group();
                 break;
@@ -446,6 +454,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
         for (int l = 0; l < o_.num_layers; ++l) {
             args.layer = l;
             args.launch_index = launches_++;
+            args.warp_timestamps = (timed && l == 0) ? ts_dev_[slot] : nullptr;
             if (asv_decode_attention(&shape_, &args, compute_) != ASV_OK) throw CudaError(asv_last_error());
         }
         ASV_CUDA(cudaEventRecord(att_end_[slot], compute_));
@@ -477,6 +486,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
         ASV_CUDA(cudaStreamSynchronize(compute_));
         ASV_CUDA(cudaSetDevice(xfer_device()));
         ASV_CUDA(cudaStreamSynchronize(xfer_));
+        ASV_CUDA(cudaStreamSynchronize(d2h_));
         ASV_CUDA(cudaSetDevice(o_.decode_device));
         ASV_CUDA(cudaStreamSynchronize(p2p_));
         for (int64_t e = std::max<int64_t>(0, executed_ - ring_); e < executed_; ++e) retire(static_cast<size_t>(e % ring_));
@@ -492,6 +502,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
             }
         }
         stats_.iterations_total = iterations_total_;
+        stats_.measured_idle_frac = span_ns_ > 0 ? 1.0 - busy_ns_ / span_ns_ : 0.0;
         stats_.virtual_window_ms = first_timed_start_ >= 0 ? last_timed_end_ms_ - first_timed_start_ : 0.0;
         stats_.virtual_decode_tok_s = log.iterations.empty() ? 0.0 : prefixsim::decode_throughput(log);
         stats_.host_decide_ms = host_ms_;
@@ -544,7 +555,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
     bool aligned_ = false;  // aligned policy: admits/evicts move between candidate buffers and HBM
 
  private:
-    int64_t cur_seq_ = -1;  // seq of the next iteration (decisions before it belong to its boundary)
+    int64_t cur_seq_ = 0;  // seq of the next iteration (decisions before it belong to its boundary)
     void fill_random(void* dst, int64_t elems, uint64_t seed) {
         std::vector<uint16_t> h(static_cast<size_t>(elems));
         uint64_t s = seed;
@@ -563,27 +574,31 @@ class GpuExecutor : public prefixsim::EngineObserver {
     }
 
     // group copies issued by one decision so one event pair times them
-    void begin_xfer_group() {
+    // H2D groups run on xfer_, D2H groups on d2h_ (both PCIe directions at once)
+    void begin_xfer_group(bool d2h = false) {
         group_timed_ = copies_active() && in_window();
+        cur_ = d2h ? d2h_ : xfer_;
+        cur_ev_ = d2h ? &d2h_ev_ : &xfer_ev_;
         if (!copies_active()) return;
         ASV_CUDA(cudaSetDevice(xfer_device()));
         // pages written/read below may have been used by the last launched iteration
-        if (last_it_end_ != nullptr && waited_it_end_ != last_it_end_) {
-            ASV_CUDA(cudaStreamWaitEvent(xfer_, last_it_end_, 0));
-            waited_it_end_ = last_it_end_;
+        cudaEvent_t& waited = d2h ? waited_it_end_d2h_ : waited_it_end_;
+        if (last_it_end_ != nullptr && waited != last_it_end_) {
+            ASV_CUDA(cudaStreamWaitEvent(cur_, last_it_end_, 0));
+            waited = last_it_end_;
         }
         if (group_timed_) {
             CopyTimer t{};
             ASV_CUDA(cudaEventCreate(&t.a));
             ASV_CUDA(cudaEventCreate(&t.b));
-            ASV_CUDA(cudaEventRecord(t.a, xfer_));
+            ASV_CUDA(cudaEventRecord(t.a, cur_));
             copy_timers_.push_back(t);
         }
     }
     cudaEvent_t end_xfer_group() {
         if (!copies_active()) return nullptr;
-        if (group_timed_) ASV_CUDA(cudaEventRecord(copy_timers_.back().b, xfer_));
-        cudaEvent_t ev = xfer_ev_.record(xfer_);
+        if (group_timed_) ASV_CUDA(cudaEventRecord(copy_timers_.back().b, cur_));
+        cudaEvent_t ev = cur_ev_->record(cur_);
         for (auto id : group_ready_) kv(id).ready = ev;
         group_ready_.clear();
         for (auto& q : group_quarantine_) q.first->release_after(ev, std::move(q.second));
@@ -606,7 +621,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
             char* d = pool.page(pages[static_cast<size_t>(j)]);
             char* h = host_page(id, j);
             ASV_CUDA(cudaMemcpyAsync(to_device ? d : h, to_device ? h : d, static_cast<size_t>(page_bytes_),
-                                     to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, xfer_));
+                                     to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, cur_));
             moved += page_bytes_;
         }
         if (rows > 0) {
@@ -614,7 +629,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
             char* h = host_page(id, full);
             const size_t blocks = static_cast<size_t>(o_.num_layers) * 2 * o_.num_kv_heads;
             ASV_CUDA(cudaMemcpy2DAsync(to_device ? d : h, 4096, to_device ? h : d, 4096, static_cast<size_t>(rows) * 256,
-                                       blocks, to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, xfer_));
+                                       blocks, to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, cur_));
             moved += rows * 256 * static_cast<int64_t>(blocks);
         }
         return moved;
@@ -630,7 +645,8 @@ class GpuExecutor : public prefixsim::EngineObserver {
         r.where = pool == &dec_ ? ReqKV::kDecode : ReqKV::kPrefetch;
         if (!copies_active()) return;
         const int64_t moved = copy_kv(r.pages, *pool, id, q.prefix_len, true);
-        if (group_timed_) stats_.h2d_bytes += moved;
+        stats_.h2d_bytes += moved;
+        if (group_timed_) stats_.h2d_bytes_window += moved;
         group_ready_.push_back(id);
     }
 
@@ -640,11 +656,12 @@ class GpuExecutor : public prefixsim::EngineObserver {
         PagePool* pool = r.where == ReqKV::kPrefetch ? &pre_ : &dec_;
         if (copies_active() && !r.pages.empty()) {
             if (r.ready != nullptr) {
-                ASV_CUDA(cudaStreamWaitEvent(xfer_, r.ready, 0));
+                ASV_CUDA(cudaStreamWaitEvent(cur_, r.ready, 0));
                 r.ready = nullptr;
             }
             const int64_t moved = copy_kv(r.pages, *pool, id, q.prefix_len, false);
-            if (group_timed_) stats_.d2h_bytes += moved;
+            stats_.d2h_bytes += moved;
+            if (group_timed_) stats_.d2h_bytes_window += moved;
             group_quarantine_.push_back({pool, std::move(r.pages)});
             r.pages.clear();
         } else {
@@ -676,10 +693,11 @@ class GpuExecutor : public prefixsim::EngineObserver {
                 ASV_CUDA(cudaEventRecord(t.a, p2p_));
             }
             const int64_t moved = copy_peer(dst, dec_, r.pages, pre_, (*requests_)[static_cast<std::size_t>(id)].prefix_len);
+            stats_.p2p_bytes += moved;
             if (timed) {
                 ASV_CUDA(cudaEventRecord(t.b, p2p_));
                 copy_timers_.push_back(t);
-                stats_.p2p_bytes += moved;
+                stats_.p2p_bytes_window += moved;
             }
             cudaEvent_t ev = p2p_ev_.record(p2p_);
             pre_.release_after(ev, std::move(r.pages));
@@ -700,7 +718,8 @@ class GpuExecutor : public prefixsim::EngineObserver {
             ASV_CUDA(cudaSetDevice(o_.decode_device));
             if (last_it_end_ != nullptr) ASV_CUDA(cudaStreamWaitEvent(p2p_, last_it_end_, 0));
             const int64_t moved = copy_peer(dst, pre_, r.pages, dec_, (*requests_)[static_cast<std::size_t>(id)].prefix_len);
-            if (in_window()) stats_.p2p_bytes += moved;
+            stats_.p2p_bytes += moved;
+            if (in_window()) stats_.p2p_bytes_window += moved;
             cudaEvent_t ev = p2p_ev_.record(p2p_);
             dec_.release_after(ev, std::move(r.pages));
             r.ready = ev;
@@ -747,6 +766,23 @@ class GpuExecutor : public prefixsim::EngineObserver {
             ASV_CUDA(cudaEventElapsedTime(&ms, att_beg_[slot], att_end_[slot]));
             stats_.attn_ms += ms;
             slot_timed_[slot] = 0;
+            // measured bubble of the layer-0 launch: idle warp time inside its span
+            ASV_CUDA(cudaMemcpy(ts_host_.data(), ts_dev_[slot], ts_host_.size() * 8, cudaMemcpyDeviceToHost));
+            uint64_t lo = UINT64_MAX, hi = 0;
+            double busy = 0.0;
+            for (int32_t w = 0; w < workers_; ++w) {
+                const uint64_t a = ts_host_[2 * w], b = ts_host_[2 * w + 1];
+                if (b <= a) continue;
+                lo = std::min(lo, a);
+                hi = std::max(hi, b);
+                busy += static_cast<double>(b - a);
+            }
+            if (hi > lo) {
+                const double span = static_cast<double>(hi - lo) * workers_;
+                busy_ns_ += busy;
+                span_ns_ += span;
+                stats_.measured_bubble_ms += (span - busy) / workers_ * 1e-6 * o_.num_layers;
+            }
         }
         dec_.reclaim(false);
         if (pair_) pre_.reclaim(false);
@@ -766,8 +802,10 @@ class GpuExecutor : public prefixsim::EngineObserver {
     bool pair_ = false;
     int64_t dec_pages_ = 0, pre_pages_ = 0;
     PagePool dec_, pre_;
-    cudaStream_t compute_ = nullptr, p2p_ = nullptr, xfer_ = nullptr;
-    EventRing xfer_ev_, p2p_ev_;
+    cudaStream_t compute_ = nullptr, p2p_ = nullptr, xfer_ = nullptr, d2h_ = nullptr, cur_ = nullptr;
+    EventRing xfer_ev_, d2h_ev_, p2p_ev_;
+    EventRing* cur_ev_ = nullptr;
+    cudaEvent_t waited_it_end_d2h_ = nullptr;
     char* arena_ = nullptr;
     int64_t arena_pages_ = 1;
     int32_t workers_ = 0;
@@ -793,6 +831,9 @@ class GpuExecutor : public prefixsim::EngineObserver {
     uint32_t launches_ = 0;
     double host_ms_ = 0.0;
     double first_timed_start_ = -1.0, last_timed_end_ms_ = 0.0;
+    std::vector<uint64_t*> ts_dev_;
+    std::vector<uint64_t> ts_host_;
+    double busy_ns_ = 0.0, span_ns_ = 0.0;
     asv_engine_stats stats_{};
 };
 

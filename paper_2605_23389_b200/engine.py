@@ -77,7 +77,8 @@ def engine_run(config, *, device: int = 0, prefetch_device: int | None = None,
                num_q_heads: int, num_kv_heads: int, num_layers: int, execute_transfers: bool,
                exec_begin: int = 0, exec_end: int = -1, timed_begin: int = 0, copy_begin: int | None = None,
                host_pool_bytes: int = 8 << 30, shard_index: int = 0, shard_count: int = 1,
-               pdl: bool = True, run_ahead: int = 16, policy: str | None = None) -> dict:
+               pdl: bool = True, run_ahead: int = 16, policy: str | None = None,
+               pair_mode: bool = False) -> dict:
     """Run the decode engine on the GPU (asv_engine_run): reference decisions executed for real."""
     text = config if isinstance(config, str) else json.dumps(config)
     o = _lib.EngineOpts()
@@ -91,6 +92,7 @@ def engine_run(config, *, device: int = 0, prefetch_device: int | None = None,
     o.shard_index, o.shard_count = shard_index, shard_count
     o.pdl = 1 if pdl else 0
     o.run_ahead = run_ahead
+    o.pair_mode = 1 if pair_mode else 0
     st = _lib.EngineStats()
     _lib.check(_lib.lib().asv_engine_run(text.encode(), policy.encode() if policy else None,
                                           C.byref(o), C.byref(st)))

@@ -1,0 +1,66 @@
+"""GPU: the engine's decisions executed for real on the B200 (asv_engine_run).
+
+The whole run is executed and timed, so every boundary KV move happens:
+physical bytes moved per direction must equal the reference's logical bytes for
+the corresponding transfer kinds, and those must equal the golden digests the
+UNMODIFIED reference produced (tests/golden).  Also exercised: the pair path
+(candidate buffers in a separate pool; admits/evicts become device copies).
+"""
+import json
+import os
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))
+
+
+def _run(cfg, policy=None, pair=False, transfers=True):
+    from paper_2605_23389_b200 import engine
+    return engine.engine_run(cfg, policy=policy, device=0, num_q_heads=32, num_kv_heads=32, num_layers=32,
+                             execute_transfers=transfers, exec_begin=0, exec_end=-1, timed_begin=0, copy_begin=0,
+                             host_pool_bytes=1 << 30, pair_mode=pair)
+
+
+def _expect(key):
+    return GOLDEN["logs"][key]["transfer_bytes"]
+
+
+@pytest.mark.parametrize("pair", [False, True])
+def test_aligned_bytes_moved_match_reference(pair):
+    cfg = GOLDEN["configs"]["smoke"]
+    st = _run(cfg, pair=pair)
+    lb, want = st["logical_bytes"], _expect("smoke:aligned")
+    for k, v in want.items():
+        assert lb[k] == v, k
+    assert st["h2d_bytes"] == lb["batch_prefetch"] + lb["stray_prefetch"]
+    assert st["d2h_bytes"] == lb["spill"] + lb["flush"]
+    assert st["p2p_bytes"] == ((lb["admit"] + lb["evict"]) if pair else 0)
+    assert st["iterations_timed"] == GOLDEN["logs"]["smoke:aligned"]["iterations"]
+    assert st["window_ms"] > 0 and st["attn_ms"] > 0
+
+
+@pytest.mark.parametrize("policy", ["fcfs", "disagg-fcfs"])
+def test_fcfs_bytes_moved_match_reference(policy):
+    cfg = GOLDEN["configs"]["smoke"]
+    st = _run(cfg, policy=policy)
+    lb, want = st["logical_bytes"], _expect(f"smoke:{policy}")
+    for k, v in want.items():
+        assert lb[k] == v, k
+    assert st["h2d_bytes"] == lb["admit"]
+    assert st["d2h_bytes"] == lb["evict"]
+
+
+def test_resident_mode_moves_nothing():
+    st = _run(GOLDEN["configs"]["smoke"], transfers=False)
+    assert st["h2d_bytes"] == st["d2h_bytes"] == st["p2p_bytes"] == 0
+    assert st["tokens_timed"] > 0 and st["kernel_launches_timed"] >= 32 * st["iterations_timed"]
+
+
+def test_mismatched_shape_is_rejected():
+    from paper_2605_23389_b200 import engine
+    with pytest.raises(ValueError, match="kv_bytes_per_token"):
+        engine.engine_run(GOLDEN["configs"]["smoke"], device=0, num_q_heads=32, num_kv_heads=8, num_layers=32,
+                          execute_transfers=False)
