@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libasv.so")
+# ASV_LIB_PATH: load an alternative build (A/B kernel experiments only)
+LIB_PATH = os.environ.get("ASV_LIB_PATH") or os.path.join(_HERE, "libasv.so")
 
 
 class AttnShape(C.Structure):

@@ -19,10 +19,10 @@
 //    fma.rn.f32.bf16 (one FHFMA per MAC, no converts), warp-shuffle softmax;
 //  * GQA (group 2..8): mma.sync.m16n8k16 bf16 on the query group (rows = heads),
 //    S fragment reused in registers as the PV A operand;
-//  * split requests publish (o, m, l) partials; a warp announces its partials in
-//    batches (one fence per batch, relaxed per-(request, kv head) counters) and
-//    the last arrival merges the rows (log-sum-exp, K2) — no per-item fences and
-//    no grid barrier, so finished CTAs free their SM for the next layer;
+//  * split requests publish (o, m, l) partials; a small PDL-chained merge kernel
+//    (K2) combines them (log-sum-exp), so the streaming kernel carries no
+//    fences, semaphores or grid barriers and finished CTAs free their SM for the
+//    next layer's prefetch;
 //  * the owner of a request's last split appends the step's K/V row at position
 //    seq_len (prefix_len += 1, cluster_sim.hpp:443-447);
 //  * programmatic dependent launch: the KV prefetch of layer l+1 overlaps layer
@@ -43,8 +43,7 @@ constexpr int kPage = 16;
 constexpr int kRowBytes = kD * 2;               // 256
 constexpr int kBlockBytes = kPage * kRowBytes;  // 4096: one (page, layer, K|V, head) block
 constexpr int kStageBytes = 2 * kBlockBytes;    // K + V
-constexpr int kWarpExtra = 1024;                // per warp: mbarriers, p scratch, desc ring, split list
-constexpr int kPendMax = 64;                    // split items a warp publishes before announcing them
+constexpr int kWarpExtra = 768;                 // per warp: mbarriers | descriptor ring | P scratch
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct Params {
@@ -163,6 +162,15 @@ __device__ __forceinline__ void mma_bf16(float* c, uint32_t a0, uint32_t a2, uin
         : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
         : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
 }
+// m16n8k16 with a full A fragment (a0..a3) and B fragment (b0, b1)
+__device__ __forceinline__ void mma_m16(float* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                        uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7},"
+        " {%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
 // zero the bf16 halves of a packed pair {token k (lo), token k+1 (hi)} past `valid`
 __device__ __forceinline__ uint32_t mask_tokens(uint32_t b, int k, int valid) {
     if (k >= valid) return 0u;
@@ -229,65 +237,14 @@ __device__ __forceinline__ void write_final_row(const Params& p, int r, int qh, 
     }
 }
 
-// Log-sum-exp merge of the split partials of (request r, query head qh).
-// Few splits: every lane owns dims 4*lane..4*lane+3 and walks the splits, 8
-// loads in flight.  Many splits (long contexts): every lane owns a subset of the
-// SPLITS and all 128 dims, then the 32 lane sums are reduced through the warp's
-// (drained) shared-memory stage area `red` (>= 16 KiB).
-__device__ __forceinline__ void merge_row(const Params& p, int r, int qh, int lane, float* red) {
+// Log-sum-exp merge of the split partials of (request r, query head qh): every
+// lane owns dims 4*lane..4*lane+3 and walks the splits with 8 loads in flight
+// (coalesced 512-byte rows; a lane-per-split variant measured slower on B200).
+__device__ __forceinline__ void merge_row(const Params& p, int r, int qh, int lane) {
     const int s0 = __ldg(p.split_base + r);
     const int ns = __ldg(p.split_base + r + 1) - s0;
     const float2* ml = p.part_ml + static_cast<int64_t>(s0) * p.n_q + qh;
     const int64_t mstride = p.n_q;
-    if (ns > 24 && red != nullptr) {
-        float M = -INFINITY;
-        for (int s = lane; s < ns; s += 32) M = fmaxf(M, __ldcg(ml + s * mstride).x);
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-        float L = 0.f;
-        for (int s = lane; s < ns; s += 32) {
-            const float2 v = __ldcg(ml + s * mstride);
-            L += (v.x == -INFINITY) ? 0.f : exp2f(v.x - M) * v.y;
-        }
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
-        float o[4] = {0.f, 0.f, 0.f, 0.f};
-        // two passes of 64 dims keep the per-lane accumulator at 64 registers
-#pragma unroll 1
-        for (int half = 0; half < 2; ++half) {
-            float acc[64];
-#pragma unroll
-            for (int d = 0; d < 64; ++d) acc[d] = 0.f;
-            for (int s = lane; s < ns; s += 32) {
-                const float mx = __ldcg(ml + s * mstride).x;
-                const float w = (mx == -INFINITY) ? 0.f : exp2f(mx - M);
-                const float4* src = reinterpret_cast<const float4*>(
-                                        p.part_o + (static_cast<int64_t>(s0 + s) * p.n_q + qh) * kD) + half * 16;
-#pragma unroll
-                for (int c = 0; c < 16; ++c) {
-                    const float4 x = __ldcg(src + c);
-                    acc[4 * c + 0] += w * x.x;
-                    acc[4 * c + 1] += w * x.y;
-                    acc[4 * c + 2] += w * x.z;
-                    acc[4 * c + 3] += w * x.w;
-                }
-            }
-            // transpose-reduce through red[lane][64] (pitch 65: conflict-free columns)
-#pragma unroll
-            for (int d = 0; d < 64; ++d) red[lane * 65 + d] = acc[d];
-            __syncwarp();
-            if ((lane >> 4) == half) {
-                const int c = (lane & 15) * 4;
-                for (int l2 = 0; l2 < 32; ++l2) {
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) o[e] += red[l2 * 65 + c + e];
-                }
-            }
-            __syncwarp();
-        }
-        write_final_row(p, r, qh, lane, o, M, L);
-        return;
-    }
     float M = -INFINITY;
     for (int s = lane; s < ns; s += 32) M = fmaxf(M, __ldcg(ml + s * mstride).x);
 #pragma unroll
@@ -341,41 +298,6 @@ __device__ __forceinline__ void append_row(const Params& p, const Desc& d, int l
     *reinterpret_cast<uint4*>(dst) = __ldg(reinterpret_cast<const uint4*>(src));
 }
 
-// Announce this warp's published split partials: one fence for the whole list
-// (release), then one relaxed counter bump per item; for every (request, kv
-// head) whose count completes here, this warp merges its GROUP query heads.
-// `pend` holds (request | head << 16, nsplit) pairs; `red` is a drained stage
-// area for wide merges (nullptr mid-kernel).
-template <int GROUP>
-__device__ __forceinline__ void announce_splits(const Params& p, const int2* pend, int n, int lane, float* red) {
-    __syncwarp();
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    for (int base = 0; base < n; base += 32) {
-        int r = 0, head = 0;
-        bool last = false;
-        if (base + lane < n) {
-            const int2 e = pend[base + lane];
-            r = e.x & 0xffff;
-            head = e.x >> 16;
-            int32_t* sem = p.sem + static_cast<int64_t>(r) * p.n_kv + head;
-            const int prev = atomicAdd(sem, 1);
-            last = prev == e.y - 1;
-            if (last) *sem = 0;  // re-arm for the next launch (stream-ordered)
-        }
-        unsigned mask = __ballot_sync(0xffffffffu, last);
-        if (mask != 0u) {
-            asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire the other splits
-            while (mask != 0u) {
-                const int j = __ffs(mask) - 1;
-                mask &= mask - 1u;
-                const int rj = __shfl_sync(0xffffffffu, r, j);
-                const int hj = __shfl_sync(0xffffffffu, head, j);
-                for (int g = 0; g < GROUP; ++g) merge_row(p, rj, hj * GROUP + g, lane, red);
-            }
-        }
-    }
-}
-
 // ------------------------------------------------------------- q staging
 // MHA: lane (t = lane & 15, half = lane >> 4) keeps the 64 q dims of its half.
 template <int GROUP>
@@ -398,19 +320,20 @@ struct QRegs<1> {
     }
 };
 
-// GQA: A fragments (rows = query heads of the group, 8 k-steps of 16 dims).
+// GQA: B fragments of Q^T (k = 16 dims per step, n = the GROUP heads padded to 8):
+// lane holds Q[head = lane/4][dims 16ks + 2(lane%4) .. +1] and the same +8.
 template <int GROUP>
 struct QRegs {
     uint32_t v[16];
     __device__ __forceinline__ void load(const Params& p, const Desc& d, int lane) {
-        const int qrow = lane >> 2, qcol = (lane & 3) * 2;
-        const bool rv = qrow < GROUP;
+        const int head = lane >> 2, kc = (lane & 3) * 2;
+        const bool hv = head < GROUP;
         const __nv_bfloat16* src =
-            p.q + (static_cast<int64_t>(d.r) * p.n_q + d.head * GROUP + (rv ? qrow : 0)) * kD;
+            p.q + (static_cast<int64_t>(d.r) * p.n_q + d.head * GROUP + (hv ? head : 0)) * kD;
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
-            v[2 * ks] = rv ? __ldg(reinterpret_cast<const uint32_t*>(src + ks * 16 + qcol)) : 0u;
-            v[2 * ks + 1] = rv ? __ldg(reinterpret_cast<const uint32_t*>(src + ks * 16 + 8 + qcol)) : 0u;
+            v[2 * ks] = hv ? __ldg(reinterpret_cast<const uint32_t*>(src + ks * 16 + kc)) : 0u;
+            v[2 * ks + 1] = hv ? __ldg(reinterpret_cast<const uint32_t*>(src + ks * 16 + 8 + kc)) : 0u;
         }
     }
 };
@@ -525,123 +448,141 @@ struct Acc<1> {
     }
 };
 
+// GQA: tokens are the MMA M dimension.  S^T[16 tok x 8 heads] = K[16 x 128] Q^T
+// (8 HMMA: all 16 M rows are real tokens), then O^T[128 d x 8 heads] += V^T P^T
+// (8 HMMA, A = V^T via ldmatrix.trans).  A lane owns query heads 2(lane%4),
+// 2(lane%4)+1 in both the S and the O fragments, so the online-softmax state is
+// per lane and the rescale needs no data movement; P^T crosses lanes once per
+// page through a 256-byte shared-memory transpose.
 template <int GROUP>
 struct Acc {
-    float m, l;
-    float o[16][4];  // full C fragments; rows 8-15 (padding heads) stay exactly 0
+    float m[2], l[2];  // heads h0 = 2(lane%4), h0+1
+    float o[8][4];     // O^T fragments: d = 16mt + lane/4 (+8), heads h0, h0+1
     __device__ __forceinline__ void reset() {
-        m = -INFINITY;
-        l = 0.f;
+        m[0] = m[1] = -INFINITY;
+        l[0] = l[1] = 0.f;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+        for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
     }
-    template <bool PARTIAL>
-    __device__ __forceinline__ void pv(const uint32_t* pa, uint32_t vs, int valid, int lane) {
-        const int qcol = (lane & 3) * 2;
-        const int trow = (lane & 7) + ((lane >> 3) & 1) * 8;
-#pragma unroll
-        for (int dn = 0; dn < 16; dn += 2) {
-            uint32_t b0, b1, b2, b3;
-            ldsm_x4_t(vs + swz(trow, dn + (lane >> 4)), b0, b1, b2, b3);
-            if constexpr (PARTIAL) {
-                // rows >= valid may hold stale data: P is 0 there but 0 * NaN = NaN
-                b0 = mask_tokens(b0, qcol, valid);
-                b2 = mask_tokens(b2, qcol, valid);
-                b1 = mask_tokens(b1, qcol + 8, valid);
-                b3 = mask_tokens(b3, qcol + 8, valid);
-            }
-            mma_bf16(o[dn], pa[0], pa[1], b0, b1);
-            mma_bf16(o[dn + 1], pa[0], pa[1], b2, b3);
-        }
-    }
-    __device__ __forceinline__ void page(const QRegs<GROUP>& q, uint32_t ks, uint32_t vs, uint32_t,
-                                         __nv_bfloat16*, int valid, float scale, int lane) {
-        const int qcol = (lane & 3) * 2;
-        // S = Q K^T: two n-tiles of 8 tokens; even/odd k-steps accumulate in
-        // separate fragments so the HMMA dependency chains are 4 deep, not 8
-        float sa[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-        float sb[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    __device__ __forceinline__ void page(const QRegs<GROUP>& q, uint32_t ks, uint32_t vs, uint32_t sp,
+                                         __nv_bfloat16* pt, int valid, float scale, int lane) {
+        const int tA = lane >> 2, tB = tA + 8;     // this lane's token rows
+        const int hc = (lane & 3) * 2;             // this lane's head pair
+        // ---- S^T = K Q^T (two accumulators: 4-deep HMMA chains)
+        float sa[4] = {0.f, 0.f, 0.f, 0.f}, sb[4] = {0.f, 0.f, 0.f, 0.f};
+        const int arow = (lane & 7) + ((lane >> 3) & 1) * 8;
 #pragma unroll
         for (int kk = 0; kk < 8; kk += 2) {
-#pragma unroll
-            for (int nt = 0; nt < 2; ++nt) {
-                uint32_t b0, b1, b2, b3;
-                ldsm_x4(ks + swz(nt * 8 + (lane & 7), 2 * kk + (lane >> 3)), b0, b1, b2, b3);
-                mma_bf16(sa[nt], q.v[2 * kk], q.v[2 * kk + 1], b0, b1);
-                mma_bf16(sb[nt], q.v[2 * kk + 2], q.v[2 * kk + 3], b2, b3);
-            }
+            uint32_t a0, a1, a2, a3, c0, c1, c2, c3;
+            ldsm_x4(ks + swz(arow, 2 * kk + (lane >> 4)), a0, a1, a2, a3);
+            ldsm_x4(ks + swz(arow, 2 * kk + 2 + (lane >> 4)), c0, c1, c2, c3);
+            mma_m16(sa, a0, a1, a2, a3, q.v[2 * kk], q.v[2 * kk + 1]);
+            mma_m16(sb, c0, c1, c2, c3, q.v[2 * kk + 2], q.v[2 * kk + 3]);
         }
+        // lane: s[0] = (tA, h0), s[1] = (tA, h1), s[2] = (tB, h0), s[3] = (tB, h1)
         float sv[4];
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
+        for (int e = 0; e < 4; ++e) {
+            const int tok = (e < 2) ? tA : tB;
+            sv[e] = (tok < valid) ? (sa[e] + sb[e]) * scale : -INFINITY;
+        }
+        float mx0 = fmaxf(sv[0], sv[2]), mx1 = fmaxf(sv[1], sv[3]);
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int tok = nt * 8 + qcol + e;
-                sv[nt * 2 + e] = (tok < valid) ? (sa[nt][e] + sb[nt][e]) * scale : -INFINITY;
+        for (int off = 4; off <= 16; off <<= 1) {
+            mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+            mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+        }
+        const float mn0 = fmaxf(m[0], mx0), mn1 = fmaxf(m[1], mx1);
+        if (__any_sync(0xffffffffu, (mn0 > m[0]) || (mn1 > m[1]))) {
+            const float al0 = exp2f(m[0] - mn0), al1 = exp2f(m[1] - mn1);
+            l[0] *= al0;
+            l[1] *= al1;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                o[i][0] *= al0;
+                o[i][1] *= al1;
+                o[i][2] *= al0;
+                o[i][3] *= al1;
             }
         }
-        float mx = fmaxf(fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3]));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-        const float m_new = fmaxf(m, mx);
-        // rescale only when some row's running max moved (rare after the first pages)
-        if (__any_sync(0xffffffffu, m_new > m)) {
-            const float alpha = exp2f(m - m_new);
-            l *= alpha;
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                o[i][0] *= alpha;
-                o[i][1] *= alpha;
-            }
-        }
-        m = m_new;
-        uint32_t pa[2];
-        float psum = 0.f;
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-            pa[nt] = pack_bf16(exp2f(sv[nt * 2] - m_new), exp2f(sv[nt * 2 + 1] - m_new));
-            psum += bf16_lo(pa[nt]) + bf16_hi(pa[nt]);
-        }
-        l += psum;
-        // O += P V: A = P (the S fragments, bf16), B = V tile via ldmatrix.trans
+        m[0] = mn0;
+        m[1] = mn1;
+        const __nv_bfloat16 p0 = __float2bfloat16_rn(exp2f(sv[0] - mn0));
+        const __nv_bfloat16 p1 = __float2bfloat16_rn(exp2f(sv[1] - mn1));
+        const __nv_bfloat16 p2 = __float2bfloat16_rn(exp2f(sv[2] - mn0));
+        const __nv_bfloat16 p3 = __float2bfloat16_rn(exp2f(sv[3] - mn1));
+        l[0] += __bfloat162float(p0) + __bfloat162float(p2);
+        l[1] += __bfloat162float(p1) + __bfloat162float(p3);
+        // ---- P^T -> B fragments (k = tokens, n = heads) via pt[head][16 tokens]
+        pt[hc * 16 + tA] = p0;
+        pt[(hc + 1) * 16 + tA] = p1;
+        pt[hc * 16 + tB] = p2;
+        pt[(hc + 1) * 16 + tB] = p3;
+        __syncwarp();
+        const uint32_t pb0 = *reinterpret_cast<const uint32_t*>(pt + (lane >> 2) * 16 + hc);
+        const uint32_t pb1 = *reinterpret_cast<const uint32_t*>(pt + (lane >> 2) * 16 + 8 + hc);
+        // ---- O^T += V^T P^T over 8 d-tiles of 16
+        const int vrow = (lane & 7) + (lane >> 4) * 8;
         if (valid == kPage) {
-            pv<false>(pa, vs, valid, lane);
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+                uint32_t a0, a1, a2, a3;
+                ldsm_x4_t(vs + swz(vrow, 2 * mt + ((lane >> 3) & 1)), a0, a1, a2, a3);
+                mma_m16(o[mt], a0, a1, a2, a3, pb0, pb1);
+            }
         } else {
-            pv<true>(pa, vs, valid, lane);
+            // stale rows >= valid: P is 0 there but 0 * NaN = NaN, so mask V too
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+                uint32_t a0, a1, a2, a3;
+                ldsm_x4_t(vs + swz(vrow, 2 * mt + ((lane >> 3) & 1)), a0, a1, a2, a3);
+                a0 = mask_tokens(a0, hc, valid);
+                a1 = mask_tokens(a1, hc, valid);
+                a2 = mask_tokens(a2, hc + 8, valid);
+                a3 = mask_tokens(a3, hc + 8, valid);
+                mma_m16(o[mt], a0, a1, a2, a3, pb0, pb1);
+            }
         }
+        __syncwarp();  // pt is rewritten by the next page
     }
     __device__ __forceinline__ bool finish(const Params& p, const Desc& d, int lane) {
-        float lt = l;
-        lt += __shfl_xor_sync(0xffffffffu, lt, 1);
-        lt += __shfl_xor_sync(0xffffffffu, lt, 2);
-        const int qrow = lane >> 2, qcol = (lane & 3) * 2;
-        const bool rv = qrow < GROUP;
-        const int qh = d.head * GROUP + qrow;
-        if (d.nsplit == 1) {
-            if (rv) {
+        float lt0 = l[0], lt1 = l[1];
+#pragma unroll
+        for (int off = 4; off <= 16; off <<= 1) {
+            lt0 += __shfl_xor_sync(0xffffffffu, lt0, off);
+            lt1 += __shfl_xor_sync(0xffffffffu, lt1, off);
+        }
+        const int hc = (lane & 3) * 2, dr = lane >> 2;
+        const bool nsplit1 = d.nsplit == 1;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int h = hc + e;
+            if (h >= GROUP) continue;
+            const int qh = d.head * GROUP + h;
+            const float lt = e ? lt1 : lt0, mm = e ? m[1] : m[0];
+            if (nsplit1) {
                 const float inv = lt > 0.f ? 1.f / lt : 0.f;
                 __nv_bfloat16* dst = p.out + (static_cast<int64_t>(d.r) * p.n_q + qh) * kD;
 #pragma unroll
-                for (int nt = 0; nt < 16; ++nt) {
-                    *reinterpret_cast<uint32_t*>(dst + nt * 8 + qcol) = pack_bf16(o[nt][0] * inv, o[nt][1] * inv);
+                for (int mt = 0; mt < 8; ++mt) {
+                    dst[16 * mt + dr] = __float2bfloat16_rn(o[mt][e] * inv);
+                    dst[16 * mt + dr + 8] = __float2bfloat16_rn(o[mt][2 + e] * inv);
                 }
-                if (p.lse != nullptr && (lane & 3) == 0) {
-                    p.lse[static_cast<int64_t>(d.r) * p.n_q + qh] =
-                        lt > 0.f ? (m + __log2f(lt)) / kLog2e : -INFINITY;
+                if (p.lse != nullptr && dr == 0) {
+                    p.lse[static_cast<int64_t>(d.r) * p.n_q + qh] = lt > 0.f ? (mm + __log2f(lt)) / kLog2e : -INFINITY;
                 }
-            }
-            return false;
-        }
-        if (rv) {
-            const int64_t slot = static_cast<int64_t>(d.slot) * p.n_q + qh;
-            float* dst = p.part_o + slot * kD;
+            } else {
+                const int64_t slot = static_cast<int64_t>(d.slot) * p.n_q + qh;
+                float* dst = p.part_o + slot * kD;
 #pragma unroll
-            for (int nt = 0; nt < 16; ++nt) {
-                __stcg(reinterpret_cast<float2*>(dst + nt * 8 + qcol), make_float2(o[nt][0], o[nt][1]));
+                for (int mt = 0; mt < 8; ++mt) {
+                    __stcg(dst + 16 * mt + dr, o[mt][e]);
+                    __stcg(dst + 16 * mt + dr + 8, o[mt][2 + e]);
+                }
+                if (dr == 0) __stcg(p.part_ml + slot, make_float2(mm, lt));
             }
-            if ((lane & 3) == 0) __stcg(p.part_ml + slot, make_float2(m, lt));
         }
-        return true;
+        return !nsplit1;
     }
 };
 
@@ -654,16 +595,14 @@ decode_attn_kernel(const Params p) {
     extern __shared__ __align__(1024) char smem_raw[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    // per warp: S stages (8 KiB) | S mbarriers (64 B) | p scratch (64 B) | desc ring
+    // per warp: S stages (8 KiB) | S mbarriers (64 B) | desc ring (<= 288 B) | P scratch (256 B @ +512)
     constexpr int kWarpBytes = S * kStageBytes + kWarpExtra;
     char* wbase = smem_raw + warp * kWarpBytes;
     const uint32_t stage0 = smem_u32(wbase);
     const uint32_t bar0 = smem_u32(wbase + S * kStageBytes);
-    __nv_bfloat16* scratch = reinterpret_cast<__nv_bfloat16*>(wbase + S * kStageBytes + 64);
+    __nv_bfloat16* scratch = reinterpret_cast<__nv_bfloat16*>(wbase + S * kStageBytes + 512);
     const uint32_t sp = smem_u32(scratch);
-    Desc* ring = reinterpret_cast<Desc*>(wbase + S * kStageBytes + 128);
-    int2* pend = reinterpret_cast<int2*>(wbase + S * kStageBytes + 512);
-    int npend = 0;
+    Desc* ring = reinterpret_cast<Desc*>(wbase + S * kStageBytes + 64);
 
     if (lane == 0) {
         for (int s = 0; s < S; ++s) mbar_init(bar0 + 8 * s, 1);
@@ -761,21 +700,9 @@ decode_attn_kernel(const Params p) {
                 qn_ready = true;
             }
         }
-        if (acc.finish(p, cd, lane)) {  // published a split partial: remember it
-            if (lane == 0) pend[npend] = make_int2(cd.r | (cd.head << 16), cd.nsplit);
-            if (++npend == kPendMax) {
-                announce_splits<GROUP>(p, pend, npend, lane, nullptr);
-                npend = 0;
-            }
-        }
+        acc.finish(p, cd, lane);  // final row (single split) or a partial for the merge kernel
     }
 
-    // ---- K2: announce the remaining split partials; last arrivals merge.  Warps
-    // with nothing left exit at once, so the next layer's CTAs can take their SM.
-    if (npend > 0) {
-        float* red = S * kStageBytes >= 32 * 65 * 4 ? reinterpret_cast<float*>(wbase) : nullptr;  // drained
-        announce_splits<GROUP>(p, pend, npend, lane, red);
-    }
     if (p.warp_ts != nullptr && lane == 0) {
         unsigned long long ts_end;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts_end));
@@ -783,13 +710,34 @@ decode_attn_kernel(const Params p) {
         p.warp_ts[2 * w] = ts_begin;
         p.warp_ts[2 * w + 1] = ts_end;
     }
-    // last warp out re-arms the counters of this launch parity
+    // last warp out re-arms the work counters of this launch parity
     if (lane == 0) {
         const uint32_t done = atomicAdd(p.work + 1, 1u);
         if (done == static_cast<uint32_t>(p.total_warps) - 1u) {
             p.work[0] = 0u;
             p.work[1] = 0u;
         }
+    }
+}
+
+// ============================================================ split merge (K2)
+// One warp per (request, query head) of every split request.  Chained with
+// programmatic dependent launch: its CTAs become resident while the streaming
+// kernel runs, let the NEXT layer's streaming kernel launch at once (so its KV
+// prefetch overlaps this merge), and park on griddepcontrol.wait until the
+// streaming grid has completed (which also publishes its partial stores) — no
+// fences or semaphores anywhere on the streaming path.
+constexpr int kMergeWarps = 4;
+
+__global__ void __launch_bounds__(kMergeWarps * 32)
+merge_splits_kernel(const Params p, const int32_t* __restrict__ merge_reqs, int32_t rows) {
+    grid_dep_launch();
+    grid_dep_wait();
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    for (int row = blockIdx.x * kMergeWarps + warp; row < rows; row += gridDim.x * kMergeWarps) {
+        const int r = __ldg(merge_reqs + row / p.n_q);
+        merge_row(p, r, row % p.n_q, lane);
     }
 }
 
@@ -894,6 +842,24 @@ cudaError_t attn_occupancy(int group, int* blocks_per_sm) {
     return dispatch(group, true, blocks_per_sm, nullptr, 0, false, nullptr);
 }
 
+cudaError_t merge_launch(const Params& p, const int32_t* merge_reqs, int32_t n_merge, int sms, bool pdl,
+                         cudaStream_t st) {
+    const int32_t rows = n_merge * p.n_q;
+    if (rows <= 0) return cudaSuccess;
+    const int blocks = min((rows + kMergeWarps - 1) / kMergeWarps, 2 * sms);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(kMergeWarps * 32);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, merge_splits_kernel, p, merge_reqs, rows);
+}
+
 cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st) {
     Params p;
     p.q = static_cast<const __nv_bfloat16*>(a.q);
@@ -921,7 +887,9 @@ cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st) {
     p.scale_log2 = a.sm_scale * kLog2e;
     p.warp_ts = a.warp_ts;
     if (p.num_items <= 0) return cudaSuccess;
-    return dispatch(a.group, false, nullptr, &p, a.grid, a.pdl, st);
+    cudaError_t e = dispatch(a.group, false, nullptr, &p, a.grid, a.pdl, st);
+    if (e != cudaSuccess) return e;
+    return merge_launch(p, a.merge_reqs, a.n_merge, a.sms, a.pdl, st);
 }
 
 }  // namespace asv

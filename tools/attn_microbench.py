@@ -69,7 +69,13 @@ if __name__ == "__main__":
         "C4_13b_gqa8_b32": (40, 8, 40, rng.integers(1024, 8192, 32).tolist()),
         "gqa_7b_b64": (32, 8, 32, rng.integers(1024, 4096, 64).tolist()),
         "mha_b1_128k": (32, 32, 4, [131072]),
+        # same launches with one layer per page: page stride 64 KiB / 256 KiB instead of
+        # 2.5 MiB / 8 MiB (probes address-stride / TLB effects of the all-layers page)
+        "C4_13b_gqa8_b32_L1": (40, 8, 1, None),
+        "C2_aligned_b13_8k_L1": (32, 32, 1, None),
     }
+    cases["C4_13b_gqa8_b32_L1"] = (40, 8, 1, cases["C4_13b_gqa8_b32"][3])
+    cases["C2_aligned_b13_8k_L1"] = (32, 32, 1, cases["C2_aligned_b13_8k"][3])
     for name, (nq, nkv, L, seq) in cases.items():
         if a.case and a.case != name:
             continue
