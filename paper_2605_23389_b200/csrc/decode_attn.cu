@@ -43,6 +43,7 @@ constexpr int kPage = 16;
 constexpr int kRowBytes = kD * 2;               // 256
 constexpr int kBlockBytes = kPage * kRowBytes;  // 4096: one (page, layer, K|V, head) block
 constexpr int kStageBytes = 2 * kBlockBytes;    // K + V
+constexpr int kDefaultL2Prefetch = 0;           // L2 bulk prefetch beyond the TMA ring: measured slower on B200, off
 constexpr int kWarpExtra = 768;                 // per warp: mbarriers | descriptor ring | P scratch
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -70,6 +71,7 @@ struct Params {
     const int32_t* merge_reqs;  // requests split more than once
     int32_t merge_rows;         // merge_reqs count * n_q
     float scale_log2;
+    int32_t l2_prefetch;          // pages beyond the TMA ring prefetched into L2 (0: off)
     unsigned long long* warp_ts;  // optional [total_warps][2] %globaltimer start/end (bubble probe, I1)
 };
 
@@ -110,6 +112,10 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
         " [%0], [%1], %2, [%3], %4;" ::"r"(dst),
         "l"(src), "r"(bytes), "r"(bar), "l"(pol)
         : "memory");
+}
+// Bulk prefetch of a block into L2 (no shared memory, no completion tracking).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
@@ -235,54 +241,6 @@ __device__ __forceinline__ void write_final_row(const Params& p, int r, int qh, 
     if (p.lse != nullptr && lane == 0) {
         p.lse[static_cast<int64_t>(r) * p.n_q + qh] = l > 0.f ? (m + __log2f(l)) / kLog2e : -INFINITY;
     }
-}
-
-// Log-sum-exp merge of the split partials of (request r, query head qh): every
-// lane owns dims 4*lane..4*lane+3 and walks the splits with 8 loads in flight
-// (coalesced 512-byte rows; a lane-per-split variant measured slower on B200).
-__device__ __forceinline__ void merge_row(const Params& p, int r, int qh, int lane) {
-    const int s0 = __ldg(p.split_base + r);
-    const int ns = __ldg(p.split_base + r + 1) - s0;
-    const float2* ml = p.part_ml + static_cast<int64_t>(s0) * p.n_q + qh;
-    const int64_t mstride = p.n_q;
-    float M = -INFINITY;
-    for (int s = lane; s < ns; s += 32) M = fmaxf(M, __ldcg(ml + s * mstride).x);
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-    float L = 0.f;
-    for (int s = lane; s < ns; s += 32) {
-        const float2 v = __ldcg(ml + s * mstride);
-        L += (v.x == -INFINITY) ? 0.f : exp2f(v.x - M) * v.y;
-    }
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
-    const float4* po = reinterpret_cast<const float4*>(p.part_o + (static_cast<int64_t>(s0) * p.n_q + qh) * kD) + lane;
-    const int64_t ostride = static_cast<int64_t>(p.n_q) * (kD / 4);
-    float o[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int base = 0; base < ns; base += 8) {
-        float4 v[8];
-        float w[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int s = base + j;
-            if (s < ns) {
-                v[j] = __ldcg(po + s * ostride);
-                const float mx = __ldcg(ml + s * mstride).x;
-                w[j] = (mx == -INFINITY) ? 0.f : exp2f(mx - M);
-            } else {
-                v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-                w[j] = 0.f;
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            o[0] += w[j] * v[j].x;
-            o[1] += w[j] * v[j].y;
-            o[2] += w[j] * v[j].z;
-            o[3] += w[j] * v[j].w;
-        }
-    }
-    write_final_row(p, r, qh, lane, o, M, L);
 }
 
 // KV append (K3): lanes 0-15 write the K row, 16-31 the V row (16 B each, swizzled).
@@ -643,6 +601,24 @@ decode_attn_kernel(const Params p) {
     };
     auto issue = [&](int slot) {
         const int phys = __shfl_sync(0xffffffffu, cur_phys, ppage - cur.pb);
+        // L2 prefetch of the page `l2_prefetch` positions further along this
+        // warp's stream (current item, else the looked-ahead next item)
+        if (p.l2_prefetch > 0) {
+            const int ahead = ppage + p.l2_prefetch;
+            int pf = -1, pf_head = cur.head;
+            if (ahead < cur.pe) {
+                pf = __shfl_sync(0xffffffffu, cur_phys, ahead - cur.pb);
+            } else if (k1 < static_cast<uint32_t>(p.num_items) && ahead - cur.pe < nxt.pe - nxt.pb) {
+                pf = __shfl_sync(0xffffffffu, nxt_phys, ahead - cur.pe);
+                pf_head = nxt.head;
+            }
+            if (pf >= 0 && lane == 0) {
+                const char* blk = p.pool + static_cast<int64_t>(pf) * p.page_bytes + p.layer_off +
+                                  static_cast<int64_t>(pf_head) * kBlockBytes;
+                bulk_prefetch_l2(blk, kBlockBytes);
+                bulk_prefetch_l2(blk + p.v_off, kBlockBytes);
+            }
+        }
         if (lane == 0) {
             const char* kblk = p.pool + static_cast<int64_t>(phys) * p.page_bytes + p.layer_off +
                                static_cast<int64_t>(cur.head) * kBlockBytes;
@@ -729,15 +705,87 @@ decode_attn_kernel(const Params p) {
 // fences or semaphores anywhere on the streaming path.
 constexpr int kMergeWarps = 4;
 
-__global__ void __launch_bounds__(kMergeWarps * 32)
+// One CTA per (request, query head) row: the 8 warps take every 8th split and
+// keep an online (max, sum, o[4 dims per lane]) state over 8-split batches of
+// coalesced loads, then the 8 states are combined through shared memory.
+__global__ void __launch_bounds__(kMergeWarps * 32, 6)
 merge_splits_kernel(const Params p, const int32_t* __restrict__ merge_reqs, int32_t rows) {
     grid_dep_launch();
     grid_dep_wait();
+    __shared__ float s_o[kMergeWarps][kD];
+    __shared__ float s_m[kMergeWarps], s_l[kMergeWarps];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    for (int row = blockIdx.x * kMergeWarps + warp; row < rows; row += gridDim.x * kMergeWarps) {
+    for (int row = blockIdx.x; row < rows; row += gridDim.x) {
         const int r = __ldg(merge_reqs + row / p.n_q);
-        merge_row(p, r, row % p.n_q, lane);
+        const int qh = row % p.n_q;
+        const int s0 = __ldg(p.split_base + r);
+        const int ns = __ldg(p.split_base + r + 1) - s0;
+        const float2* ml = p.part_ml + static_cast<int64_t>(s0) * p.n_q + qh;
+        const float4* po = reinterpret_cast<const float4*>(p.part_o + (static_cast<int64_t>(s0) * p.n_q + qh) * kD) + lane;
+        const int64_t mstride = p.n_q, ostride = static_cast<int64_t>(p.n_q) * (kD / 4);
+        float M = -INFINITY, L = 0.f;
+        float o[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int base = warp; base < ns; base += 8 * kMergeWarps) {
+            float4 v[8];
+            float2 w[8];
+            float bm = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int sidx = base + j * kMergeWarps;
+                if (sidx < ns) {
+                    v[j] = __ldcg(po + sidx * ostride);
+                    w[j] = __ldcg(ml + sidx * mstride);
+                } else {
+                    v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    w[j] = make_float2(-INFINITY, 0.f);
+                }
+                bm = fmaxf(bm, w[j].x);
+            }
+            const float mn = fmaxf(M, bm);
+            if (mn == -INFINITY) continue;
+            const float a = exp2f(M - mn);
+            L *= a;
+            o[0] *= a;
+            o[1] *= a;
+            o[2] *= a;
+            o[3] *= a;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float e = (w[j].x == -INFINITY) ? 0.f : exp2f(w[j].x - mn);
+                L += e * w[j].y;
+                o[0] += e * v[j].x;
+                o[1] += e * v[j].y;
+                o[2] += e * v[j].z;
+                o[3] += e * v[j].w;
+            }
+            M = mn;
+        }
+        *reinterpret_cast<float4*>(&s_o[warp][4 * lane]) = make_float4(o[0], o[1], o[2], o[3]);
+        if (lane == 0) {
+            s_m[warp] = M;
+            s_l[warp] = L;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            float Mt = -INFINITY;
+#pragma unroll
+            for (int w = 0; w < kMergeWarps; ++w) Mt = fmaxf(Mt, s_m[w]);
+            float ot[4] = {0.f, 0.f, 0.f, 0.f};
+            float Lt = 0.f;
+#pragma unroll
+            for (int w = 0; w < kMergeWarps; ++w) {
+                const float e = (s_m[w] == -INFINITY) ? 0.f : exp2f(s_m[w] - Mt);
+                const float4 x = *reinterpret_cast<const float4*>(&s_o[w][4 * lane]);
+                ot[0] += e * x.x;
+                ot[1] += e * x.y;
+                ot[2] += e * x.z;
+                ot[3] += e * x.w;
+                Lt += e * s_l[w];
+            }
+            write_final_row(p, r, qh, lane, ot, Mt, Lt);
+        }
+        __syncthreads();
     }
 }
 
@@ -846,7 +894,7 @@ cudaError_t merge_launch(const Params& p, const int32_t* merge_reqs, int32_t n_m
                          cudaStream_t st) {
     const int32_t rows = n_merge * p.n_q;
     if (rows <= 0) return cudaSuccess;
-    const int blocks = min((rows + kMergeWarps - 1) / kMergeWarps, 2 * sms);
+    const int blocks = min(rows, 6 * sms);  // one CTA per row, grid-strided beyond 6 CTAs/SM
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(blocks);
     cfg.blockDim = dim3(kMergeWarps * 32);
@@ -886,6 +934,13 @@ cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st) {
     p.merge_rows = a.n_merge * a.n_q;
     p.scale_log2 = a.sm_scale * kLog2e;
     p.warp_ts = a.warp_ts;
+    {
+        static const int pf = [] {
+            const char* e = getenv("ASV_L2_PREFETCH");
+            return e != nullptr ? atoi(e) : kDefaultL2Prefetch;
+        }();
+        p.l2_prefetch = pf;
+    }
     if (p.num_items <= 0) return cudaSuccess;
     cudaError_t e = dispatch(a.group, false, nullptr, &p, a.grid, a.pdl, st);
     if (e != cudaSuccess) return e;

@@ -208,8 +208,10 @@ class GpuExecutor : public prefixsim::EngineObserver {
         ASV_CUDA(cudaSetDevice(xfer_device()));
         ASV_CUDA(cudaStreamCreateWithFlags(&xfer_, cudaStreamNonBlocking));
         ASV_CUDA(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));  // other PCIe direction
+        ASV_CUDA(cudaStreamCreateWithFlags(&urgent_, cudaStreamNonBlocking));  // strays / swap-ins
         xfer_ev_.init(xfer_device(), 4096);
         d2h_ev_.init(xfer_device(), 4096);
+        urgent_ev_.init(xfer_device(), 4096);
         ASV_CUDA(cudaSetDevice(o.decode_device));
         p2p_ev_.init(o.decode_device, 4096);
         // host pool
@@ -295,6 +297,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
         cudaStreamDestroy(p2p_);
         cudaStreamDestroy(xfer_);
         cudaStreamDestroy(d2h_);
+        cudaStreamDestroy(urgent_);
     }
 
     // ---------------------------------------------------------- observer
@@ -342,14 +345,14 @@ class GpuExecutor : public prefixsim::EngineObserver {
                 break;
             }
             case ASV_XFER_STRAY_PREFETCH:
-                begin_xfer_group();
+                begin_xfer_group(Lane::kUrgent);
                 fetch_from_host(t.request_id, staging_pool());
                 end_xfer_group();
                 break;
             case ASV_XFER_ADMIT:
                 if (!aligned_) {
                     // FCFS swap-in / disaggregated admit: host pool -> decode pages (PCIe)
-                    begin_xfer_group();
+                    begin_xfer_group(Lane::kUrgent);
                     fetch_from_host(t.request_id, &dec_);
                     end_xfer_group();
                 } else {
@@ -359,7 +362,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
                 break;
             case ASV_XFER_EVICT:
                 if (!aligned_) {
-                    begin_xfer_group(true);
+                    begin_xfer_group(Lane::kD2H);
                     write_back_to_host(t.request_id);
                     end_xfer_group();
                 } else {
@@ -368,7 +371,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
                 break;
             case ASV_XFER_SPILL:
             case ASV_XFER_FLUSH:
-                begin_xfer_group(true);
+                begin_xfer_group(Lane::kD2H);
                 write_back_to_host(t.request_id);
                 end_xfer_group();
                 break;
@@ -487,6 +490,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
         ASV_CUDA(cudaSetDevice(xfer_device()));
         ASV_CUDA(cudaStreamSynchronize(xfer_));
         ASV_CUDA(cudaStreamSynchronize(d2h_));
+        ASV_CUDA(cudaStreamSynchronize(urgent_));
         ASV_CUDA(cudaSetDevice(o_.decode_device));
         ASV_CUDA(cudaStreamSynchronize(p2p_));
         for (int64_t e = std::max<int64_t>(0, executed_ - ring_); e < executed_; ++e) retire(static_cast<size_t>(e % ring_));
@@ -574,15 +578,19 @@ class GpuExecutor : public prefixsim::EngineObserver {
     }
 
     // group copies issued by one decision so one event pair times them
-    // H2D groups run on xfer_, D2H groups on d2h_ (both PCIe directions at once)
-    void begin_xfer_group(bool d2h = false) {
+    // Batch prefetches run on xfer_, small urgent H2D moves (strays, swap-ins) on
+    // urgent_ so they never queue behind a whole batch, D2H on d2h_ (both PCIe
+    // directions at once).
+    enum class Lane { kBulk, kUrgent, kD2H };
+    void begin_xfer_group(Lane lane_sel = Lane::kBulk) {
         group_timed_ = copies_active() && in_window();
-        cur_ = d2h ? d2h_ : xfer_;
-        cur_ev_ = d2h ? &d2h_ev_ : &xfer_ev_;
+        cur_ = lane_sel == Lane::kD2H ? d2h_ : (lane_sel == Lane::kUrgent ? urgent_ : xfer_);
+        cur_ev_ = lane_sel == Lane::kD2H ? &d2h_ev_ : (lane_sel == Lane::kUrgent ? &urgent_ev_ : &xfer_ev_);
         if (!copies_active()) return;
         ASV_CUDA(cudaSetDevice(xfer_device()));
         // pages written/read below may have been used by the last launched iteration
-        cudaEvent_t& waited = d2h ? waited_it_end_d2h_ : waited_it_end_;
+        cudaEvent_t& waited = lane_sel == Lane::kD2H ? waited_it_end_d2h_
+                              : (lane_sel == Lane::kUrgent ? waited_it_end_urg_ : waited_it_end_);
         if (last_it_end_ != nullptr && waited != last_it_end_) {
             ASV_CUDA(cudaStreamWaitEvent(cur_, last_it_end_, 0));
             waited = last_it_end_;
@@ -647,7 +655,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
         const int64_t moved = copy_kv(r.pages, *pool, id, q.prefix_len, true);
         stats_.h2d_bytes += moved;
         if (group_timed_) stats_.h2d_bytes_window += moved;
-        group_ready_.push_back(id);
+        r.ready = cur_ev_->record(cur_);  // this request is usable as soon as its own pages land
     }
 
     void write_back_to_host(prefixsim::RequestId id) {
@@ -802,10 +810,11 @@ class GpuExecutor : public prefixsim::EngineObserver {
     bool pair_ = false;
     int64_t dec_pages_ = 0, pre_pages_ = 0;
     PagePool dec_, pre_;
-    cudaStream_t compute_ = nullptr, p2p_ = nullptr, xfer_ = nullptr, d2h_ = nullptr, cur_ = nullptr;
-    EventRing xfer_ev_, d2h_ev_, p2p_ev_;
+    cudaStream_t compute_ = nullptr, p2p_ = nullptr, xfer_ = nullptr, d2h_ = nullptr, urgent_ = nullptr,
+                 cur_ = nullptr;
+    EventRing xfer_ev_, d2h_ev_, urgent_ev_, p2p_ev_;
     EventRing* cur_ev_ = nullptr;
-    cudaEvent_t waited_it_end_d2h_ = nullptr;
+    cudaEvent_t waited_it_end_d2h_ = nullptr, waited_it_end_urg_ = nullptr;
     char* arena_ = nullptr;
     int64_t arena_pages_ = 1;
     int32_t workers_ = 0;
