@@ -297,11 +297,15 @@ def main():
         h2d_gbps = ((e2e["h2d_bytes_window"] + e2e["d2h_bytes_window"]) / (e2e["h2d_busy_ms"] * 1e-3) / 1e9
                     if e2e["h2d_busy_ms"] > 0 else None)
         p2p_gbps = e2e["p2p_bytes_window"] / (e2e["p2p_busy_ms"] * 1e-3) / 1e9 if e2e["p2p_busy_ms"] > 0 else None
+        e_steps = max(1, e2e["iterations_timed"])
+        busy_per_step = e2e["h2d_busy_ms"] / e_steps
+        exposed_per_step = max(0.0, e2e["window_ms"] / e_steps - res["window_ms"] / max(1, res["iterations_timed"]))
         prefetch = {"h2d_gbps": h2d_gbps, "h2d_roofline_gbps": 64.0, "p2p_gbps": p2p_gbps,
-                    "p2p_roofline_gbps": 770.0, "h2d_busy_ms": e2e["h2d_busy_ms"],
-                    "window_ms": e2e["window_ms"],
-                    "hidden_fraction": (1.0 - max(0.0, e2e["window_ms"] - res["window_ms"]) /
-                                        max(1e-9, e2e["h2d_busy_ms"])) if e2e["h2d_busy_ms"] > 0 else None}
+                    "p2p_roofline_gbps": 770.0, "pcie_busy_ms_per_step": busy_per_step,
+                    "pcie_utilisation": e2e["h2d_busy_ms"] / max(1e-9, e2e["window_ms"]),
+                    "exposed_ms_per_step": exposed_per_step,
+                    "hidden_fraction": (max(0.0, 1.0 - exposed_per_step / busy_per_step) if busy_per_step > 0
+                                        else None)}
 
     cpu = None
     if d.rank == 0 and d.world == 1 and not args.no_cpu_baseline:

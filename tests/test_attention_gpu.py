@@ -151,3 +151,39 @@ def test_empty_batch_raises():
         att.plan([], [0], [])
     with pytest.raises(ValueError, match="prefix lengths must be >= 1"):
         att.plan([0], [0, 1], [0])
+
+
+def test_many_short_requests(oracle):
+    """b = 300 requests of 1-40 tokens: hundreds of tiny single-page items."""
+    rng = np.random.default_rng(99)
+    seq = rng.integers(1, 41, size=300).tolist()
+    _run_case(oracle, 32, 32, 1, 0, seq, seed=81)
+
+
+@pytest.mark.parametrize("n_q,n_kv", [(32, 32), (40, 8)])
+def test_pdl_chain_of_layers_matches_oracle(oracle, n_q, n_kv):
+    """Several layers launched back to back (PDL, alternating work-counter parity):
+    every layer's output must match the oracle for that layer."""
+    from paper_2605_23389_b200 import PagedDecodeAttention
+
+    L = 4
+    seq = [700, 33, 2048, 15, 4100]
+    dev = torch.device("cuda", 0)
+    att = PagedDecodeAttention(n_q, n_kv, L, device=0)
+    pages = sum((s + 16) // 16 for s in seq) + 3
+    pool = U.random_bf16(91, pages * att.page_bytes // 2).view(np.uint8).copy()
+    indptr, indices = U.make_batch(seq, pages, 92)
+    pool_d = torch.from_numpy(pool).to(dev)
+    plan = att.plan(seq, indptr, indices)
+    outs, qs = [], []
+    for layer in range(L):
+        q = U.random_bf16(100 + layer, len(seq) * n_q * 128).reshape(len(seq), n_q, 128)
+        qs.append(q)
+        out = torch.empty(len(seq), n_q, 128, dtype=torch.bfloat16, device=dev)
+        att.run(torch.from_numpy(q.view(np.int16)).to(dev).view(torch.bfloat16), pool_d, layer, plan, out)
+        outs.append(out)
+    torch.cuda.synchronize()
+    for layer in range(L):
+        ref, _ = oracle.attention(n_q, n_kv, L, layer, qs[layer], pool, seq, indptr, indices, att.sm_scale)
+        got = outs[layer].float().cpu().numpy()
+        assert (np.abs(got - ref) <= ATOL + RTOL * np.abs(ref)).all(), f"layer {layer}"
