@@ -35,16 +35,21 @@ const char* asv_last_error(void);
 int asv_abi_version(void);
 
 /* ------------------------------------------------------------------------ */
-/* Paged KV layout (device HBM and pinned host pool share it, so KV moves are  */
-/* opaque byte copies of whole pages):                                       */
-/*   page = [num_layers][2 (K,V)][num_kv_heads][page_size=16][head_dim=128]  */
-/* bf16.  Inside each (page, layer, K|V, head) 4 KiB block the 16-byte chunk  */
-/* c of token row t is stored at chunk position c ^ (t & 7) (XOR swizzle), so */
+/* Paged KV layout.  A page holds 16 tokens (= ClusterConfig::block_size,     */
+/* cluster_sim.hpp:45) of every layer, K and V, every kv head.                */
+/*  * device pool (HBM), LAYER-MAJOR:                                          */
+/*      [num_layers][pool_pages][2 (K,V)][num_kv_heads][16][head_dim=128]      */
+/*    so one layer's slices of all pages are contiguous (dense address range   */
+/*    per decode launch);                                                      */
+/*  * host pool / transfer format, PAGE-MAJOR: one page is                      */
+/*      [num_layers][2][num_kv_heads][16][128] contiguous (asv_page_bytes).    */
+/* Every (page, layer, K|V, head) block is 4 KiB, bf16, and XOR-swizzled: the  */
+/* 16-byte chunk c of token row t is stored at chunk position c ^ (t & 7), so */
 /* a 1-D bulk TMA of the block lands bank-conflict-free in shared memory for  */
-/* both the FFMA (MHA) and ldmatrix/mma (GQA) consumers.                     */
-/* Page = 16 tokens = ClusterConfig::block_size (cluster_sim.hpp:45);         */
-/* bytes per token over all layers = ModelSpec::kv_bytes_per_token()          */
-/* (cost_model.hpp:34-36) when num_kv_heads*head_dim == hidden_dim.           */
+/* both the FFMA (MHA) and ldmatrix/mma (GQA) consumers.  KV moves are strided */
+/* byte copies (one 2-D copy per page, a 3-D copy for the valid rows of a     */
+/* partial last page): bytes moved = s * kv_bytes_per_token                    */
+/* (cost_model.hpp:34-36, cluster_sim.hpp:239-241).                            */
 /* ------------------------------------------------------------------------ */
 typedef struct asv_attn_shape {
     int32_t num_q_heads;  /* n_h */
@@ -56,9 +61,12 @@ typedef struct asv_attn_shape {
 
 /* bytes of one page (all layers, K and V) */
 int64_t asv_page_bytes(const asv_attn_shape* shape);
-/* byte offset of token row t, dim-chunk c (8 elements) of (layer, kv, head) inside a page */
+/* byte offset of element (layer, kv, head, token, dim) inside one PAGE-MAJOR (host) page */
 int64_t asv_page_offset(const asv_attn_shape* shape, int32_t layer, int32_t kv, int32_t head,
                         int32_t token, int32_t dim);
+/* byte offset of element (page, layer, kv, head, token, dim) in a LAYER-MAJOR device pool */
+int64_t asv_pool_offset(const asv_attn_shape* shape, int64_t pool_pages, int64_t page, int32_t layer,
+                        int32_t kv, int32_t head, int32_t token, int32_t dim);
 
 /* ------------------------------------------------------------------------ */
 /* Split-KV work plan (host side, K4 in SURVEY §2).  Built once per decode    */
@@ -103,8 +111,8 @@ int asv_attn_workspace_init(void* workspace, size_t bytes, void* stream);
 
 typedef struct asv_attn_args {
     const void* q;          /* [b][n_h][128] bf16, this layer */
-    void* kv_pool;          /* device page pool base (layout above) */
-    int64_t pool_pages;     /* pages in the pool (bounds checking on the plan) */
+    void* kv_pool;          /* device page pool base (layer-major layout above) */
+    int64_t pool_pages;     /* pages in the pool: the layer stride of the layer-major pool */
     int32_t layer;          /* layer slice of every page to attend over */
     const int32_t* plan_dev;/* device copy of the plan buffer */
     const asv_attn_plan* plan;
@@ -126,6 +134,27 @@ typedef struct asv_attn_args {
  * launch when pdl = 1.  Replaces the attention term of iteration_latency
  * (cost_model.hpp:112-135). */
 int asv_decode_attention(const asv_attn_shape* shape, const asv_attn_args* args, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* KV page moves (copy engines).  Replace the PRICED transfers of the          */
+/* reference (transfer_time cluster_sim.hpp:60-66; start_async_transfer /     */
+/* sync_transfer :220-232).  A request with `tokens` tokens owns               */
+/* ceil(tokens/16) pages; exactly tokens * kv_bytes_per_token bytes move:     */
+/* whole pages as 2-D copies, the valid rows of a partial last page as a 3-D   */
+/* copy.  host_pages[j] = page j of the request in the host (page-major)       */
+/* format.  Asynchronous on `stream`; *bytes_out = bytes moved.                */
+/* ------------------------------------------------------------------------ */
+/* C1: pinned host pool -> device pool (batch_prefetch / stray_prefetch, PCIe) */
+int asv_kv_copy_h2d(const asv_attn_shape* shape, void* pool, int64_t pool_pages, const int32_t* pages,
+                    int64_t tokens, const void* const* host_pages, void* stream, int64_t* bytes_out);
+/* device pool -> pinned host pool (spill / flush / FCFS swap-out, PCIe) */
+int asv_kv_copy_d2h(const asv_attn_shape* shape, const void* pool, int64_t pool_pages, const int32_t* pages,
+                    int64_t tokens, void* const* host_pages, void* stream, int64_t* bytes_out);
+/* C2/C3: device pool -> device pool, across a (prefetch, decode) pair over NVLink
+ * (admit / evict) or within one device */
+int asv_kv_copy_d2d(const asv_attn_shape* shape, void* dst_pool, int64_t dst_pool_pages, int32_t dst_device,
+                    const int32_t* dst_pages, const void* src_pool, int64_t src_pool_pages, int32_t src_device,
+                    const int32_t* src_pages, int64_t tokens, void* stream, int64_t* bytes_out);
 
 /* ------------------------------------------------------------------------ */
 /* Host-side decision path (reference API underneath, C ABI on top).          */

@@ -17,7 +17,8 @@
  *
  * Numerics: bf16 inputs widened to fp32 exactly; dot products in fp32, the
  * softmax normaliser and the weighted V sum accumulated in double.
- * Paged layout and swizzle: include/asv.h.
+ * Layout and swizzle: include/asv.h (device pool LAYER-MAJOR:
+ * [L][pool_pages][2][n_kv][16][128]).
  */
 #include <math.h>
 #include <pthread.h>
@@ -42,7 +43,7 @@ typedef struct {
     int n_q, n_kv, L, layer, batch;
     const uint16_t* q;
     const uint8_t* pool;
-    int64_t page_bytes;
+    int64_t pool_pages;
     const int32_t* seq_lens;
     const int32_t* indptr;
     const int32_t* indices;
@@ -62,12 +63,12 @@ static void one_row(const job_t* j, int r, int h) {
     float qf[128];
     for (int d = 0; d < D; ++d) qf[d] = bf16_to_f32(qv[d]);
     float* scores = (float*)malloc(sizeof(float) * (size_t)(s > 0 ? s : 1));
-    const int64_t kblk = (((int64_t)j->layer * 2 + 0) * j->n_kv + kvh) * 4096;
-    const int64_t vblk = (((int64_t)j->layer * 2 + 1) * j->n_kv + kvh) * 4096;
+    /* block (page, layer, kv, head) of the layer-major pool */
+#define BLOCK(page, kv) ((((((int64_t)j->layer * j->pool_pages + (page)) * 2 + (kv)) * j->n_kv) + kvh) * 4096)
     float mx = -INFINITY;
     for (int t = 0; t < s; ++t) {
         const int64_t page = j->indices[j->indptr[r] + t / 16];
-        const uint8_t* base = j->pool + page * j->page_bytes + kblk;
+        const uint8_t* base = j->pool + BLOCK(page, 0);
         float acc = 0.f;
         for (int d = 0; d < D; ++d) {
             uint16_t kb;
@@ -84,7 +85,7 @@ static void one_row(const job_t* j, int r, int h) {
         const double p = exp((double)scores[t] - (double)mx);
         l += p;
         const int64_t page = j->indices[j->indptr[r] + t / 16];
-        const uint8_t* base = j->pool + page * j->page_bytes + vblk;
+        const uint8_t* base = j->pool + BLOCK(page, 1);
         for (int d = 0; d < D; ++d) {
             uint16_t vb;
             memcpy(&vb, base + swz_off(t % 16, d), 2);
@@ -95,6 +96,7 @@ static void one_row(const job_t* j, int r, int h) {
     for (int d = 0; d < D; ++d) dst[d] = s > 0 ? (float)(o[d] / l) : 0.f;
     if (j->lse) j->lse[(int64_t)r * j->n_q + h] = s > 0 ? (float)((double)mx + log(l)) : -INFINITY;
     free(scores);
+#undef BLOCK
 }
 
 static void* worker(void* arg) {
@@ -113,7 +115,7 @@ static void* worker(void* arg) {
 /* out: [batch][n_q][128] fp32; lse: [batch][n_q] natural log (nullable).
  * Returns 0 on success. */
 int asv_oracle_decode_attention(int n_q, int n_kv, int num_layers, int layer, const uint16_t* q,
-                                const uint8_t* pool, int64_t page_bytes, const int32_t* seq_lens,
+                                const uint8_t* pool, int64_t pool_pages, const int32_t* seq_lens,
                                 const int32_t* indptr, const int32_t* indices, int batch,
                                 float sm_scale, float* out, float* lse, int threads) {
     if (n_kv <= 0 || n_q % n_kv != 0 || batch < 1) return 1;
@@ -125,7 +127,7 @@ int asv_oracle_decode_attention(int n_q, int n_kv, int num_layers, int layer, co
     j.batch = batch;
     j.q = q;
     j.pool = pool;
-    j.page_bytes = page_bytes;
+    j.pool_pages = pool_pages;
     j.seq_lens = seq_lens;
     j.indptr = indptr;
     j.indices = indices;

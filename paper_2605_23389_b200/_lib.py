@@ -135,6 +135,8 @@ SIGNATURES = [
     ("asv_page_bytes", C.c_int64, [C.POINTER(AttnShape)]),
     ("asv_page_offset", C.c_int64,
      [C.POINTER(AttnShape), C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
+    ("asv_pool_offset", C.c_int64,
+     [C.POINTER(AttnShape), C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
     ("asv_attn_num_workers", C.c_int, [C.POINTER(AttnShape), C.c_int, C.POINTER(C.c_int32)]),
     ("asv_attn_plan_build", C.c_int,
      [C.POINTER(AttnShape), C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
@@ -142,6 +144,15 @@ SIGNATURES = [
     ("asv_attn_workspace_bytes", C.c_size_t, [C.POINTER(AttnShape), C.c_int32, C.c_int32]),
     ("asv_attn_workspace_init", C.c_int, [C.c_void_p, C.c_size_t, C.c_void_p]),
     ("asv_decode_attention", C.c_int, [C.POINTER(AttnShape), C.POINTER(AttnArgs), C.c_void_p]),
+    ("asv_kv_copy_h2d", C.c_int,
+     [C.POINTER(AttnShape), C.c_void_p, C.c_int64, C.POINTER(C.c_int32), C.c_int64, C.POINTER(C.c_void_p),
+      C.c_void_p, C.POINTER(C.c_int64)]),
+    ("asv_kv_copy_d2h", C.c_int,
+     [C.POINTER(AttnShape), C.c_void_p, C.c_int64, C.POINTER(C.c_int32), C.c_int64, C.POINTER(C.c_void_p),
+      C.c_void_p, C.POINTER(C.c_int64)]),
+    ("asv_kv_copy_d2d", C.c_int,
+     [C.POINTER(AttnShape), C.c_void_p, C.c_int64, C.c_int32, C.POINTER(C.c_int32), C.c_void_p, C.c_int64,
+      C.c_int32, C.POINTER(C.c_int32), C.c_int64, C.c_void_p, C.POINTER(C.c_int64)]),
     ("asv_run_config_jsonl", C.c_int,
      [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
     ("asv_engine_run", C.c_int,

@@ -78,6 +78,15 @@ int64_t asv_page_offset(const asv_attn_shape* s, int32_t layer, int32_t kv, int3
     return block + token * 256 + ((c ^ (token & 7)) << 4) + (dim % 8) * 2;
 }
 
+int64_t asv_pool_offset(const asv_attn_shape* s, int64_t pool_pages, int64_t page, int32_t layer, int32_t kv,
+                        int32_t head, int32_t token, int32_t dim) {
+    if (check_shape(s) != ASV_OK) return -1;
+    const int64_t block = (((static_cast<int64_t>(layer) * pool_pages + page) * 2 + kv) * s->num_kv_heads + head) *
+                          kBlockBytes;
+    const int c = dim / 8;
+    return block + token * 256 + ((c ^ (token & 7)) << 4) + (dim % 8) * 2;
+}
+
 int asv_attn_num_workers(const asv_attn_shape* shape, int device, int32_t* workers_out) {
     if (int rc = check_shape(shape)) return rc;
     const int g = group_of(shape);
@@ -268,8 +277,10 @@ int asv_decode_attention(const asv_attn_shape* shape, const asv_attn_args* a, vo
     }
     L.q = a->q;
     L.pool = a->kv_pool;
-    L.page_bytes = static_cast<int64_t>(shape->num_layers) * 2 * n_kv * kBlockBytes;
-    L.layer_off = static_cast<int64_t>(a->layer) * 2 * n_kv * kBlockBytes;
+    if (a->pool_pages < 1) return fail(ASV_ERR_INVALID, "pool_pages must be >= 1 (layer stride of the pool)");
+    // layer-major pool: consecutive pages of one layer are one slice apart
+    L.page_bytes = static_cast<int64_t>(2) * n_kv * kBlockBytes;
+    L.layer_off = static_cast<int64_t>(a->layer) * a->pool_pages * L.page_bytes;
     L.v_off = static_cast<int64_t>(n_kv) * kBlockBytes;
     L.gdesc = a->plan_dev + pl.off_desc;
     L.split_base = a->plan_dev + pl.off_split_base;

@@ -69,10 +69,12 @@ int xfer_kind(const std::string& k) {
 // Fixed pool of physical KV pages on one device.
 class PagePool {
  public:
-    void init(int device, int64_t pages, int64_t page_bytes) {
+    // `page_bytes`: one page across all layers; `slice`: one layer of one page
+    void init(int device, int64_t pages, int64_t page_bytes, int64_t slice) {
         device_ = device;
         pages_ = pages;
         page_bytes_ = page_bytes;
+        slice_ = slice;
         ASV_CUDA(cudaSetDevice(device));
         ASV_CUDA(cudaMalloc(&base_, static_cast<size_t>(pages * page_bytes)));
         ASV_CUDA(cudaMemset(base_, 0, static_cast<size_t>(pages * page_bytes)));
@@ -108,7 +110,8 @@ class PagePool {
             quarantine_.pop_front();
         }
     }
-    char* page(int32_t p) const { return base_ + static_cast<int64_t>(p) * page_bytes_; }
+    // layer-0 slice of page p (layer l is l * size() * slice bytes further)
+    char* page(int32_t p) const { return base_ + static_cast<int64_t>(p) * slice_; }
     char* base() const { return base_; }
     int64_t size() const { return pages_; }
     int device() const { return device_; }
@@ -119,7 +122,7 @@ class PagePool {
         std::vector<int32_t> pages;
     };
     int device_ = 0;
-    int64_t pages_ = 0, page_bytes_ = 0;
+    int64_t pages_ = 0, page_bytes_ = 0, slice_ = 0;
     char* base_ = nullptr;
     std::vector<int32_t> free_;
     std::deque<Q> quarantine_;
@@ -186,7 +189,8 @@ class GpuExecutor : public prefixsim::EngineObserver {
                                         std::to_string(page_bytes_) + " B) does not fit free HBM (" +
                                         std::to_string(fr) + " B)");
         }
-        dec_.init(o.decode_device, dec_pages_, page_bytes_);
+        slice_ = 2 * static_cast<int64_t>(o.num_kv_heads) * 4096;
+        dec_.init(o.decode_device, dec_pages_, page_bytes_, slice_);
         if (pair_ && peer) {
             ASV_CUDA(cudaSetDevice(o.decode_device));
             int can = 0;
@@ -200,7 +204,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
             if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) ASV_CUDA(e);
             cudaGetLastError();
         }
-        if (pair_) pre_.init(o.prefetch_device, pre_pages_, page_bytes_);
+        if (pair_) pre_.init(o.prefetch_device, pre_pages_, page_bytes_, slice_);
         // streams
         ASV_CUDA(cudaSetDevice(o.decode_device));
         ASV_CUDA(cudaStreamCreateWithFlags(&compute_, cudaStreamNonBlocking));
@@ -621,25 +625,18 @@ class GpuExecutor : public prefixsim::EngineObserver {
     }
 
     // copy `tokens` tokens of KV between host pages and device pages (exact bytes)
+    // KV moves go through the C-ABI copy routines (kv_copy.cpp): whole pages as
+    // 2-D copies, the valid rows of a partial last page as one 3-D copy.
     int64_t copy_kv(const std::vector<int32_t>& pages, const PagePool& pool, prefixsim::RequestId id, int64_t tokens,
                     bool to_device) {
-        const int64_t full = tokens / 16, rows = tokens % 16;
+        host_ptrs_.clear();
+        for (int64_t j = 0; j < (tokens + 15) / 16; ++j) host_ptrs_.push_back(host_page(id, j));
         int64_t moved = 0;
-        for (int64_t j = 0; j < full; ++j) {
-            char* d = pool.page(pages[static_cast<size_t>(j)]);
-            char* h = host_page(id, j);
-            ASV_CUDA(cudaMemcpyAsync(to_device ? d : h, to_device ? h : d, static_cast<size_t>(page_bytes_),
-                                     to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, cur_));
-            moved += page_bytes_;
-        }
-        if (rows > 0) {
-            char* d = pool.page(pages[static_cast<size_t>(full)]);
-            char* h = host_page(id, full);
-            const size_t blocks = static_cast<size_t>(o_.num_layers) * 2 * o_.num_kv_heads;
-            ASV_CUDA(cudaMemcpy2DAsync(to_device ? d : h, 4096, to_device ? h : d, 4096, static_cast<size_t>(rows) * 256,
-                                       blocks, to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, cur_));
-            moved += rows * 256 * static_cast<int64_t>(blocks);
-        }
+        const int rc = to_device ? asv_kv_copy_h2d(&shape_, pool.base(), pool.size(), pages.data(), tokens,
+                                                   host_ptrs_.data(), cur_, &moved)
+                                 : asv_kv_copy_d2h(&shape_, pool.base(), pool.size(), pages.data(), tokens,
+                                                   const_cast<void* const*>(host_ptrs_.data()), cur_, &moved);
+        if (rc != ASV_OK) throw CudaError(asv_last_error());
         return moved;
     }
 
@@ -740,21 +737,10 @@ class GpuExecutor : public prefixsim::EngineObserver {
 
     int64_t copy_peer(const std::vector<int32_t>& dst, const PagePool& dpool, const std::vector<int32_t>& src,
                       const PagePool& spool, int64_t tokens) {
-        const int64_t full = std::min<int64_t>(tokens / 16, static_cast<int64_t>(src.size()));
-        const int64_t rows = tokens % 16;
         int64_t moved = 0;
-        for (int64_t j = 0; j < full; ++j) {
-            ASV_CUDA(cudaMemcpyPeerAsync(dpool.page(dst[static_cast<size_t>(j)]), dpool.device(),
-                                         spool.page(src[static_cast<size_t>(j)]), spool.device(),
-                                         static_cast<size_t>(page_bytes_), p2p_));
-            moved += page_bytes_;
-        }
-        if (rows > 0 && full < static_cast<int64_t>(src.size())) {
-            const size_t blocks = static_cast<size_t>(o_.num_layers) * 2 * o_.num_kv_heads;
-            ASV_CUDA(cudaMemcpy2DAsync(dpool.page(dst[static_cast<size_t>(full)]), 4096,
-                                       spool.page(src[static_cast<size_t>(full)]), 4096,
-                                       static_cast<size_t>(rows) * 256, blocks, cudaMemcpyDefault, p2p_));
-            moved += rows * 256 * static_cast<int64_t>(blocks);
+        if (asv_kv_copy_d2d(&shape_, dpool.base(), dpool.size(), dpool.device(), dst.data(), spool.base(), spool.size(),
+                            spool.device(), src.data(), tokens, p2p_, &moved) != ASV_OK) {
+            throw CudaError(asv_last_error());
         }
         return moved;
     }
@@ -806,7 +792,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
     };
     asv_engine_opts o_;
     asv_attn_shape shape_{};
-    int64_t page_bytes_ = 0, row_bytes_all_ = 0;
+    int64_t page_bytes_ = 0, row_bytes_all_ = 0, slice_ = 0;
     bool pair_ = false;
     int64_t dec_pages_ = 0, pre_pages_ = 0;
     PagePool dec_, pre_;
@@ -836,6 +822,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
     std::vector<std::pair<PagePool*, std::vector<int32_t>>> group_quarantine_;
     std::vector<CopyTimer> copy_timers_;
     std::vector<int32_t> seq_, indptr_, indices_;
+    std::vector<const void*> host_ptrs_;
     int64_t executed_ = 0, iterations_total_ = 0;
     uint32_t launches_ = 0;
     double host_ms_ = 0.0;

@@ -1,0 +1,158 @@
+// KV page moves between the pinned host pool (page-major pages) and layer-major
+// device page pools (include/asv.h): C1 host -> prefetch GPU, C2/C3 prefetch
+// <-> decode GPU.  Replace the PRICED transfers of the reference
+// (transfer_time, cluster_sim.hpp:60-66; start_async_transfer / sync_transfer
+// :220-232) with copy-engine work.  A request with s tokens moves floor(s/16)
+// whole pages (one 2-D copy each: L slices) and the s%16 valid rows of its last
+// page (one 3-D copy: rows x blocks x layers) — exactly s * kv_bytes_per_token
+// bytes (cluster_sim.hpp:239-241).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+
+#include "../../include/asv.h"
+#include "asv_internal.h"
+
+namespace asv {
+namespace {
+
+constexpr int64_t kBlock = 4096;
+
+struct Geo {
+    int64_t slice;  // one layer of one page
+    int64_t bps;    // 4 KiB blocks per slice
+    int64_t layers;
+    int64_t page_bytes;
+};
+
+int geo(const asv_attn_shape* s, Geo* g) {
+    const int64_t pb = asv_page_bytes(s);
+    if (pb <= 0) return fail(ASV_ERR_INVALID, asv_last_error());
+    g->bps = 2 * static_cast<int64_t>(s->num_kv_heads);
+    g->slice = g->bps * kBlock;
+    g->layers = s->num_layers;
+    g->page_bytes = pb;
+    return ASV_OK;
+}
+
+cudaPitchedPtr pitched(const void* base, int64_t rows_per_layer) {
+    return make_cudaPitchedPtr(const_cast<void*>(base), kBlock, kBlock, static_cast<size_t>(rows_per_layer));
+}
+
+// host <-> device, `to_device` selects the direction
+int host_device(const asv_attn_shape* shape, void* pool, int64_t pool_pages, const int32_t* pages, int64_t tokens,
+                void* const* host_pages, bool to_device, cudaStream_t st, int64_t* bytes_out) {
+    Geo g;
+    if (int rc = geo(shape, &g)) return rc;
+    if (pool == nullptr || pages == nullptr || host_pages == nullptr || tokens < 0 || pool_pages < 1)
+        return fail(ASV_ERR_INVALID, "bad kv copy arguments");
+    const int64_t full = tokens / 16, rows = tokens % 16;
+    const size_t dpitch = static_cast<size_t>(pool_pages * g.slice);
+    const cudaMemcpyKind kind = to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+    char* base = static_cast<char*>(pool);
+    int64_t moved = 0;
+    for (int64_t j = 0; j < full; ++j) {
+        char* d = base + static_cast<int64_t>(pages[j]) * g.slice;
+        char* h = static_cast<char*>(host_pages[j]);
+        cudaError_t e = to_device ? cudaMemcpy2DAsync(d, dpitch, h, g.slice, g.slice, g.layers, kind, st)
+                                  : cudaMemcpy2DAsync(h, g.slice, d, dpitch, g.slice, g.layers, kind, st);
+        if (e != cudaSuccess) return cuda_fail(e, "kv page copy");
+        moved += g.page_bytes;
+    }
+    if (rows > 0) {
+        cudaMemcpy3DParms m = {};
+        const cudaPitchedPtr dev = pitched(base, pool_pages * g.bps);
+        const cudaPitchedPtr host = pitched(host_pages[full], g.bps);
+        const cudaPos dpos = make_cudaPos(0, static_cast<size_t>(pages[full]) * g.bps, 0);
+        m.srcPtr = to_device ? host : dev;
+        m.dstPtr = to_device ? dev : host;
+        m.srcPos = to_device ? make_cudaPos(0, 0, 0) : dpos;
+        m.dstPos = to_device ? dpos : make_cudaPos(0, 0, 0);
+        m.extent = make_cudaExtent(static_cast<size_t>(rows) * 256, static_cast<size_t>(g.bps),
+                                   static_cast<size_t>(g.layers));
+        m.kind = kind;
+        cudaError_t e = cudaMemcpy3DAsync(&m, st);
+        if (e != cudaSuccess) return cuda_fail(e, "kv partial page copy");
+        moved += rows * 256 * g.bps * g.layers;
+    }
+    if (bytes_out) *bytes_out = moved;
+    return ASV_OK;
+}
+
+}  // namespace
+}  // namespace asv
+
+using namespace asv;
+
+extern "C" {
+
+int asv_kv_copy_h2d(const asv_attn_shape* shape, void* pool, int64_t pool_pages, const int32_t* pages,
+                    int64_t tokens, const void* const* host_pages, void* stream, int64_t* bytes_out) {
+    return host_device(shape, pool, pool_pages, pages, tokens, const_cast<void* const*>(host_pages), true,
+                       static_cast<cudaStream_t>(stream), bytes_out);
+}
+
+int asv_kv_copy_d2h(const asv_attn_shape* shape, const void* pool, int64_t pool_pages, const int32_t* pages,
+                    int64_t tokens, void* const* host_pages, void* stream, int64_t* bytes_out) {
+    return host_device(shape, const_cast<void*>(pool), pool_pages, pages, tokens, host_pages, false,
+                       static_cast<cudaStream_t>(stream), bytes_out);
+}
+
+int asv_kv_copy_d2d(const asv_attn_shape* shape, void* dst_pool, int64_t dst_pool_pages, int32_t dst_device,
+                    const int32_t* dst_pages, const void* src_pool, int64_t src_pool_pages, int32_t src_device,
+                    const int32_t* src_pages, int64_t tokens, void* stream, int64_t* bytes_out) {
+    Geo g;
+    if (int rc = geo(shape, &g)) return rc;
+    if (dst_pool == nullptr || src_pool == nullptr || dst_pages == nullptr || src_pages == nullptr || tokens < 0 ||
+        dst_pool_pages < 1 || src_pool_pages < 1)
+        return fail(ASV_ERR_INVALID, "bad kv copy arguments");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t full = tokens / 16, rows = tokens % 16;
+    const size_t dp = static_cast<size_t>(dst_pool_pages * g.slice), sp = static_cast<size_t>(src_pool_pages * g.slice);
+    char* db = static_cast<char*>(dst_pool);
+    const char* sb = static_cast<const char*>(src_pool);
+    int64_t moved = 0;
+    for (int64_t j = 0; j < full; ++j) {
+        cudaError_t e = cudaMemcpy2DAsync(db + static_cast<int64_t>(dst_pages[j]) * g.slice, dp,
+                                          sb + static_cast<int64_t>(src_pages[j]) * g.slice, sp, g.slice, g.layers,
+                                          cudaMemcpyDefault, st);
+        if (e != cudaSuccess) return cuda_fail(e, "kv peer page copy");
+        moved += g.page_bytes;
+    }
+    if (rows > 0) {
+        const cudaExtent ext = make_cudaExtent(static_cast<size_t>(rows) * 256, static_cast<size_t>(g.bps),
+                                               static_cast<size_t>(g.layers));
+        const cudaPitchedPtr d = pitched(db, dst_pool_pages * g.bps);
+        const cudaPitchedPtr s = pitched(sb, src_pool_pages * g.bps);
+        const cudaPos dpos = make_cudaPos(0, static_cast<size_t>(dst_pages[full]) * g.bps, 0);
+        const cudaPos spos = make_cudaPos(0, static_cast<size_t>(src_pages[full]) * g.bps, 0);
+        cudaError_t e;
+        if (dst_device != src_device) {
+            cudaMemcpy3DPeerParms m = {};
+            m.dstPtr = d;
+            m.dstPos = dpos;
+            m.dstDevice = dst_device;
+            m.srcPtr = s;
+            m.srcPos = spos;
+            m.srcDevice = src_device;
+            m.extent = ext;
+            e = cudaMemcpy3DPeerAsync(&m, st);
+        } else {
+            cudaMemcpy3DParms m = {};
+            m.dstPtr = d;
+            m.dstPos = dpos;
+            m.srcPtr = s;
+            m.srcPos = spos;
+            m.extent = ext;
+            m.kind = cudaMemcpyDeviceToDevice;
+            e = cudaMemcpy3DAsync(&m, st);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "kv peer partial page copy");
+        moved += rows * 256 * g.bps * g.layers;
+    }
+    if (bytes_out) *bytes_out = moved;
+    return ASV_OK;
+}
+
+}  // extern "C"

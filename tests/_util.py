@@ -58,8 +58,12 @@ def page_bytes(n_kv: int, num_layers: int) -> int:
 
 
 def block_view(pool: np.ndarray, n_kv: int, num_layers: int) -> np.ndarray:
-    """uint8 pool -> [pages][layers][2][n_kv][4096] byte view."""
-    return pool.reshape(-1, num_layers, 2, n_kv, 4096)
+    """uint8 LAYER-MAJOR device pool -> [layers][pages][2][n_kv][4096] byte view (include/asv.h)."""
+    return pool.reshape(num_layers, -1, 2, n_kv, 4096)
+
+
+def pool_pages(pool: np.ndarray, n_kv: int, num_layers: int) -> int:
+    return pool.size // page_bytes(n_kv, num_layers)
 
 
 def unswizzle_block(block: np.ndarray) -> np.ndarray:
@@ -114,7 +118,7 @@ class Oracle:
         lse = np.zeros((b, n_q), dtype=np.float32)
         rc = self.h.asv_oracle_decode_attention(
             n_q, n_kv, num_layers, layer, q_bits.ctypes.data, pool.ctypes.data,
-            page_bytes(n_kv, num_layers), seq.ctypes.data, indptr.ctypes.data, indices.ctypes.data,
+            pool_pages(pool, n_kv, num_layers), seq.ctypes.data, indptr.ctypes.data, indices.ctypes.data,
             b, float(sm_scale), out.ctypes.data, lse.ctypes.data, threads or os.cpu_count() or 1)
         assert rc == 0
         return out, lse
@@ -132,8 +136,8 @@ def numpy_attention(n_q, n_kv, num_layers, layer, q_bits, pool, seq_lens, indptr
         s = int(seq_lens[r])
         pages = indices[indptr[r]:indptr[r + 1]]
         for kvh in range(n_kv):
-            K = np.concatenate([unswizzle_block(blocks[p, layer, 0, kvh]) for p in pages[:(s + 15) // 16]])[:s]
-            V = np.concatenate([unswizzle_block(blocks[p, layer, 1, kvh]) for p in pages[:(s + 15) // 16]])[:s]
+            K = np.concatenate([unswizzle_block(blocks[layer, p, 0, kvh]) for p in pages[:(s + 15) // 16]])[:s]
+            V = np.concatenate([unswizzle_block(blocks[layer, p, 1, kvh]) for p in pages[:(s + 15) // 16]])[:s]
             K = bf16_bits_to_f32(K).astype(np.float64)
             V = bf16_bits_to_f32(V).astype(np.float64)
             for h in range(kvh * g, (kvh + 1) * g):

@@ -39,7 +39,7 @@ def _run_case(oracle, n_q, n_kv, L, layer, seq_lens, seed=1, num_workers=None, a
     if const_v is not None:
         # every element of every V block equal: the swizzle is irrelevant
         cv = U.f32_to_bf16_bits(np.array([const_v], np.float32))[0]
-        blocks[:, :, 1] = np.full(2048, cv, np.uint16).view(np.uint8)
+        blocks[:, :, 1] = np.full(2048, cv, np.uint16).view(np.uint8)  # [layer][page][V]
     if poison_tail:
         # rows >= seq_len in each last page hold NaN bit patterns; the kernel must ignore them
         nan_row = np.full(128, 0x7FC1, np.uint16)
@@ -50,7 +50,7 @@ def _run_case(oracle, n_q, n_kv, L, layer, seq_lens, seed=1, num_workers=None, a
                     for h in range(n_kv):
                         for d in range(128):
                             off = U.swz_off(t, d)
-                            blocks[last, layer, kv, h].view(np.uint16)[off // 2] = nan_row[d]
+                            blocks[layer, last, kv, h].view(np.uint16)[off // 2] = nan_row[d]
     b = len(seq_lens)
     q_bits = U.random_bf16(seed + 2, b * n_q * 128).reshape(b, n_q, 128)
     kn_bits = U.random_bf16(seed + 3, b * n_kv * 128).reshape(b, n_kv, 128)
@@ -89,8 +89,8 @@ def _run_case(oracle, n_q, n_kv, L, layer, seq_lens, seed=1, num_workers=None, a
             page = indices[indptr[r] + s // 16]
             t = s % 16
             for h in range(n_kv):
-                krow = U.unswizzle_block(ba[page, layer, 0, h])[t]
-                vrow = U.unswizzle_block(ba[page, layer, 1, h])[t]
+                krow = U.unswizzle_block(ba[layer, page, 0, h])[t]
+                vrow = U.unswizzle_block(ba[layer, page, 1, h])[t]
                 assert (krow == kn_bits[r, h]).all()
                 assert (vrow == vn_bits[r, h]).all()
     return got, ref_out, plan

@@ -68,7 +68,7 @@ def test_known_answer_single_token(oracle):
     out, _ = oracle.attention(4, 4, L, 0, q, pool, [1], [0, 1], [1], 0.1)
     blocks = U.block_view(pool, n_kv, L)
     for h in range(4):
-        v0 = U.bf16_bits_to_f32(U.unswizzle_block(blocks[1, 0, 1, h])[0])
+        v0 = U.bf16_bits_to_f32(U.unswizzle_block(blocks[0, 1, 1, h])[0])
         assert np.array_equal(out[0, h], v0)
 
 
@@ -86,7 +86,7 @@ def test_known_answer_dominant_key(oracle):
         for d in range(128):
             for kv, src in ((0, kb), (1, vb)):
                 o = U.swz_off(t, d)
-                blocks[0, 0, kv, 0][o:o + 2] = U.f32_to_bf16_bits(src[t, d:d + 1]).view(np.uint8)
+                blocks[0, 0, kv, 0][o:o + 2] = U.f32_to_bf16_bits(src[t, d:d + 1]).view(np.uint8)  # [layer][page]
     out, _ = oracle.attention(1, 1, L, 0, U.f32_to_bf16_bits(q), pool, [16], [0, 1], [0], 1.0)
     v5 = U.bf16_bits_to_f32(U.f32_to_bf16_bits(vb[5]))
     assert np.abs(out[0, 0] - v5).max() < 1e-6
