@@ -37,10 +37,13 @@ int asv_abi_version(void);
 /* ------------------------------------------------------------------------ */
 /* Paged KV layout.  A page holds 16 tokens (= ClusterConfig::block_size,     */
 /* cluster_sim.hpp:45) of every layer, K and V, every kv head.                */
-/*  * device pool (HBM), LAYER-MAJOR:                                          */
-/*      [num_layers][pool_pages][2 (K,V)][num_kv_heads][16][head_dim=128]      */
-/*    so one layer's slices of all pages are contiguous (dense address range   */
-/*    per decode launch);                                                      */
+/*  * device pool (HBM), LAYER-MAJOR in page groups: group g holds pages      */
+/*    [g*G, (g+1)*G) as [num_layers][G][2 (K,V)][num_kv_heads][16][128], with  */
+/*    G = asv_pool_group_pages() chosen so the layer pitch G * slice stays     */
+/*    below 2 GiB (the copy engines' full-rate 2-D pitch; measured).  A pool  */
+/*    that fits one group is plain [num_layers][pool_pages][...], so one      */
+/*    layer's slices of all pages are dense per decode launch.  Page ids must  */
+/*    be < asv_pool_usable_pages() (= groups * G, at most groups-1 fewer).     */
 /*  * host pool / transfer format, PAGE-MAJOR: one page is                      */
 /*      [num_layers][2][num_kv_heads][16][128] contiguous (asv_page_bytes).    */
 /* Every (page, layer, K|V, head) block is 4 KiB, bf16, and XOR-swizzled: the  */
@@ -67,6 +70,10 @@ int64_t asv_page_offset(const asv_attn_shape* shape, int32_t layer, int32_t kv, 
 /* byte offset of element (page, layer, kv, head, token, dim) in a LAYER-MAJOR device pool */
 int64_t asv_pool_offset(const asv_attn_shape* shape, int64_t pool_pages, int64_t page, int32_t layer,
                         int32_t kv, int32_t head, int32_t token, int32_t dim);
+/* pages per layer-major group G of a pool of `pool_pages` pages (-1 on bad arguments) */
+int64_t asv_pool_group_pages(const asv_attn_shape* shape, int64_t pool_pages);
+/* page ids valid in such a pool: [0, groups * G) */
+int64_t asv_pool_usable_pages(const asv_attn_shape* shape, int64_t pool_pages);
 
 /* ------------------------------------------------------------------------ */
 /* Split-KV work plan (host side, K4 in SURVEY §2).  Built once per decode    */
@@ -104,6 +111,16 @@ int asv_attn_plan_build(const asv_attn_shape* shape, int32_t batch, const int32_
                         int32_t num_workers, int32_t* plan_buf, int64_t plan_cap,
                         asv_attn_plan* plan_out);
 
+/* Upload a plan buffer from MAPPED pinned host memory (cudaHostAllocMapped) into
+ * device memory with SM loads over PCIe (one small kernel on `stream`), not with
+ * a copy-engine memcpy: a plan upload issued on the compute stream must never
+ * queue behind multi-GB KV prefetches on the shared host-to-device copy engine
+ * (measured: a cudaMemcpyAsync plan upload serialised every decode iteration
+ * behind the batch prefetch in flight).  `host_plan` must be readable for
+ * n_int32 rounded up to a multiple of 4.  The next kernel on `stream` must not
+ * be launched with programmatic dependent launch. */
+int asv_plan_upload(const int32_t* host_plan, int32_t* plan_dev, int64_t n_int32, void* stream);
+
 /* Workspace: split partials + per-(request, kv head) semaphores. */
 size_t asv_attn_workspace_bytes(const asv_attn_shape* shape, int32_t max_batch,
                                 int32_t max_total_splits);
@@ -125,8 +142,9 @@ typedef struct asv_attn_args {
     float sm_scale;         /* 1/sqrt(128) for the paper's Eq. 2 */
     uint32_t launch_index;  /* consecutive launches on one workspace must alternate parity */
     int32_t pdl;            /* 1: programmatic dependent launch (overlap with the previous kernel) */
-    uint64_t* warp_timestamps; /* optional [workers][2] device buffer: %globaltimer at each persistent
-                                  warp's start and end — the measured intra-iteration bubble */
+    uint64_t* warp_timestamps; /* optional [workers][2] device-accessible buffer (device or mapped host):
+                                  %globaltimer at each persistent warp's start and end — the measured
+                                  intra-iteration bubble */
 } asv_attn_args;
 
 /* K1+K2+K3: paged split-KV decode attention with fused KV append (K1+K3), then the
@@ -241,6 +259,10 @@ typedef struct asv_engine_stats {
     double measured_idle_frac;    /* 1 - sum(warp busy) / (warps x launch span), layer-0 launch of each
                                      timed iteration, from per-warp %globaltimer */
     double measured_bubble_ms;    /* sum over timed iterations of the mean idle time per warp x layers */
+    double pcie_union_ms;         /* union of the PCIe copy-group intervals (both directions) inside the
+                                     window: time the host link had work (single device only, else 0) */
+    double host_wait_ms;          /* host time blocked on the GPU (run-ahead ring, page reclaim) */
+    int64_t hazard_waits;         /* copy-stream waits on a page's last iteration (page reuse) */
 } asv_engine_stats;
 
 int asv_engine_run(const char* config_json, const char* policy_override, const asv_engine_opts* opts,

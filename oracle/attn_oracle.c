@@ -17,8 +17,9 @@
  *
  * Numerics: bf16 inputs widened to fp32 exactly; dot products in fp32, the
  * softmax normaliser and the weighted V sum accumulated in double.
- * Layout and swizzle: include/asv.h (device pool LAYER-MAJOR:
- * [L][pool_pages][2][n_kv][16][128]).
+ * Layout and swizzle: include/asv.h (device pool LAYER-MAJOR in page groups of
+ * G pages, each group [L][G][2][n_kv][16][128], G the largest equal split with
+ * G * slice < 2 GiB; one group = [L][pool_pages][...] for every test-sized pool).
  */
 #include <math.h>
 #include <pthread.h>
@@ -63,8 +64,12 @@ static void one_row(const job_t* j, int r, int h) {
     float qf[128];
     for (int d = 0; d < D; ++d) qf[d] = bf16_to_f32(qv[d]);
     float* scores = (float*)malloc(sizeof(float) * (size_t)(s > 0 ? s : 1));
-    /* block (page, layer, kv, head) of the layer-major pool */
-#define BLOCK(page, kv) ((((((int64_t)j->layer * j->pool_pages + (page)) * 2 + (kv)) * j->n_kv) + kvh) * 4096)
+    /* block (page, layer, kv, head) of the grouped layer-major pool */
+    const int64_t slice = (int64_t)2 * j->n_kv * 4096;
+    const int64_t gmax = (((int64_t)1 << 31) - 1) / slice;
+    const int64_t gp = j->pool_pages / ((j->pool_pages + gmax - 1) / gmax);
+#define BLOCK(page, kv) \
+    ((((page) / gp) * gp * j->L + (int64_t)j->layer * gp + (page) % gp) * slice + ((int64_t)(kv) * j->n_kv + kvh) * 4096)
     float mx = -INFINITY;
     for (int t = 0; t < s; ++t) {
         const int64_t page = j->indices[j->indptr[r] + t / 16];

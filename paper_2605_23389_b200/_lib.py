@@ -115,6 +115,9 @@ class EngineStats(C.Structure):
         ("p2p_bytes_window", C.c_int64),
         ("measured_idle_frac", C.c_double),
         ("measured_bubble_ms", C.c_double),
+        ("pcie_union_ms", C.c_double),
+        ("host_wait_ms", C.c_double),
+        ("hazard_waits", C.c_int64),
     ]
 
     def as_dict(self):
@@ -137,10 +140,13 @@ SIGNATURES = [
      [C.POINTER(AttnShape), C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
     ("asv_pool_offset", C.c_int64,
      [C.POINTER(AttnShape), C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
+    ("asv_pool_group_pages", C.c_int64, [C.POINTER(AttnShape), C.c_int64]),
+    ("asv_pool_usable_pages", C.c_int64, [C.POINTER(AttnShape), C.c_int64]),
     ("asv_attn_num_workers", C.c_int, [C.POINTER(AttnShape), C.c_int, C.POINTER(C.c_int32)]),
     ("asv_attn_plan_build", C.c_int,
      [C.POINTER(AttnShape), C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
       C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_int32), C.c_int64, C.POINTER(AttnPlan)]),
+    ("asv_plan_upload", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     ("asv_attn_workspace_bytes", C.c_size_t, [C.POINTER(AttnShape), C.c_int32, C.c_int32]),
     ("asv_attn_workspace_init", C.c_int, [C.c_void_p, C.c_size_t, C.c_void_p]),
     ("asv_decode_attention", C.c_int, [C.POINTER(AttnShape), C.POINTER(AttnArgs), C.c_void_p]),

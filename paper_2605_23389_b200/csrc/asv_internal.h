@@ -14,6 +14,29 @@ namespace asv {
 constexpr int kDescWords = 40;
 constexpr int kMaxItemPages = 32;
 
+// Layer-major device pools are split into equal page GROUPS so that the layer
+// pitch of a group (group_pages * slice) stays below 2 GiB: the copy engines
+// run a 2-D copy at full PCIe rate only below that pitch (measured on B200:
+// 54 GB/s at a 1 GiB pitch, 29.7 GB/s = one row per copy at >= 2 GiB;
+// tools/copy_tlb_probe.py).  Group g holds pages [g*G, (g+1)*G) as
+// [L][G][slice]; page p's layer-l slice is at slice index
+//   pool_slot(p) + l*G,  pool_slot(p) = p + (p / G) * G * (L - 1).
+// A pool that fits one group (every test-sized pool) is plain [L][pages][slice].
+constexpr int64_t kMaxGroupPitch = (int64_t(1) << 31) - 1;
+
+inline int64_t pool_group_pages(int64_t slice, int64_t pool_pages) {
+    const int64_t gmax = kMaxGroupPitch / slice;
+    const int64_t groups = (pool_pages + gmax - 1) / gmax;
+    return pool_pages / groups;
+}
+inline int64_t pool_usable_pages(int64_t slice, int64_t pool_pages) {
+    const int64_t g = pool_group_pages(slice, pool_pages);
+    return (pool_pages / g) * g;
+}
+inline int64_t pool_slot(int64_t page, int64_t group_pages, int64_t layers) {
+    return page + (page / group_pages) * group_pages * (layers - 1);
+}
+
 // Launch description for the decode-attention kernel (decode_attn.cu).
 struct AttnLaunch {
     int group;              // n_q / n_kv
@@ -21,9 +44,11 @@ struct AttnLaunch {
     bool pdl;               // programmatic dependent launch
     const void* q;
     void* pool;
-    int64_t page_bytes;
-    int64_t layer_off;
+    int64_t page_bytes;     // one layer slice of one page (pool_slot unit)
+    int64_t layer_off;      // layer * group_pages * page_bytes
     int64_t v_off;
+    int32_t group_pages;    // pages per layer-major group (pool_group_pages)
+    int32_t group_skip;     // group_pages * (L - 1): pool_slot(p) = p + (p / group_pages) * group_skip
     const int32_t* gdesc;
     const int32_t* split_base;
     int32_t num_items;
@@ -47,6 +72,7 @@ struct AttnLaunch {
 int attn_warps_per_cta(int group);
 cudaError_t attn_occupancy(int group, int* blocks_per_sm);
 cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st);
+cudaError_t plan_upload(const int32_t* host_plan, int32_t* plan_dev, int64_t n_int32, cudaStream_t st);
 
 // thread-local last error (asv_last_error)
 void set_error(const std::string& msg);

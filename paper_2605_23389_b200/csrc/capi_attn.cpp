@@ -81,10 +81,28 @@ int64_t asv_page_offset(const asv_attn_shape* s, int32_t layer, int32_t kv, int3
 int64_t asv_pool_offset(const asv_attn_shape* s, int64_t pool_pages, int64_t page, int32_t layer, int32_t kv,
                         int32_t head, int32_t token, int32_t dim) {
     if (check_shape(s) != ASV_OK) return -1;
-    const int64_t block = (((static_cast<int64_t>(layer) * pool_pages + page) * 2 + kv) * s->num_kv_heads + head) *
-                          kBlockBytes;
+    const int64_t slice = static_cast<int64_t>(2) * s->num_kv_heads * kBlockBytes;
+    if (pool_pages < 1 || page < 0 || page >= pool_usable_pages(slice, pool_pages)) {
+        fail(ASV_ERR_INVALID, "page outside the usable pool");
+        return -1;
+    }
+    const int64_t gp = pool_group_pages(slice, pool_pages);
+    const int64_t sl = pool_slot(page, gp, s->num_layers) + static_cast<int64_t>(layer) * gp;
+    const int64_t block = sl * slice + (static_cast<int64_t>(kv) * s->num_kv_heads + head) * kBlockBytes;
     const int c = dim / 8;
     return block + token * 256 + ((c ^ (token & 7)) << 4) + (dim % 8) * 2;
+}
+
+int64_t asv_pool_group_pages(const asv_attn_shape* s, int64_t pool_pages) {
+    if (check_shape(s) != ASV_OK) return -1;
+    if (pool_pages < 1) return fail(ASV_ERR_INVALID, "pool_pages must be >= 1"), -1;
+    return pool_group_pages(static_cast<int64_t>(2) * s->num_kv_heads * kBlockBytes, pool_pages);
+}
+
+int64_t asv_pool_usable_pages(const asv_attn_shape* s, int64_t pool_pages) {
+    if (check_shape(s) != ASV_OK) return -1;
+    if (pool_pages < 1) return fail(ASV_ERR_INVALID, "pool_pages must be >= 1"), -1;
+    return pool_usable_pages(static_cast<int64_t>(2) * s->num_kv_heads * kBlockBytes, pool_pages);
 }
 
 int asv_attn_num_workers(const asv_attn_shape* shape, int device, int32_t* workers_out) {
@@ -243,6 +261,15 @@ int asv_attn_workspace_init(void* workspace, size_t bytes, void* stream) {
     return ASV_OK;
 }
 
+int asv_plan_upload(const int32_t* host_plan, int32_t* plan_dev, int64_t n_int32, void* stream) {
+    if (host_plan == nullptr || plan_dev == nullptr || n_int32 < 0) return fail(ASV_ERR_INVALID, "bad plan upload");
+    if ((reinterpret_cast<uintptr_t>(host_plan) | reinterpret_cast<uintptr_t>(plan_dev)) & 15u)
+        return fail(ASV_ERR_INVALID, "plan buffers must be 16-byte aligned");
+    cudaError_t e = plan_upload(host_plan, plan_dev, n_int32, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "plan upload");
+    return ASV_OK;
+}
+
 int asv_decode_attention(const asv_attn_shape* shape, const asv_attn_args* a, void* stream) {
     if (int rc = check_shape(shape)) return rc;
     if (a == nullptr || a->plan == nullptr || a->plan_dev == nullptr)
@@ -278,9 +305,12 @@ int asv_decode_attention(const asv_attn_shape* shape, const asv_attn_args* a, vo
     L.q = a->q;
     L.pool = a->kv_pool;
     if (a->pool_pages < 1) return fail(ASV_ERR_INVALID, "pool_pages must be >= 1 (layer stride of the pool)");
-    // layer-major pool: consecutive pages of one layer are one slice apart
+    // layer-major pool (in page groups): consecutive pages of one layer are one slice apart
     L.page_bytes = static_cast<int64_t>(2) * n_kv * kBlockBytes;
-    L.layer_off = static_cast<int64_t>(a->layer) * a->pool_pages * L.page_bytes;
+    const int64_t gp = pool_group_pages(L.page_bytes, a->pool_pages);
+    L.group_pages = static_cast<int32_t>(gp);
+    L.group_skip = static_cast<int32_t>(gp * (shape->num_layers - 1));
+    L.layer_off = static_cast<int64_t>(a->layer) * gp * L.page_bytes;
     L.v_off = static_cast<int64_t>(n_kv) * kBlockBytes;
     L.gdesc = a->plan_dev + pl.off_desc;
     L.split_base = a->plan_dev + pl.off_split_base;

@@ -54,6 +54,8 @@ struct Params {
     int64_t page_bytes;
     int64_t layer_off;
     int64_t v_off;
+    int32_t group_pages;        // layer-major page groups (asv_internal.h pool_slot)
+    int32_t group_skip;
     const int32_t* gdesc;       // [G][kDescWords]
     const int32_t* split_base;  // [b+1]
     int32_t num_items;
@@ -221,13 +223,14 @@ __device__ __forceinline__ void load_desc(const Params& p, uint32_t k, int lane,
     const int4 a = __ldg(reinterpret_cast<const int4*>(gd));
     const int4 b = __ldg(reinterpret_cast<const int4*>(gd) + 1);
     phys = __ldg(gd + 8 + lane);
+    phys += (phys / p.group_pages) * p.group_skip;  // page id -> slice index in the grouped pool
     d.r = a.x;
     d.slot = a.y;
     d.pb = a.z;
     d.pe = a.w;
     d.seq = b.x;
     d.nsplit = b.y;
-    d.append_phys = b.z;
+    d.append_phys = b.z < 0 ? b.z : b.z + (b.z / p.group_pages) * p.group_skip;
 }
 
 // ------------------------------------------------------------- epilogues
@@ -886,8 +889,18 @@ int attn_warps_per_cta(int group) {
     return variant_available(group, v) ? v.nw : 4;
 }
 
+__global__ void plan_fetch_kernel(const int4* __restrict__ src, int4* __restrict__ dst, int64_t n16);
+
 cudaError_t attn_occupancy(int group, int* blocks_per_sm) {
-    return dispatch(group, true, blocks_per_sm, nullptr, 0, false, nullptr);
+    cudaError_t e = dispatch(group, true, blocks_per_sm, nullptr, 0, false, nullptr);
+    if (e != cudaSuccess) return e;
+    // Load every kernel of the path now (lazy module loading would load them at
+    // their first launch, which blocks on device-wide progress: a first launch
+    // queued behind a stream-memory-op wait then deadlocks; measured).
+    cudaFuncAttributes fa;
+    e = cudaFuncGetAttributes(&fa, merge_splits_kernel);
+    if (e != cudaSuccess) return e;
+    return cudaFuncGetAttributes(&fa, plan_fetch_kernel);
 }
 
 cudaError_t merge_launch(const Params& p, const int32_t* merge_reqs, int32_t n_merge, int sms, bool pdl,
@@ -908,6 +921,30 @@ cudaError_t merge_launch(const Params& p, const int32_t* merge_reqs, int32_t n_m
     return cudaLaunchKernelEx(&cfg, merge_splits_kernel, p, merge_reqs, rows);
 }
 
+// Plan upload through SM loads of mapped pinned host memory (asv_plan_upload):
+// 16-byte loads, grid-strided, all in flight at once (one PCIe round trip for a
+// typical 10-100 KB plan).  Keeps the compute stream off the copy-engine queue.
+__global__ void plan_fetch_kernel(const int4* __restrict__ src, int4* __restrict__ dst, int64_t n16) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n16;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        dst[i] = src[i];
+    }
+}
+
+cudaError_t plan_upload(const int32_t* host_plan, int32_t* plan_dev, int64_t n_int32, cudaStream_t st) {
+    const int64_t n16 = (n_int32 + 3) / 4;
+    if (n16 <= 0) return cudaSuccess;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int threads = 256;
+    int64_t blocks = (n16 + threads - 1) / threads;
+    if (blocks > sms) blocks = sms;
+    plan_fetch_kernel<<<static_cast<unsigned>(blocks), threads, 0, st>>>(reinterpret_cast<const int4*>(host_plan),
+                                                                         reinterpret_cast<int4*>(plan_dev), n16);
+    return cudaGetLastError();
+}
+
 cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st) {
     Params p;
     p.q = static_cast<const __nv_bfloat16*>(a.q);
@@ -916,6 +953,8 @@ cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st) {
     p.page_bytes = a.page_bytes;
     p.layer_off = a.layer_off;
     p.v_off = a.v_off;
+    p.group_pages = a.group_pages;
+    p.group_skip = a.group_skip;
     p.gdesc = a.gdesc;
     p.split_base = a.split_base;
     p.num_items = a.num_items;

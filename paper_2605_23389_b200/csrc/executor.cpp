@@ -16,11 +16,20 @@
 // floor(s/16) whole pages plus a 2-D copy of the s%16 valid rows of its last
 // page (s * kv_bytes_per_token in total, cluster_sim.hpp:239-241).
 //
-// Ordering: the transfer stream waits on the last launched iteration before
-// touching pages (reuse after release / reads for spill); the compute stream
-// waits on a request's copy event when it is admitted; pages freed by a copy
-// are quarantined until that copy's event completes.  The host runs ahead of
-// the GPU by at most `run_ahead` iterations (ring of plan buffers and events).
+// Threads and ordering (copy_runtime.h): the engine thread runs the decisions
+// and launches iterations on the compute stream; a CopyWorker thread issues
+// every copy-stream operation, so a full copy queue never stalls a launch.
+// Streams order each other through sequence flags (stream memory ops):
+//   * after executed iteration e the compute stream writes kIter = e + 1;
+//   * each KV move writes its lane flag (kBulk / kUrgent / kD2H / kP2P) with
+//     the next lane sequence number; the compute stream waits for it when the
+//     request is admitted;
+//   * a copy writing fresh pages waits only for the iteration that last used
+//     them (page hazards, oldest-released pages first); D2H / evict copies of
+//     running pages wait for the last launched iteration;
+//   * pages read by a copy are quarantined until its lane flag passes.
+// The host runs ahead of the GPU by at most `run_ahead` iterations (ring of
+// events + a plan arena), issuing future boundaries' KV moves early.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -28,16 +37,20 @@
 #include <prefixsim/io.hpp>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <thread>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <stdexcept>
 #include <string>
-#include <unordered_map>
 #include <vector>
 
 #include "../../include/asv.h"
 #include "asv_internal.h"
+#include "copy_runtime.h"
 #include "engine_internal.h"
 
 namespace asv {
@@ -67,19 +80,25 @@ int xfer_kind(const std::string& k) {
 }
 
 // Fixed pool of physical KV pages on one device.
+// Free pages are handed out oldest-released first, each with its hazard: the
+// executed-iteration index of the last decode iteration that may still read or
+// append to it (-1: none).  A copy writing a fresh page waits only for that
+// iteration, not for the whole GPU queue, so prefetches stream back to back.
 class PagePool {
  public:
     // `page_bytes`: one page across all layers; `slice`: one layer of one page
-    void init(int device, int64_t pages, int64_t page_bytes, int64_t slice) {
+    void init(int device, int64_t pages, int64_t page_bytes, int64_t slice, const SeqFlags* flags) {
         device_ = device;
+        flags_ = flags;
         pages_ = pages;
         page_bytes_ = page_bytes;
         slice_ = slice;
         ASV_CUDA(cudaSetDevice(device));
         ASV_CUDA(cudaMalloc(&base_, static_cast<size_t>(pages * page_bytes)));
         ASV_CUDA(cudaMemset(base_, 0, static_cast<size_t>(pages * page_bytes)));
-        free_.reserve(static_cast<size_t>(pages));
-        for (int64_t p = pages - 1; p >= 0; --p) free_.push_back(static_cast<int32_t>(p));
+        // page ids beyond the last full layer-major group are never handed out
+        const int64_t usable = pool_usable_pages(slice, pages);
+        for (int64_t p = 0; p < usable; ++p) free_.push_back({static_cast<int32_t>(p), -1});
     }
     ~PagePool() {
         if (base_ != nullptr) {
@@ -87,77 +106,66 @@ class PagePool {
             cudaFree(base_);
         }
     }
-    int32_t alloc() {
+    // `hazard` (optional) accumulates the newest iteration the page may still be used by
+    int32_t alloc(int64_t* hazard = nullptr) {
         if (free_.empty()) reclaim(true);
         if (free_.empty()) throw std::runtime_error("KV page pool exhausted on device " + std::to_string(device_));
-        const int32_t p = free_.back();
-        free_.pop_back();
-        return p;
+        const FreePage f = free_.front();
+        free_.pop_front();
+        if (hazard != nullptr) *hazard = std::max(*hazard, f.hazard);
+        return f.page;
     }
-    void release(const std::vector<int32_t>& pages) { free_.insert(free_.end(), pages.begin(), pages.end()); }
-    // pages become reusable once `ev` (a copy reading them) has completed
-    void release_after(cudaEvent_t ev, std::vector<int32_t> pages) { quarantine_.push_back({ev, std::move(pages)}); }
+    void release(const std::vector<int32_t>& pages, int64_t hazard) {
+        for (const int32_t p : pages) free_.push_back({p, hazard});
+    }
+    // pages become reusable once lane flag `slot` reaches `v` (the copy reading them is done)
+    void release_after(int slot, uint32_t v, std::vector<int32_t> pages) {
+        quarantine_.push_back({slot, v, std::move(pages)});
+    }
     void reclaim(bool block) {
         while (!quarantine_.empty()) {
             auto& q = quarantine_.front();
-            if (block) {
-                ASV_CUDA(cudaEventSynchronize(q.ev));
+            if (!flags_->reached(q.slot, q.v)) {
+                if (!block) break;
+                const auto t0 = std::chrono::steady_clock::now();
+                while (!flags_->reached(q.slot, q.v)) std::this_thread::sleep_for(std::chrono::microseconds(20));
+                wait_ms_ += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
                 block = false;  // one blocking wait, then drain whatever else finished
-            } else if (cudaEventQuery(q.ev) != cudaSuccess) {
-                break;
             }
-            free_.insert(free_.end(), q.pages.begin(), q.pages.end());
+            for (const int32_t p : q.pages) free_.push_back({p, -1});  // the copy waited for its readers
             quarantine_.pop_front();
         }
     }
-    // layer-0 slice of page p (layer l is l * size() * slice bytes further)
-    char* page(int32_t p) const { return base_ + static_cast<int64_t>(p) * slice_; }
     char* base() const { return base_; }
     int64_t size() const { return pages_; }
     int device() const { return device_; }
+    double wait_ms() const { return wait_ms_; }
 
  private:
+    struct FreePage {
+        int32_t page;
+        int64_t hazard;
+    };
     struct Q {
-        cudaEvent_t ev;
+        int slot;
+        uint32_t v;
         std::vector<int32_t> pages;
     };
+    const SeqFlags* flags_ = nullptr;
     int device_ = 0;
     int64_t pages_ = 0, page_bytes_ = 0, slice_ = 0;
     char* base_ = nullptr;
-    std::vector<int32_t> free_;
+    std::deque<FreePage> free_;
     std::deque<Q> quarantine_;
-};
-
-// Ring of reusable events recorded on one stream.
-class EventRing {
- public:
-    void init(int device, int n) {
-        ASV_CUDA(cudaSetDevice(device));
-        ev_.resize(static_cast<size_t>(n));
-        for (auto& e : ev_) ASV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    }
-    ~EventRing() {
-        for (auto e : ev_) cudaEventDestroy(e);
-    }
-    // record on `st`; the slot's previous recording must have completed (it is
-    // older than the ring, so in stream order it has)
-    cudaEvent_t record(cudaStream_t st) {
-        cudaEvent_t e = ev_[next_++ % ev_.size()];
-        ASV_CUDA(cudaEventSynchronize(e));
-        ASV_CUDA(cudaEventRecord(e, st));
-        return e;
-    }
-
- private:
-    std::vector<cudaEvent_t> ev_;
-    size_t next_ = 0;
+    double wait_ms_ = 0.0;
 };
 
 struct ReqKV {
     enum Where { kHost, kDecode, kPrefetch };
     Where where = kHost;
     std::vector<int32_t> pages;
-    cudaEvent_t ready = nullptr;  // copy that filled `pages` (nullptr: nothing pending)
+    int ready_slot = -1;          // lane flag + value of the copy that filled `pages` (-1: none pending)
+    uint32_t ready_v = 0;
     int64_t prefix = 0;
 };
 
@@ -190,7 +198,8 @@ class GpuExecutor : public prefixsim::EngineObserver {
                                         std::to_string(fr) + " B)");
         }
         slice_ = 2 * static_cast<int64_t>(o.num_kv_heads) * 4096;
-        dec_.init(o.decode_device, dec_pages_, page_bytes_, slice_);
+        flags_.init();
+        dec_.init(o.decode_device, dec_pages_, page_bytes_, slice_, &flags_);
         if (pair_ && peer) {
             ASV_CUDA(cudaSetDevice(o.decode_device));
             int can = 0;
@@ -204,7 +213,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
             if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) ASV_CUDA(e);
             cudaGetLastError();
         }
-        if (pair_) pre_.init(o.prefetch_device, pre_pages_, page_bytes_, slice_);
+        if (pair_) pre_.init(o.prefetch_device, pre_pages_, page_bytes_, slice_, &flags_);
         // streams
         ASV_CUDA(cudaSetDevice(o.decode_device));
         ASV_CUDA(cudaStreamCreateWithFlags(&compute_, cudaStreamNonBlocking));
@@ -213,11 +222,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
         ASV_CUDA(cudaStreamCreateWithFlags(&xfer_, cudaStreamNonBlocking));
         ASV_CUDA(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));  // other PCIe direction
         ASV_CUDA(cudaStreamCreateWithFlags(&urgent_, cudaStreamNonBlocking));  // strays / swap-ins
-        xfer_ev_.init(xfer_device(), 4096);
-        d2h_ev_.init(xfer_device(), 4096);
-        urgent_ev_.init(xfer_device(), 4096);
         ASV_CUDA(cudaSetDevice(o.decode_device));
-        p2p_ev_.init(o.decode_device, 4096);
         // host pool
         if (o.execute_transfers) {
             arena_pages_ = std::max<int64_t>(1, o.host_pool_bytes / page_bytes_);
@@ -240,25 +245,34 @@ class GpuExecutor : public prefixsim::EngineObserver {
         fill_random(q_, qbytes / 2, 11);
         fill_random(k_new_, kvbytes / 2, 12);
         fill_random(v_new_, kvbytes / 2, 13);
-        // plan ring: every split holds >= 2 pages or is a whole request
+        // Run-ahead ring of in-flight iterations (events, timestamps) and a plan
+        // arena: each iteration's plan occupies exactly its size in a circular
+        // mapped-host + device arena, so the host can run hundreds of iterations
+        // ahead of the GPU (issuing the KV moves of future boundaries early)
+        // with bounded memory.  Worst-case plan: every split holds >= 2 pages or
+        // is a whole request.
         ring_ = std::max(2, o.run_ahead);
         plan_cap_ = 40 * (dec_pages_ / 2 + max_rows_ + 1) + 2 * max_rows_ + 8;
-        plan_host_.resize(static_cast<size_t>(ring_));
-        plan_dev_.resize(static_cast<size_t>(ring_));
+        plan_scratch_.resize(static_cast<size_t>(plan_cap_ + 4));
+        arena_words_ = std::max<int64_t>(2 * (plan_cap_ + 4), int64_t(16) << 20);  // >= 64 MiB
+        ASV_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&plan_arena_host_), static_cast<size_t>(arena_words_) * 4,
+                               cudaHostAllocMapped));  // pulled by SM loads (asv_plan_upload)
+        ASV_CUDA(cudaMalloc(&plan_arena_dev_, static_cast<size_t>(arena_words_) * 4));
         it_end_.resize(static_cast<size_t>(ring_));
         att_beg_.resize(static_cast<size_t>(ring_));
         att_end_.resize(static_cast<size_t>(ring_));
         slot_timed_.assign(static_cast<size_t>(ring_), 0);
-        ts_dev_.resize(static_cast<size_t>(ring_));
+        slot_seq_.assign(static_cast<size_t>(ring_), 0);
+        slot_b_.assign(static_cast<size_t>(ring_), 0);
+        slot_waits_.assign(static_cast<size_t>(ring_), 0);
         ts_host_.resize(static_cast<size_t>(2 * workers_));
+        // per-warp timestamps land in mapped host memory (no copy back, no copy-engine queue)
+        ASV_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ts_arena_),
+                               static_cast<size_t>(ring_) * static_cast<size_t>(workers_) * 16, cudaHostAllocMapped));
         for (int i = 0; i < ring_; ++i) {
-            ASV_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&plan_host_[static_cast<size_t>(i)]),
-                                   static_cast<size_t>(plan_cap_) * 4, cudaHostAllocDefault));
-            ASV_CUDA(cudaMalloc(&plan_dev_[static_cast<size_t>(i)], static_cast<size_t>(plan_cap_) * 4));
             ASV_CUDA(cudaEventCreateWithFlags(&it_end_[static_cast<size_t>(i)], cudaEventDisableTiming));
             ASV_CUDA(cudaEventCreate(&att_beg_[static_cast<size_t>(i)]));
             ASV_CUDA(cudaEventCreate(&att_end_[static_cast<size_t>(i)]));
-            ASV_CUDA(cudaMalloc(&ts_dev_[static_cast<size_t>(i)], static_cast<size_t>(workers_) * 16));
         }
         ws_splits_ = static_cast<int32_t>(dec_pages_ / 2 + max_rows_ + 1);
         ws_bytes_ = asv_attn_workspace_bytes(&shape_, 0, ws_splits_);
@@ -269,9 +283,32 @@ class GpuExecutor : public prefixsim::EngineObserver {
         ASV_CUDA(cudaStreamSynchronize(compute_));
         std::memset(stats_.logical_bytes, 0, sizeof(stats_.logical_bytes));
         std::memset(stats_.logical_count, 0, sizeof(stats_.logical_count));
+        if (o.execute_transfers) warm_up_copies();
+        worker_.start();
+        if (std::getenv("ASV_WATCHDOG") != nullptr) {
+            watchdog_ = std::thread([this] {
+                while (!watchdog_stop_.load()) {
+                    std::this_thread::sleep_for(std::chrono::seconds(5));
+                    std::fprintf(stderr,
+                                 "[asv watchdog] executed=%lld phase=%d worker done=%llu queued=%zu in=%s | flags iter=%u "
+                                 "bulk=%u/%u urgent=%u/%u d2h=%u/%u p2p=%u/%u\n",
+                                 static_cast<long long>(executed_), phase_.load(),
+                                 static_cast<unsigned long long>(worker_.done()), worker_.queued(), worker_.current(),
+                                 flags_.value(kIter),
+                                 flags_.value(kBulk), lane_seq_[kBulk], flags_.value(kUrgent), lane_seq_[kUrgent],
+                                 flags_.value(kD2H), lane_seq_[kD2H], flags_.value(kP2P), lane_seq_[kP2P]);
+                }
+            });
+        }
     }
 
     ~GpuExecutor() override {
+        watchdog_stop_.store(true);
+        if (watchdog_.joinable()) watchdog_.join();
+        // error paths: drop queued copies and release every stream wait on a
+        // lane flag that will now never be written, so the device can drain
+        worker_.stop(true);
+        for (int l = kBulk; l <= kP2P; ++l) flags_.force(l, lane_seq_[l]);
         cudaSetDevice(o_.decode_device);
         cudaDeviceSynchronize();
         if (pair_) {
@@ -279,15 +316,15 @@ class GpuExecutor : public prefixsim::EngineObserver {
             cudaDeviceSynchronize();
             cudaSetDevice(o_.decode_device);
         }
-        for (auto p : plan_host_) cudaFreeHost(p);
-        for (auto p : plan_dev_) cudaFree(p);
+        if (plan_arena_host_) cudaFreeHost(plan_arena_host_);
+        if (plan_arena_dev_) cudaFree(plan_arena_dev_);
         for (auto e : it_end_) cudaEventDestroy(e);
         for (auto e : att_beg_) cudaEventDestroy(e);
         for (auto e : att_end_) cudaEventDestroy(e);
-        for (auto p : ts_dev_) cudaFree(p);
+        if (ts_arena_) cudaFreeHost(ts_arena_);
         for (auto& pr : copy_timers_) {
-            cudaEventDestroy(pr.a);
-            cudaEventDestroy(pr.b);
+            if (pr.a) cudaEventDestroy(pr.a);
+            if (pr.b) cudaEventDestroy(pr.b);
         }
         cudaEventDestroy(win_beg_);
         cudaEventDestroy(win_end_);
@@ -328,6 +365,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
 
     void on_transfer(const prefixsim::TransferRecord& t) override {
         const auto t0 = clock_now();
+        phase_.store(1);
         const int k = xfer_kind(t.kind);
         if (k >= 0) {
             stats_.logical_bytes[k] += t.bytes;
@@ -349,14 +387,14 @@ class GpuExecutor : public prefixsim::EngineObserver {
                 break;
             }
             case ASV_XFER_STRAY_PREFETCH:
-                begin_xfer_group(Lane::kUrgent);
+                begin_xfer_group(kUrgent);
                 fetch_from_host(t.request_id, staging_pool());
                 end_xfer_group();
                 break;
             case ASV_XFER_ADMIT:
                 if (!aligned_) {
                     // FCFS swap-in / disaggregated admit: host pool -> decode pages (PCIe)
-                    begin_xfer_group(Lane::kUrgent);
+                    begin_xfer_group(kUrgent);
                     fetch_from_host(t.request_id, &dec_);
                     end_xfer_group();
                 } else {
@@ -366,7 +404,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
                 break;
             case ASV_XFER_EVICT:
                 if (!aligned_) {
-                    begin_xfer_group(Lane::kD2H);
+                    begin_xfer_group(kD2H);
                     write_back_to_host(t.request_id);
                     end_xfer_group();
                 } else {
@@ -375,7 +413,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
                 break;
             case ASV_XFER_SPILL:
             case ASV_XFER_FLUSH:
-                begin_xfer_group(Lane::kD2H);
+                begin_xfer_group(kD2H);
                 write_back_to_host(t.request_id);
                 end_xfer_group();
                 break;
@@ -383,10 +421,12 @@ class GpuExecutor : public prefixsim::EngineObserver {
                 break;  // prefill_offload: prefill is off the decode path (its KV lands in the pool)
         }
         host_ms_ += ms_since(t0);
+        host_copy_ms_ += ms_since(t0);
     }
 
     void on_iteration(const prefixsim::IterationRecord& rec, const std::vector<prefixsim::RunningMember>& running) override {
         const auto t0 = clock_now();
+        phase_.store(2);
         ++iterations_total_;
         const int64_t seq = rec.seq;
         const bool exec = seq >= o_.exec_begin && (o_.exec_end < 0 || seq < o_.exec_end);
@@ -409,7 +449,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
         const int64_t e = executed_++;
         const size_t slot = static_cast<size_t>(e % ring_);
         // throttle: the slot's previous iteration must be complete before reuse
-        if (e >= ring_) retire(slot);
+        if (e >= ring_) retire_through(e - ring_);
         if (static_cast<int64_t>(running.size()) > max_rows_) throw std::runtime_error("batch exceeds q/out rows");
 
         // CSR page table in running order (= the reference's prefix_lengths order)
@@ -424,7 +464,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
         }
         asv_attn_plan plan{};
         if (asv_attn_plan_build(&shape_, static_cast<int32_t>(running.size()), seq_.data(), indptr_.data(),
-                                indices_.data(), workers_, plan_host_[slot], plan_cap_, &plan) != ASV_OK) {
+                                indices_.data(), workers_, plan_scratch_.data(), plan_cap_, &plan) != ASV_OK) {
             throw std::runtime_error(asv_last_error());
         }
         if (plan.total_splits > ws_splits_) throw std::runtime_error("attention workspace too small");
@@ -433,22 +473,29 @@ class GpuExecutor : public prefixsim::EngineObserver {
             ASV_CUDA(cudaEventRecord(win_beg_, compute_));
             window_open_ = true;
         }
+        if (worker_.failed()) throw CudaError("copy worker: " + worker_.error());
         // admitted requests whose KV is still in flight: the iteration waits for it
+        int64_t ready_waits = 0;
         for (const auto& m : running) {
             ReqKV& r = kv(m.id);
-            if (r.ready != nullptr) {
-                ASV_CUDA(cudaStreamWaitEvent(compute_, r.ready, 0));
-                r.ready = nullptr;
+            if (r.ready_slot >= 0) {
+                if (!flags_.reached(r.ready_slot, r.ready_v)) {
+                    flags_.wait(compute_, r.ready_slot, r.ready_v);
+                    ++ready_waits;
+                }
+                r.ready_slot = -1;
             }
         }
-        ASV_CUDA(cudaMemcpyAsync(plan_dev_[slot], plan_host_[slot], static_cast<size_t>(plan.total_int32) * 4,
-                                 cudaMemcpyHostToDevice, compute_));
+        const int64_t pw = plan_region(e, (static_cast<int64_t>(plan.total_int32) + 3) & ~int64_t(3));
+        std::memcpy(plan_arena_host_ + pw, plan_scratch_.data(), static_cast<size_t>(plan.total_int32) * 4);
+        if (asv_plan_upload(plan_arena_host_ + pw, plan_arena_dev_ + pw, plan.total_int32, compute_) != ASV_OK)
+            throw CudaError(asv_last_error());
         ASV_CUDA(cudaEventRecord(att_beg_[slot], compute_));
         asv_attn_args args{};
         args.q = q_;
         args.kv_pool = dec_.base();
         args.pool_pages = dec_.size();
-        args.plan_dev = plan_dev_[slot];
+        args.plan_dev = plan_arena_dev_ + pw;
         args.plan = &plan;
         args.k_new = k_new_;
         args.v_new = v_new_;
@@ -461,13 +508,19 @@ class GpuExecutor : public prefixsim::EngineObserver {
         for (int l = 0; l < o_.num_layers; ++l) {
             args.layer = l;
             args.launch_index = launches_++;
-            args.warp_timestamps = (timed && l == 0) ? ts_dev_[slot] : nullptr;
+            args.warp_timestamps = (timed && l == 0) ? ts_slot(slot) : nullptr;
+            args.pdl = l == 0 ? 0 : o_.pdl;  // layer 0 reads the plan the upload kernel just wrote
             if (asv_decode_attention(&shape_, &args, compute_) != ASV_OK) throw CudaError(asv_last_error());
         }
         ASV_CUDA(cudaEventRecord(att_end_[slot], compute_));
         ASV_CUDA(cudaEventRecord(it_end_[slot], compute_));
-        last_it_end_ = it_end_[slot];
+        flags_.write(compute_, kIter, static_cast<uint32_t>(e + 1));  // executed iterations complete
         slot_timed_[slot] = timed ? 1 : 0;
+        if (tracing_) {
+            slot_seq_[slot] = seq;
+            slot_b_[slot] = static_cast<int64_t>(running.size());
+            slot_waits_[slot] = ready_waits;
+        }
         if (timed) {
             ++stats_.iterations_timed;
             stats_.tokens_timed += static_cast<int64_t>(running.size());
@@ -485,9 +538,14 @@ class GpuExecutor : public prefixsim::EngineObserver {
             last_timed_end_ = true;
         }
         host_ms_ += ms_since(t0);
+        if (exec) host_iter_ms_ += ms_since(t0);
     }
 
     void finish(const prefixsim::MetricsLog& log, asv_engine_stats* out) {
+        phase_.store(3);
+        worker_.drain();
+        phase_.store(4);
+        if (worker_.failed()) throw CudaError("copy worker: " + worker_.error());
         ASV_CUDA(cudaSetDevice(o_.decode_device));
         if (window_open_) ASV_CUDA(cudaEventRecord(win_end_, compute_));
         ASV_CUDA(cudaStreamSynchronize(compute_));
@@ -497,16 +555,54 @@ class GpuExecutor : public prefixsim::EngineObserver {
         ASV_CUDA(cudaStreamSynchronize(urgent_));
         ASV_CUDA(cudaSetDevice(o_.decode_device));
         ASV_CUDA(cudaStreamSynchronize(p2p_));
-        for (int64_t e = std::max<int64_t>(0, executed_ - ring_); e < executed_; ++e) retire(static_cast<size_t>(e % ring_));
+        retire_through(executed_ - 1);
         if (window_open_) {
             float ms = 0.f;
             ASV_CUDA(cudaEventElapsedTime(&ms, win_beg_, win_end_));
             stats_.window_ms = ms;
         }
+        std::vector<std::pair<float, float>> pcie;  // PCIe copy groups relative to the window start
         for (auto& pr : copy_timers_) {
             float ms = 0.f;
             if (cudaEventElapsedTime(&ms, pr.a, pr.b) == cudaSuccess) {
                 (pr.p2p ? stats_.p2p_busy_ms : stats_.h2d_busy_ms) += ms;
+            }
+            float a = 0.f, b = 0.f;
+            if (!pr.p2p && window_open_ && cudaEventElapsedTime(&a, win_beg_, pr.a) == cudaSuccess &&
+                cudaEventElapsedTime(&b, win_beg_, pr.b) == cudaSuccess) {
+                pcie.emplace_back(std::max(0.f, a), std::min(b, static_cast<float>(stats_.window_ms)));
+                if (tracing_) {
+                    trace_.push_back(std::string("{\"copy\":\"") + pr.lane + "\",\"seq\":" + std::to_string(pr.seq) +
+                                     ",\"bytes\":" + std::to_string(pr.bytes) + ",\"t0\":" + std::to_string(a) +
+                                     ",\"t1\":" + std::to_string(b) + "}");
+                }
+            }
+        }
+        cudaGetLastError();
+        std::sort(pcie.begin(), pcie.end());
+        float cur_a = -1.f, cur_b = -1.f;
+        for (const auto& [a, b] : pcie) {
+            if (b <= a) continue;
+            if (a > cur_b) {
+                if (cur_b > cur_a) stats_.pcie_union_ms += cur_b - cur_a;
+                cur_a = a;
+                cur_b = b;
+            } else {
+                cur_b = std::max(cur_b, b);
+            }
+        }
+        if (cur_b > cur_a) stats_.pcie_union_ms += cur_b - cur_a;
+        stats_.host_wait_ms = host_wait_ms_ + dec_.wait_ms() + (pair_ ? pre_.wait_ms() : 0.0);
+        if (tracing_) {
+            trace_.push_back("{\"host_wait\":{\"retire\":" + std::to_string(host_wait_ms_) + ",\"plan_arena\":" +
+                             std::to_string(arena_wait_ms_) + ",\"reclaim\":" +
+                             std::to_string(dec_.wait_ms() + (pair_ ? pre_.wait_ms() : 0.0)) +
+                             "},\"host_copy_ms\":" +
+                             std::to_string(host_copy_ms_) + ",\"host_iter_ms\":" + std::to_string(host_iter_ms_) +
+                             ",\"executed\":" + std::to_string(executed_) + "}");
+            if (FILE* f = std::fopen(std::getenv("ASV_TRACE"), "w")) {
+                for (const auto& line : trace_) std::fprintf(f, "%s\n", line.c_str());
+                std::fclose(f);
             }
         }
         stats_.iterations_total = iterations_total_;
@@ -581,42 +677,106 @@ class GpuExecutor : public prefixsim::EngineObserver {
         ASV_CUDA(cudaMemcpy(dst, h.data(), static_cast<size_t>(elems) * 2, cudaMemcpyHostToDevice));
     }
 
-    // group copies issued by one decision so one event pair times them
-    // Batch prefetches run on xfer_, small urgent H2D moves (strays, swap-ins) on
+    // Copies issued by one decision form a group (one timer pair).  Batch
+    // prefetches run on xfer_, small urgent H2D moves (strays, swap-ins) on
     // urgent_ so they never queue behind a whole batch, D2H on d2h_ (both PCIe
-    // directions at once).
-    enum class Lane { kBulk, kUrgent, kD2H };
-    void begin_xfer_group(Lane lane_sel = Lane::kBulk) {
-        group_timed_ = copies_active() && in_window();
-        cur_ = lane_sel == Lane::kD2H ? d2h_ : (lane_sel == Lane::kUrgent ? urgent_ : xfer_);
-        cur_ev_ = lane_sel == Lane::kD2H ? &d2h_ev_ : (lane_sel == Lane::kUrgent ? &urgent_ev_ : &xfer_ev_);
-        if (!copies_active()) return;
-        ASV_CUDA(cudaSetDevice(xfer_device()));
-        // pages written/read below may have been used by the last launched iteration
-        cudaEvent_t& waited = lane_sel == Lane::kD2H ? waited_it_end_d2h_
-                              : (lane_sel == Lane::kUrgent ? waited_it_end_urg_ : waited_it_end_);
-        if (last_it_end_ != nullptr && waited != last_it_end_) {
-            ASV_CUDA(cudaStreamWaitEvent(cur_, last_it_end_, 0));
-            waited = last_it_end_;
-        }
-        if (group_timed_) {
-            CopyTimer t{};
-            ASV_CUDA(cudaEventCreate(&t.a));
-            ASV_CUDA(cudaEventCreate(&t.b));
-            ASV_CUDA(cudaEventRecord(t.a, cur_));
-            copy_timers_.push_back(t);
-        }
+    // directions at once), admits/evicts of a pair on p2p_.  Every operation on
+    // those streams is posted to the copy worker thread.
+    enum Lane { kIter = 0, kBulk = 1, kUrgent = 2, kD2H = 3, kP2P = 4, kLanes = 5 };
+    cudaStream_t lane_stream(int lane) const {
+        return lane == kD2H ? d2h_ : lane == kUrgent ? urgent_ : lane == kP2P ? p2p_ : xfer_;
     }
-    cudaEvent_t end_xfer_group() {
-        if (!copies_active()) return nullptr;
-        if (group_timed_) ASV_CUDA(cudaEventRecord(copy_timers_.back().b, cur_));
-        cudaEvent_t ev = cur_ev_->record(cur_);
-        for (auto id : group_ready_) kv(id).ready = ev;
-        group_ready_.clear();
-        for (auto& q : group_quarantine_) q.first->release_after(ev, std::move(q.second));
-        group_quarantine_.clear();
+    int lane_device(int lane) const { return lane == kP2P ? o_.decode_device : xfer_device(); }
+
+    // the lane's stream waits for executed iteration `hz` (skipped when it is
+    // known complete, or already awaited on that stream)
+    void lane_wait_iteration(int lane, int64_t hz) {
+        if (hz < 0 || hz + 1 <= waited_iter_[lane]) return;
+        if (flags_.reached(kIter, static_cast<uint32_t>(hz + 1))) return;
+        waited_iter_[lane] = hz + 1;
+        ++stats_.hazard_waits;
+        const cudaStream_t st = lane_stream(lane);
+        const int dev = lane_device(lane);
+        const uint32_t v = static_cast<uint32_t>(hz + 1);
+        worker_.post([this, st, dev, v] {
+            ASV_CUDA(cudaSetDevice(dev));
+            flags_.wait(st, kIter, v);
+        }, "wait_iter");
+    }
+    // the lane's stream waits for another lane's copy (a request's readiness)
+    void lane_wait_ready(int lane, ReqKV& r) {
+        if (r.ready_slot < 0) return;
+        const int slot = r.ready_slot;
+        const uint32_t v = r.ready_v;
+        r.ready_slot = -1;
+        if (slot == lane || flags_.reached(slot, v)) return;  // same stream: ordered already
+        const cudaStream_t st = lane_stream(lane);
+        const int dev = lane_device(lane);
+        worker_.post([this, st, dev, slot, v] {
+            ASV_CUDA(cudaSetDevice(dev));
+            flags_.wait(st, slot, v);
+        }, "wait_ready");
+    }
+    // the lane's stream announces everything posted so far: returns the value
+    uint32_t lane_signal(int lane) {
+        const uint32_t v = ++lane_seq_[lane];
+        const cudaStream_t st = lane_stream(lane);
+        const int dev = lane_device(lane);
+        worker_.post([this, st, dev, lane, v] {
+            ASV_CUDA(cudaSetDevice(dev));
+            flags_.write(st, lane, v);
+        }, "signal");
+        return v;
+    }
+    void timer_begin(int lane, bool p2p) {
+        CopyTimer t{};
+        t.p2p = p2p;
+        t.lane = lane == kD2H ? 'd' : lane == kUrgent ? 'u' : lane == kP2P ? 'p' : 'b';
+        t.seq = cur_seq_;
+        t.bytes = -(stats_.h2d_bytes + stats_.d2h_bytes + stats_.p2p_bytes);
+        const cudaStream_t st = lane_stream(lane);
+        const int dev = lane_device(lane);
+        // events are created here (not on the worker) and recorded there
+        ASV_CUDA(cudaSetDevice(dev));
+        ASV_CUDA(cudaEventCreate(&t.a));
+        ASV_CUDA(cudaEventCreate(&t.b));
         ASV_CUDA(cudaSetDevice(o_.decode_device));
-        return ev;
+        copy_timers_.push_back(t);
+        const cudaEvent_t ev = t.a;
+        worker_.post([st, dev, ev] {
+            ASV_CUDA(cudaSetDevice(dev));
+            ASV_CUDA(cudaEventRecord(ev, st));
+        }, "timer_a");
+    }
+    void timer_end(int lane) {
+        CopyTimer& t = copy_timers_.back();
+        t.bytes += stats_.h2d_bytes + stats_.d2h_bytes + stats_.p2p_bytes;
+        const cudaStream_t st = lane_stream(lane);
+        const int dev = lane_device(lane);
+        const cudaEvent_t ev = t.b;
+        worker_.post([st, dev, ev] {
+            ASV_CUDA(cudaSetDevice(dev));
+            ASV_CUDA(cudaEventRecord(ev, st));
+        }, "timer_b");
+    }
+
+    void begin_xfer_group(int lane = kBulk) {
+        lane_ = lane;
+        group_timed_ = copies_active() && in_window();
+        if (!copies_active()) return;
+        // D2H reads pages the last launched iteration may still use; H2D lanes
+        // only wait for the hazards of the pages they allocate (fetch_from_host)
+        if (lane == kD2H) lane_wait_iteration(kD2H, executed_ - 1);
+        if (group_timed_) timer_begin(lane, false);
+    }
+    void end_xfer_group() {
+        if (!copies_active()) return;
+        if (group_timed_) timer_end(lane_);
+        if (!group_quarantine_.empty()) {
+            const uint32_t v = lane_signal(lane_);
+            for (auto& q : group_quarantine_) q.first->release_after(lane_, v, std::move(q.second));
+            group_quarantine_.clear();
+        }
     }
 
     char* host_page(prefixsim::RequestId id, int64_t j) const {
@@ -624,20 +784,31 @@ class GpuExecutor : public prefixsim::EngineObserver {
         return arena_ + a * page_bytes_;
     }
 
-    // copy `tokens` tokens of KV between host pages and device pages (exact bytes)
-    // KV moves go through the C-ABI copy routines (kv_copy.cpp): whole pages as
-    // 2-D copies, the valid rows of a partial last page as one 3-D copy.
-    int64_t copy_kv(const std::vector<int32_t>& pages, const PagePool& pool, prefixsim::RequestId id, int64_t tokens,
-                    bool to_device) {
-        host_ptrs_.clear();
-        for (int64_t j = 0; j < (tokens + 15) / 16; ++j) host_ptrs_.push_back(host_page(id, j));
-        int64_t moved = 0;
-        const int rc = to_device ? asv_kv_copy_h2d(&shape_, pool.base(), pool.size(), pages.data(), tokens,
-                                                   host_ptrs_.data(), cur_, &moved)
-                                 : asv_kv_copy_d2h(&shape_, pool.base(), pool.size(), pages.data(), tokens,
-                                                   const_cast<void* const*>(host_ptrs_.data()), cur_, &moved);
-        if (rc != ASV_OK) throw CudaError(asv_last_error());
-        return moved;
+    // post one request's KV move between host pages and device pages (exact
+    // bytes) through the C-ABI copy routines (kv_copy.cpp): whole pages as 2-D
+    // copies, the valid rows of a partial last page as one 3-D copy
+    int64_t post_copy_kv(const std::vector<int32_t>& pages, const PagePool& pool, prefixsim::RequestId id,
+                         int64_t tokens, bool to_device) {
+        std::vector<void*> host;
+        host.reserve(static_cast<size_t>((tokens + 15) / 16));
+        for (int64_t j = 0; j < (tokens + 15) / 16; ++j) host.push_back(host_page(id, j));
+        const int64_t expect = tokens * row_bytes_all_;
+        const cudaStream_t st = lane_stream(lane_);
+        const int dev = lane_device(lane_);
+        void* base = pool.base();
+        const int64_t pool_pages = pool.size();
+        worker_.post([this, pages, host = std::move(host), base, pool_pages, tokens, to_device, st, dev, expect] {
+            ASV_CUDA(cudaSetDevice(dev));
+            int64_t moved = 0;
+            const int rc = to_device ? asv_kv_copy_h2d(&shape_, base, pool_pages, pages.data(), tokens,
+                                                       const_cast<const void* const*>(host.data()), st, &moved)
+                                     : asv_kv_copy_d2h(&shape_, base, pool_pages, pages.data(), tokens, host.data(), st,
+                                                       &moved);
+            if (rc != ASV_OK) throw CudaError(asv_last_error());
+            if (moved != expect) throw std::logic_error("kv copy moved " + std::to_string(moved) + " bytes, expected " +
+                                                        std::to_string(expect));
+        }, "copy_host");
+        return expect;
     }
 
     void fetch_from_host(prefixsim::RequestId id, PagePool* pool) {
@@ -646,13 +817,16 @@ class GpuExecutor : public prefixsim::EngineObserver {
         r.prefix = q.prefix_len;
         release_pages(r);  // (defensive) a request never holds pages while pooled
         const int64_t n = (q.prefix_len + 15) / 16;
-        for (int64_t j = 0; j < n; ++j) r.pages.push_back(pool->alloc());
+        int64_t hz = -1;
+        for (int64_t j = 0; j < n; ++j) r.pages.push_back(pool->alloc(&hz));
         r.where = pool == &dec_ ? ReqKV::kDecode : ReqKV::kPrefetch;
         if (!copies_active()) return;
-        const int64_t moved = copy_kv(r.pages, *pool, id, q.prefix_len, true);
+        lane_wait_iteration(lane_, hz);
+        const int64_t moved = post_copy_kv(r.pages, *pool, id, q.prefix_len, true);
         stats_.h2d_bytes += moved;
         if (group_timed_) stats_.h2d_bytes_window += moved;
-        r.ready = cur_ev_->record(cur_);  // this request is usable as soon as its own pages land
+        r.ready_slot = lane_;  // this request is usable as soon as its own pages land
+        r.ready_v = lane_signal(lane_);
     }
 
     void write_back_to_host(prefixsim::RequestId id) {
@@ -660,19 +834,17 @@ class GpuExecutor : public prefixsim::EngineObserver {
         const prefixsim::Request& q = (*requests_)[static_cast<std::size_t>(id)];
         PagePool* pool = r.where == ReqKV::kPrefetch ? &pre_ : &dec_;
         if (copies_active() && !r.pages.empty()) {
-            if (r.ready != nullptr) {
-                ASV_CUDA(cudaStreamWaitEvent(cur_, r.ready, 0));
-                r.ready = nullptr;
-            }
-            const int64_t moved = copy_kv(r.pages, *pool, id, q.prefix_len, false);
+            lane_wait_ready(lane_, r);
+            const int64_t moved = post_copy_kv(r.pages, *pool, id, q.prefix_len, false);
             stats_.d2h_bytes += moved;
             if (group_timed_) stats_.d2h_bytes_window += moved;
             group_quarantine_.push_back({pool, std::move(r.pages)});
             r.pages.clear();
         } else {
-            pool->release(r.pages);
+            pool->release(r.pages, pool == &dec_ ? executed_ - 1 : -1);
             r.pages.clear();
         }
+        r.ready_slot = -1;
         r.where = ReqKV::kHost;
     }
 
@@ -684,31 +856,26 @@ class GpuExecutor : public prefixsim::EngineObserver {
         }
         // pair: prefetch GPU -> decode GPU over NVLink
         std::vector<int32_t> dst;
-        for (size_t j = 0; j < r.pages.size(); ++j) dst.push_back(dec_.alloc());
+        int64_t hz = -1;
+        for (size_t j = 0; j < r.pages.size(); ++j) dst.push_back(dec_.alloc(&hz));
         if (copies_active()) {
-            ASV_CUDA(cudaSetDevice(o_.decode_device));
-            if (r.ready != nullptr) ASV_CUDA(cudaStreamWaitEvent(p2p_, r.ready, 0));
-            if (last_it_end_ != nullptr) ASV_CUDA(cudaStreamWaitEvent(p2p_, last_it_end_, 0));
-            CopyTimer t{};
+            lane_wait_ready(kP2P, r);
+            lane_wait_iteration(kP2P, hz);  // destination pages: only the iteration that last used them
             const bool timed = in_window();
-            if (timed) {
-                ASV_CUDA(cudaEventCreate(&t.a));
-                ASV_CUDA(cudaEventCreate(&t.b));
-                t.p2p = true;
-                ASV_CUDA(cudaEventRecord(t.a, p2p_));
-            }
-            const int64_t moved = copy_peer(dst, dec_, r.pages, pre_, (*requests_)[static_cast<std::size_t>(id)].prefix_len);
+            if (timed) timer_begin(kP2P, true);
+            const int64_t moved = post_copy_peer(dst, dec_, r.pages, pre_,
+                                                 (*requests_)[static_cast<std::size_t>(id)].prefix_len);
             stats_.p2p_bytes += moved;
             if (timed) {
-                ASV_CUDA(cudaEventRecord(t.b, p2p_));
-                copy_timers_.push_back(t);
                 stats_.p2p_bytes_window += moved;
+                timer_end(kP2P);
             }
-            cudaEvent_t ev = p2p_ev_.record(p2p_);
-            pre_.release_after(ev, std::move(r.pages));
-            r.ready = ev;
+            const uint32_t v = lane_signal(kP2P);
+            pre_.release_after(kP2P, v, std::move(r.pages));
+            r.ready_slot = kP2P;
+            r.ready_v = v;
         } else {
-            pre_.release(r.pages);
+            pre_.release(r.pages, -1);
         }
         r.pages = std::move(dst);
         r.where = ReqKV::kDecode;
@@ -720,48 +887,131 @@ class GpuExecutor : public prefixsim::EngineObserver {
         std::vector<int32_t> dst;
         for (size_t j = 0; j < r.pages.size(); ++j) dst.push_back(pre_.alloc());
         if (copies_active()) {
-            ASV_CUDA(cudaSetDevice(o_.decode_device));
-            if (last_it_end_ != nullptr) ASV_CUDA(cudaStreamWaitEvent(p2p_, last_it_end_, 0));
-            const int64_t moved = copy_peer(dst, pre_, r.pages, dec_, (*requests_)[static_cast<std::size_t>(id)].prefix_len);
+            lane_wait_iteration(kP2P, executed_ - 1);  // the request ran in the last launched iteration
+            const int64_t moved = post_copy_peer(dst, pre_, r.pages, dec_,
+                                                 (*requests_)[static_cast<std::size_t>(id)].prefix_len);
             stats_.p2p_bytes += moved;
             if (in_window()) stats_.p2p_bytes_window += moved;
-            cudaEvent_t ev = p2p_ev_.record(p2p_);
-            dec_.release_after(ev, std::move(r.pages));
-            r.ready = ev;
+            const uint32_t v = lane_signal(kP2P);
+            dec_.release_after(kP2P, v, std::move(r.pages));
+            r.ready_slot = kP2P;
+            r.ready_v = v;
         } else {
-            dec_.release(r.pages);
+            dec_.release(r.pages, executed_ - 1);
         }
         r.pages = std::move(dst);
         r.where = ReqKV::kPrefetch;
     }
 
-    int64_t copy_peer(const std::vector<int32_t>& dst, const PagePool& dpool, const std::vector<int32_t>& src,
-                      const PagePool& spool, int64_t tokens) {
-        int64_t moved = 0;
-        if (asv_kv_copy_d2d(&shape_, dpool.base(), dpool.size(), dpool.device(), dst.data(), spool.base(), spool.size(),
-                            spool.device(), src.data(), tokens, p2p_, &moved) != ASV_OK) {
-            throw CudaError(asv_last_error());
-        }
-        return moved;
+    int64_t post_copy_peer(const std::vector<int32_t>& dst, const PagePool& dpool, const std::vector<int32_t>& src,
+                           const PagePool& spool, int64_t tokens) {
+        const int64_t expect = tokens * row_bytes_all_;
+        const cudaStream_t st = p2p_;
+        const int dev = o_.decode_device;
+        void* dbase = dpool.base();
+        void* sbase = spool.base();
+        const int64_t dn = dpool.size(), sn = spool.size();
+        const int ddev = dpool.device(), sdev = spool.device();
+        worker_.post([this, dst, src, dbase, sbase, dn, sn, ddev, sdev, tokens, st, dev, expect] {
+            ASV_CUDA(cudaSetDevice(dev));
+            int64_t moved = 0;
+            if (asv_kv_copy_d2d(&shape_, dbase, dn, ddev, dst.data(), sbase, sn, sdev, src.data(), tokens, st,
+                                &moved) != ASV_OK) {
+                throw CudaError(asv_last_error());
+            }
+            if (moved != expect) throw std::logic_error("kv peer copy moved a wrong byte count");
+        }, "copy_peer");
+        return expect;
     }
 
     void release_pages(ReqKV& r) {
         if (r.pages.empty()) return;
-        (r.where == ReqKV::kPrefetch ? pre_ : dec_).release(r.pages);
+        if (r.where == ReqKV::kPrefetch) pre_.release(r.pages, -1);
+        else dec_.release(r.pages, executed_ - 1);  // the last launched iteration may still read them
         r.pages.clear();
-        r.ready = nullptr;
+        r.ready_slot = -1;
         r.where = ReqKV::kHost;
     }
 
+    // One move of every copy shape the run can issue (whole page: 2-D, partial
+    // page: 3-D; H2D, D2H, device-local and peer D2D), before any stream waits
+    // on a sequence flag: the runtime loads its internal copy kernels lazily at
+    // first use, and that load blocks on device-wide progress (a deadlock once
+    // a stream is parked on a flag the blocked thread would write; measured).
+    void warm_up_copies() {
+        const int32_t a[2] = {0, 1}, b[2] = {2, 3};
+        const void* host[2] = {arena_, arena_pages_ > 1 ? arena_ + page_bytes_ : arena_};
+        int64_t moved = 0;
+        ASV_CUDA(cudaSetDevice(xfer_device()));
+        PagePool& stage = *staging_pool();
+        if (asv_kv_copy_h2d(&shape_, stage.base(), stage.size(), a, 17, host, xfer_, &moved) != ASV_OK ||
+            asv_kv_copy_d2h(&shape_, stage.base(), stage.size(), a, 17, const_cast<void* const*>(host), d2h_, &moved) !=
+                ASV_OK) {
+            throw CudaError(asv_last_error());
+        }
+        ASV_CUDA(cudaStreamSynchronize(xfer_));
+        ASV_CUDA(cudaStreamSynchronize(d2h_));
+        ASV_CUDA(cudaSetDevice(o_.decode_device));
+        if (asv_kv_copy_d2d(&shape_, dec_.base(), dec_.size(), dec_.device(), b, dec_.base(), dec_.size(),
+                            dec_.device(), a, 17, p2p_, &moved) != ASV_OK) {
+            throw CudaError(asv_last_error());
+        }
+        if (pair_ && (asv_kv_copy_d2d(&shape_, dec_.base(), dec_.size(), dec_.device(), a, pre_.base(), pre_.size(),
+                                      pre_.device(), a, 17, p2p_, &moved) != ASV_OK ||
+                      asv_kv_copy_d2d(&shape_, pre_.base(), pre_.size(), pre_.device(), b, dec_.base(), dec_.size(),
+                                      dec_.device(), b, 17, p2p_, &moved) != ASV_OK)) {
+            throw CudaError(asv_last_error());
+        }
+        ASV_CUDA(cudaStreamSynchronize(p2p_));
+    }
+
+    uint64_t* ts_slot(size_t slot) const { return ts_arena_ + slot * static_cast<size_t>(workers_) * 2; }
+
+    // retire every executed iteration up to and including `e`, in order
+    void retire_through(int64_t e) {
+        for (; retired_upto_ <= e; ++retired_upto_) retire(static_cast<size_t>(retired_upto_ % ring_));
+        while (!live_plans_.empty() && live_plans_.front().first < retired_upto_) live_plans_.pop_front();
+    }
+
+    // `words` contiguous words of the plan arena for executed iteration `e`
+    // (word offset); waits for the oldest in-flight iterations while their plans
+    // still occupy the space
+    int64_t plan_region(int64_t e, int64_t words) {
+        if (words > arena_words_) throw std::runtime_error("plan larger than the plan arena");
+        if (arena_head_ % arena_words_ + words > arena_words_) arena_head_ += arena_words_ - arena_head_ % arena_words_;
+        const int64_t begin = arena_head_, end = begin + words;
+        // a live plan [b, ...) is overwritten once the new region, one lap back, passes b
+        if (!live_plans_.empty() && live_plans_.front().second < end - arena_words_) {
+            const auto t0 = clock_now();
+            while (!live_plans_.empty() && live_plans_.front().second < end - arena_words_) {
+                retire_through(live_plans_.front().first);
+            }
+            arena_wait_ms_ += ms_since(t0);
+        }
+        live_plans_.emplace_back(e, begin);
+        arena_head_ = end;
+        return begin % arena_words_;
+    }
+
     void retire(size_t slot) {
+        const auto t0 = clock_now();
         ASV_CUDA(cudaEventSynchronize(it_end_[slot]));
+        host_wait_ms_ += ms_since(t0);
         if (slot_timed_[slot]) {
             float ms = 0.f;
             ASV_CUDA(cudaEventElapsedTime(&ms, att_beg_[slot], att_end_[slot]));
             stats_.attn_ms += ms;
+            if (tracing_) {
+                float a = 0.f, b = 0.f;
+                ASV_CUDA(cudaEventElapsedTime(&a, win_beg_, att_beg_[slot]));
+                ASV_CUDA(cudaEventElapsedTime(&b, win_beg_, att_end_[slot]));
+                trace_.push_back("{\"it\":" + std::to_string(slot_seq_[slot]) + ",\"b\":" +
+                                 std::to_string(slot_b_[slot]) + ",\"waits\":" + std::to_string(slot_waits_[slot]) +
+                                 ",\"t0\":" + std::to_string(a) + ",\"t1\":" + std::to_string(b) + "}");
+            }
             slot_timed_[slot] = 0;
             // measured bubble of the layer-0 launch: idle warp time inside its span
-            ASV_CUDA(cudaMemcpy(ts_host_.data(), ts_dev_[slot], ts_host_.size() * 8, cudaMemcpyDeviceToHost));
+            std::memcpy(ts_host_.data(), ts_slot(slot), ts_host_.size() * 8);  // mapped, complete at it_end_
             uint64_t lo = UINT64_MAX, hi = 0;
             double busy = 0.0;
             for (int32_t w = 0; w < workers_; ++w) {
@@ -789,6 +1039,9 @@ class GpuExecutor : public prefixsim::EngineObserver {
     struct CopyTimer {
         cudaEvent_t a = nullptr, b = nullptr;
         bool p2p = false;
+        char lane = 'b';       // b bulk H2D, u urgent H2D, d D2H, p P2P (trace only)
+        int64_t seq = 0;       // boundary that issued it
+        int64_t bytes = 0;
     };
     asv_engine_opts o_;
     asv_attn_shape shape_{};
@@ -796,11 +1049,15 @@ class GpuExecutor : public prefixsim::EngineObserver {
     bool pair_ = false;
     int64_t dec_pages_ = 0, pre_pages_ = 0;
     PagePool dec_, pre_;
-    cudaStream_t compute_ = nullptr, p2p_ = nullptr, xfer_ = nullptr, d2h_ = nullptr, urgent_ = nullptr,
-                 cur_ = nullptr;
-    EventRing xfer_ev_, d2h_ev_, urgent_ev_, p2p_ev_;
-    EventRing* cur_ev_ = nullptr;
-    cudaEvent_t waited_it_end_d2h_ = nullptr, waited_it_end_urg_ = nullptr;
+    cudaStream_t compute_ = nullptr, p2p_ = nullptr, xfer_ = nullptr, d2h_ = nullptr, urgent_ = nullptr;
+    SeqFlags flags_;
+    CopyWorker worker_;
+    std::thread watchdog_;                  // ASV_WATCHDOG=1: progress report every 5 s (debugging)
+    std::atomic<bool> watchdog_stop_{false};
+    std::atomic<int> phase_{0};             // 1 decide/copy, 2 iteration launch, 3 finish
+    int lane_ = kBulk;                      // lane of the open copy group
+    uint32_t lane_seq_[kLanes] = {};         // last value each lane announced
+    int64_t waited_iter_[kLanes] = {};       // iteration flag value each lane's stream already waits for
     char* arena_ = nullptr;
     int64_t arena_pages_ = 1;
     int32_t workers_ = 0;
@@ -810,24 +1067,31 @@ class GpuExecutor : public prefixsim::EngineObserver {
     int32_t ws_splits_ = 0;
     int ring_ = 16;
     int64_t plan_cap_ = 0;
-    std::vector<int32_t*> plan_host_, plan_dev_;
+    std::vector<int32_t> plan_scratch_;
+    int32_t *plan_arena_host_ = nullptr, *plan_arena_dev_ = nullptr;
+    int64_t arena_words_ = 0, arena_head_ = 0;   // absolute word counter (position = head % arena)
+    std::deque<std::pair<int64_t, int64_t>> live_plans_;  // (executed index, absolute begin) in issue order
+    int64_t retired_upto_ = 0;                   // every executed iteration below this is retired
+    uint64_t* ts_arena_ = nullptr;
     std::vector<cudaEvent_t> it_end_, att_beg_, att_end_;
     std::vector<int> slot_timed_;
-    cudaEvent_t last_it_end_ = nullptr, waited_it_end_ = nullptr;
     cudaEvent_t win_beg_ = nullptr, win_end_ = nullptr;
     bool window_open_ = false, last_timed_end_ = false, group_timed_ = false, admit_moved_ = false;
     std::vector<ReqKV> reqs_;
     std::vector<prefixsim::RequestId> pending_batch_;
-    std::vector<prefixsim::RequestId> group_ready_;
     std::vector<std::pair<PagePool*, std::vector<int32_t>>> group_quarantine_;
-    std::vector<CopyTimer> copy_timers_;
+    std::vector<CopyTimer> copy_timers_;  // events created by the engine thread, recorded by the worker
     std::vector<int32_t> seq_, indptr_, indices_;
-    std::vector<const void*> host_ptrs_;
     int64_t executed_ = 0, iterations_total_ = 0;
     uint32_t launches_ = 0;
-    double host_ms_ = 0.0;
+    double host_ms_ = 0.0, host_wait_ms_ = 0.0, arena_wait_ms_ = 0.0;
+    double host_copy_ms_ = 0.0, host_iter_ms_ = 0.0;  // trace: issue cost of copies / executed iterations
+    // ASV_TRACE=<file>: per timed iteration / copy group GPU start-end (ms from the window start)
+    const bool tracing_ = std::getenv("ASV_TRACE") != nullptr;
+    std::vector<std::string> trace_;
+    std::vector<int64_t> slot_seq_, slot_b_, slot_waits_;
     double first_timed_start_ = -1.0, last_timed_end_ms_ = 0.0;
-    std::vector<uint64_t*> ts_dev_;
+
     std::vector<uint64_t> ts_host_;
     double busy_ns_ = 0.0, span_ns_ = 0.0;
     asv_engine_stats stats_{};

@@ -3,9 +3,9 @@
 // <-> decode GPU.  Replace the PRICED transfers of the reference
 // (transfer_time, cluster_sim.hpp:60-66; start_async_transfer / sync_transfer
 // :220-232) with copy-engine work.  A request with s tokens moves floor(s/16)
-// whole pages (one 2-D copy each: L slices) and the s%16 valid rows of its last
-// page (one 3-D copy: rows x blocks x layers) — exactly s * kv_bytes_per_token
-// bytes (cluster_sim.hpp:239-241).
+// whole pages (one 2-D copy each: L slices at its page group's < 2 GiB layer
+// pitch) and the s%16 valid rows of its last page (one 3-D copy: rows x blocks
+// x layers) — exactly s * kv_bytes_per_token bytes (cluster_sim.hpp:239-241).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -40,6 +40,33 @@ cudaPitchedPtr pitched(const void* base, int64_t rows_per_layer) {
     return make_cudaPitchedPtr(const_cast<void*>(base), kBlock, kBlock, static_cast<size_t>(rows_per_layer));
 }
 
+// A layer-major pool in page groups (asv_internal.h): page p's layer-0 slice,
+// the layer pitch of its group, and its group's base (3-D views of a group).
+struct PoolView {
+    char* base;
+    int64_t group_pages, layers, slice;
+    PoolView(const void* b, int64_t pool_pages, const Geo& g)
+        : base(static_cast<char*>(const_cast<void*>(b))),
+          group_pages(pool_group_pages(g.slice, pool_pages)),
+          layers(g.layers),
+          slice(g.slice) {}
+    char* page0(int32_t p) const { return base + pool_slot(p, group_pages, layers) * slice; }
+    size_t pitch() const { return static_cast<size_t>(group_pages * slice); }
+    char* group_base(int32_t p) const { return base + (p / group_pages) * group_pages * layers * slice; }
+    int64_t in_group(int32_t p) const { return p % group_pages; }
+};
+
+int check_pages(const int32_t* pages, int64_t n, int64_t pool_pages, const Geo& g) {
+    const int64_t usable = pool_usable_pages(g.slice, pool_pages);
+    for (int64_t j = 0; j < n; ++j) {
+        if (pages[j] < 0 || pages[j] >= usable) {
+            return fail(ASV_ERR_INVALID, "kv copy: page id " + std::to_string(pages[j]) + " outside the usable pool (" +
+                                             std::to_string(usable) + " pages)");
+        }
+    }
+    return ASV_OK;
+}
+
 // host <-> device, `to_device` selects the direction
 int host_device(const asv_attn_shape* shape, void* pool, int64_t pool_pages, const int32_t* pages, int64_t tokens,
                 void* const* host_pages, bool to_device, cudaStream_t st, int64_t* bytes_out) {
@@ -48,12 +75,13 @@ int host_device(const asv_attn_shape* shape, void* pool, int64_t pool_pages, con
     if (pool == nullptr || pages == nullptr || host_pages == nullptr || tokens < 0 || pool_pages < 1)
         return fail(ASV_ERR_INVALID, "bad kv copy arguments");
     const int64_t full = tokens / 16, rows = tokens % 16;
-    const size_t dpitch = static_cast<size_t>(pool_pages * g.slice);
+    if (int rc = check_pages(pages, (tokens + 15) / 16, pool_pages, g)) return rc;
+    const PoolView pv(pool, pool_pages, g);
+    const size_t dpitch = pv.pitch();
     const cudaMemcpyKind kind = to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
-    char* base = static_cast<char*>(pool);
     int64_t moved = 0;
     for (int64_t j = 0; j < full; ++j) {
-        char* d = base + static_cast<int64_t>(pages[j]) * g.slice;
+        char* d = pv.page0(pages[j]);
         char* h = static_cast<char*>(host_pages[j]);
         cudaError_t e = to_device ? cudaMemcpy2DAsync(d, dpitch, h, g.slice, g.slice, g.layers, kind, st)
                                   : cudaMemcpy2DAsync(h, g.slice, d, dpitch, g.slice, g.layers, kind, st);
@@ -62,9 +90,9 @@ int host_device(const asv_attn_shape* shape, void* pool, int64_t pool_pages, con
     }
     if (rows > 0) {
         cudaMemcpy3DParms m = {};
-        const cudaPitchedPtr dev = pitched(base, pool_pages * g.bps);
+        const cudaPitchedPtr dev = pitched(pv.group_base(pages[full]), pv.group_pages * g.bps);
         const cudaPitchedPtr host = pitched(host_pages[full], g.bps);
-        const cudaPos dpos = make_cudaPos(0, static_cast<size_t>(pages[full]) * g.bps, 0);
+        const cudaPos dpos = make_cudaPos(0, static_cast<size_t>(pv.in_group(pages[full]) * g.bps), 0);
         m.srcPtr = to_device ? host : dev;
         m.dstPtr = to_device ? dev : host;
         m.srcPos = to_device ? make_cudaPos(0, 0, 0) : dpos;
@@ -109,13 +137,14 @@ int asv_kv_copy_d2d(const asv_attn_shape* shape, void* dst_pool, int64_t dst_poo
         return fail(ASV_ERR_INVALID, "bad kv copy arguments");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int64_t full = tokens / 16, rows = tokens % 16;
-    const size_t dp = static_cast<size_t>(dst_pool_pages * g.slice), sp = static_cast<size_t>(src_pool_pages * g.slice);
-    char* db = static_cast<char*>(dst_pool);
-    const char* sb = static_cast<const char*>(src_pool);
+    const int64_t npg = (tokens + 15) / 16;
+    if (int rc = check_pages(dst_pages, npg, dst_pool_pages, g)) return rc;
+    if (int rc = check_pages(src_pages, npg, src_pool_pages, g)) return rc;
+    const PoolView dv(dst_pool, dst_pool_pages, g), sv(src_pool, src_pool_pages, g);
+    const size_t dp = dv.pitch(), sp = sv.pitch();
     int64_t moved = 0;
     for (int64_t j = 0; j < full; ++j) {
-        cudaError_t e = cudaMemcpy2DAsync(db + static_cast<int64_t>(dst_pages[j]) * g.slice, dp,
-                                          sb + static_cast<int64_t>(src_pages[j]) * g.slice, sp, g.slice, g.layers,
+        cudaError_t e = cudaMemcpy2DAsync(dv.page0(dst_pages[j]), dp, sv.page0(src_pages[j]), sp, g.slice, g.layers,
                                           cudaMemcpyDefault, st);
         if (e != cudaSuccess) return cuda_fail(e, "kv peer page copy");
         moved += g.page_bytes;
@@ -123,10 +152,10 @@ int asv_kv_copy_d2d(const asv_attn_shape* shape, void* dst_pool, int64_t dst_poo
     if (rows > 0) {
         const cudaExtent ext = make_cudaExtent(static_cast<size_t>(rows) * 256, static_cast<size_t>(g.bps),
                                                static_cast<size_t>(g.layers));
-        const cudaPitchedPtr d = pitched(db, dst_pool_pages * g.bps);
-        const cudaPitchedPtr s = pitched(sb, src_pool_pages * g.bps);
-        const cudaPos dpos = make_cudaPos(0, static_cast<size_t>(dst_pages[full]) * g.bps, 0);
-        const cudaPos spos = make_cudaPos(0, static_cast<size_t>(src_pages[full]) * g.bps, 0);
+        const cudaPitchedPtr d = pitched(dv.group_base(dst_pages[full]), dv.group_pages * g.bps);
+        const cudaPitchedPtr s = pitched(sv.group_base(src_pages[full]), sv.group_pages * g.bps);
+        const cudaPos dpos = make_cudaPos(0, static_cast<size_t>(dv.in_group(dst_pages[full]) * g.bps), 0);
+        const cudaPos spos = make_cudaPos(0, static_cast<size_t>(sv.in_group(src_pages[full]) * g.bps), 0);
         cudaError_t e;
         if (dst_device != src_device) {
             cudaMemcpy3DPeerParms m = {};

@@ -77,7 +77,7 @@ def engine_run(config, *, device: int = 0, prefetch_device: int | None = None,
                num_q_heads: int, num_kv_heads: int, num_layers: int, execute_transfers: bool,
                exec_begin: int = 0, exec_end: int = -1, timed_begin: int = 0, copy_begin: int | None = None,
                host_pool_bytes: int = 8 << 30, shard_index: int = 0, shard_count: int = 1,
-               pdl: bool = True, run_ahead: int = 16, policy: str | None = None,
+               pdl: bool = True, run_ahead: int = 256, policy: str | None = None,
                pair_mode: bool = False) -> dict:
     """Run the decode engine on the GPU (asv_engine_run): reference decisions executed for real."""
     text = config if isinstance(config, str) else json.dumps(config)

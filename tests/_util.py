@@ -57,9 +57,26 @@ def page_bytes(n_kv: int, num_layers: int) -> int:
     return num_layers * 2 * n_kv * 4096
 
 
+def group_pages(n_kv: int, pool_pages: int) -> int:
+    """pages per layer-major group: the largest equal split whose layer pitch is < 2 GiB (include/asv.h)."""
+    slice_ = 2 * n_kv * 4096
+    gmax = ((1 << 31) - 1) // slice_
+    return pool_pages // ((pool_pages + gmax - 1) // gmax)
+
+
 def block_view(pool: np.ndarray, n_kv: int, num_layers: int) -> np.ndarray:
-    """uint8 LAYER-MAJOR device pool -> [layers][pages][2][n_kv][4096] byte view (include/asv.h)."""
+    """uint8 LAYER-MAJOR device pool of ONE page group -> [layers][pages][2][n_kv][4096] byte view."""
+    assert group_pages(n_kv, pool_pages(pool, n_kv, num_layers)) == pool_pages(pool, n_kv, num_layers), \
+        "multi-group pool: use pool_block_offset"
     return pool.reshape(num_layers, -1, 2, n_kv, 4096)
+
+
+def pool_block_offset(n_kv: int, num_layers: int, pool_pages_: int, page: int, layer: int, kv: int,
+                      head: int) -> int:
+    """byte offset of block (page, layer, K|V, head) in a grouped layer-major pool (include/asv.h)."""
+    g = group_pages(n_kv, pool_pages_)
+    slot = (page // g) * g * num_layers + layer * g + page % g
+    return slot * 2 * n_kv * 4096 + (kv * n_kv + head) * 4096
 
 
 def pool_pages(pool: np.ndarray, n_kv: int, num_layers: int) -> int:

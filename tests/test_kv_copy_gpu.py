@@ -78,3 +78,17 @@ def test_h2d_d2h_d2d_roundtrip(n_kv, L, tokens):
         rows = min(16, tokens - 16 * j)
         assert np.array_equal(got[j, :, :, :, :rows], src[j, :, :, :, :rows])
         assert not got[j, :, :, :, rows:].any()
+
+
+@pytest.mark.parametrize("n", [1, 4, 1001, 40 * 2000 + 3])
+def test_plan_upload_through_sm_loads_is_exact(n):
+    """asv_plan_upload pulls a plan from mapped pinned memory with SM loads (no copy engine)."""
+    from paper_2605_23389_b200 import _lib
+    h = _lib.lib()
+    src = torch.from_numpy(np.random.default_rng(n).integers(-2**31, 2**31 - 1, n + 3, dtype=np.int64)
+                           .astype(np.int32)).pin_memory()
+    dst = torch.full((n + 3,), -7, dtype=torch.int32, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.check(h.asv_plan_upload(src.data_ptr(), dst.data_ptr(), n, st))
+    torch.cuda.synchronize()
+    assert torch.equal(dst[:n].cpu(), src[:n])
