@@ -220,6 +220,9 @@ class GpuExecutor : public prefixsim::EngineObserver {
         ASV_CUDA(cudaStreamCreateWithFlags(&p2p_, cudaStreamNonBlocking));
         ASV_CUDA(cudaSetDevice(xfer_device()));
         ASV_CUDA(cudaStreamCreateWithFlags(&xfer_, cudaStreamNonBlocking));
+        ASV_CUDA(cudaStreamCreateWithFlags(&xfer2_, cudaStreamNonBlocking));
+        ASV_CUDA(cudaStreamCreateWithFlags(&xfer3_, cudaStreamNonBlocking));
+        if (const char* nb = std::getenv("ASV_BULK_STREAMS")) n_bulk_ = std::max(1, std::min(3, std::atoi(nb)));
         ASV_CUDA(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));  // other PCIe direction
         ASV_CUDA(cudaStreamCreateWithFlags(&urgent_, cudaStreamNonBlocking));  // strays / swap-ins
         ASV_CUDA(cudaSetDevice(o.decode_device));
@@ -258,7 +261,6 @@ class GpuExecutor : public prefixsim::EngineObserver {
         ASV_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&plan_arena_host_), static_cast<size_t>(arena_words_) * 4,
                                cudaHostAllocMapped));  // pulled by SM loads (asv_plan_upload)
         ASV_CUDA(cudaMalloc(&plan_arena_dev_, static_cast<size_t>(arena_words_) * 4));
-        it_end_.resize(static_cast<size_t>(ring_));
         att_beg_.resize(static_cast<size_t>(ring_));
         att_end_.resize(static_cast<size_t>(ring_));
         slot_timed_.assign(static_cast<size_t>(ring_), 0);
@@ -270,7 +272,6 @@ class GpuExecutor : public prefixsim::EngineObserver {
         ASV_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ts_arena_),
                                static_cast<size_t>(ring_) * static_cast<size_t>(workers_) * 16, cudaHostAllocMapped));
         for (int i = 0; i < ring_; ++i) {
-            ASV_CUDA(cudaEventCreateWithFlags(&it_end_[static_cast<size_t>(i)], cudaEventDisableTiming));
             ASV_CUDA(cudaEventCreate(&att_beg_[static_cast<size_t>(i)]));
             ASV_CUDA(cudaEventCreate(&att_end_[static_cast<size_t>(i)]));
         }
@@ -285,15 +286,16 @@ class GpuExecutor : public prefixsim::EngineObserver {
         std::memset(stats_.logical_count, 0, sizeof(stats_.logical_count));
         if (o.execute_transfers) warm_up_copies();
         worker_.start();
+        launcher_.start();
         if (std::getenv("ASV_WATCHDOG") != nullptr) {
             watchdog_ = std::thread([this] {
                 while (!watchdog_stop_.load()) {
                     std::this_thread::sleep_for(std::chrono::seconds(5));
                     std::fprintf(stderr,
-                                 "[asv watchdog] executed=%lld phase=%d worker done=%llu queued=%zu in=%s | flags iter=%u "
+                                 "[asv watchdog] executed=%lld phase=%d worker done=%llu queued=%zu in=%s launcher queued=%zu | flags iter=%u "
                                  "bulk=%u/%u urgent=%u/%u d2h=%u/%u p2p=%u/%u\n",
                                  static_cast<long long>(executed_), phase_.load(),
-                                 static_cast<unsigned long long>(worker_.done()), worker_.queued(), worker_.current(),
+                                 static_cast<unsigned long long>(worker_.done()), worker_.queued(), worker_.current(), launcher_.queued(),
                                  flags_.value(kIter),
                                  flags_.value(kBulk), lane_seq_[kBulk], flags_.value(kUrgent), lane_seq_[kUrgent],
                                  flags_.value(kD2H), lane_seq_[kD2H], flags_.value(kP2P), lane_seq_[kP2P]);
@@ -307,8 +309,10 @@ class GpuExecutor : public prefixsim::EngineObserver {
         if (watchdog_.joinable()) watchdog_.join();
         // error paths: drop queued copies and release every stream wait on a
         // lane flag that will now never be written, so the device can drain
+        launcher_.stop(true);
         worker_.stop(true);
-        for (int l = kBulk; l <= kP2P; ++l) flags_.force(l, lane_seq_[l]);
+        for (int l = kBulk; l < kLanes; ++l) flags_.force(l, lane_seq_[l]);
+        flags_.force(kIter, static_cast<uint32_t>(executed_));
         cudaSetDevice(o_.decode_device);
         cudaDeviceSynchronize();
         if (pair_) {
@@ -318,7 +322,6 @@ class GpuExecutor : public prefixsim::EngineObserver {
         }
         if (plan_arena_host_) cudaFreeHost(plan_arena_host_);
         if (plan_arena_dev_) cudaFree(plan_arena_dev_);
-        for (auto e : it_end_) cudaEventDestroy(e);
         for (auto e : att_beg_) cudaEventDestroy(e);
         for (auto e : att_end_) cudaEventDestroy(e);
         if (ts_arena_) cudaFreeHost(ts_arena_);
@@ -337,6 +340,8 @@ class GpuExecutor : public prefixsim::EngineObserver {
         cudaStreamDestroy(compute_);
         cudaStreamDestroy(p2p_);
         cudaStreamDestroy(xfer_);
+        cudaStreamDestroy(xfer2_);
+        cudaStreamDestroy(xfer3_);
         cudaStreamDestroy(d2h_);
         cudaStreamDestroy(urgent_);
     }
@@ -468,53 +473,58 @@ class GpuExecutor : public prefixsim::EngineObserver {
             throw std::runtime_error(asv_last_error());
         }
         if (plan.total_splits > ws_splits_) throw std::runtime_error("attention workspace too small");
-        ASV_CUDA(cudaSetDevice(o_.decode_device));
-        if (timed && !window_open_) {
-            ASV_CUDA(cudaEventRecord(win_beg_, compute_));
-            window_open_ = true;
-        }
         if (worker_.failed()) throw CudaError("copy worker: " + worker_.error());
+        if (launcher_.failed()) throw CudaError("launch worker: " + launcher_.error());
         // admitted requests whose KV is still in flight: the iteration waits for it
-        int64_t ready_waits = 0;
+        std::vector<std::pair<int, uint32_t>> waits;
         for (const auto& m : running) {
             ReqKV& r = kv(m.id);
             if (r.ready_slot >= 0) {
-                if (!flags_.reached(r.ready_slot, r.ready_v)) {
-                    flags_.wait(compute_, r.ready_slot, r.ready_v);
-                    ++ready_waits;
-                }
+                if (!flags_.reached(r.ready_slot, r.ready_v)) waits.emplace_back(r.ready_slot, r.ready_v);
                 r.ready_slot = -1;
             }
         }
+        const int64_t ready_waits = static_cast<int64_t>(waits.size());
         const int64_t pw = plan_region(e, (static_cast<int64_t>(plan.total_int32) + 3) & ~int64_t(3));
         std::memcpy(plan_arena_host_ + pw, plan_scratch_.data(), static_cast<size_t>(plan.total_int32) * 4);
-        if (asv_plan_upload(plan_arena_host_ + pw, plan_arena_dev_ + pw, plan.total_int32, compute_) != ASV_OK)
-            throw CudaError(asv_last_error());
-        ASV_CUDA(cudaEventRecord(att_beg_[slot], compute_));
-        asv_attn_args args{};
-        args.q = q_;
-        args.kv_pool = dec_.base();
-        args.pool_pages = dec_.size();
-        args.plan_dev = plan_arena_dev_ + pw;
-        args.plan = &plan;
-        args.k_new = k_new_;
-        args.v_new = v_new_;
-        args.out = out_;
-        args.lse = nullptr;
-        args.workspace = ws_;
-        args.workspace_bytes = ws_bytes_;
-        args.sm_scale = 0.08838834764831845f;
-        args.pdl = o_.pdl;
-        for (int l = 0; l < o_.num_layers; ++l) {
-            args.layer = l;
-            args.launch_index = launches_++;
-            args.warp_timestamps = (timed && l == 0) ? ts_slot(slot) : nullptr;
-            args.pdl = l == 0 ? 0 : o_.pdl;  // layer 0 reads the plan the upload kernel just wrote
-            if (asv_decode_attention(&shape_, &args, compute_) != ASV_OK) throw CudaError(asv_last_error());
-        }
-        ASV_CUDA(cudaEventRecord(att_end_[slot], compute_));
-        ASV_CUDA(cudaEventRecord(it_end_[slot], compute_));
-        flags_.write(compute_, kIter, static_cast<uint32_t>(e + 1));  // executed iterations complete
+        const bool open_window = timed && !window_open_;
+        window_open_ = window_open_ || timed;
+        const uint32_t launch0 = launches_;
+        launches_ += static_cast<uint32_t>(o_.num_layers);
+        uint64_t* ts = timed ? ts_slot(slot) : nullptr;
+        // The launch worker enqueues the iteration (so a full compute queue never
+        // stalls the decisions that issue future KV moves)
+        launcher_.post([this, e, slot, pw, plan, waits = std::move(waits), open_window, launch0, ts] {
+            ASV_CUDA(cudaSetDevice(o_.decode_device));
+            if (open_window) ASV_CUDA(cudaEventRecord(win_beg_, compute_));
+            for (const auto& [lane, v] : waits) flags_.wait(compute_, lane, v);
+            if (asv_plan_upload(plan_arena_host_ + pw, plan_arena_dev_ + pw, plan.total_int32, compute_) != ASV_OK)
+                throw CudaError(asv_last_error());
+            ASV_CUDA(cudaEventRecord(att_beg_[slot], compute_));
+            asv_attn_plan pl = plan;
+            asv_attn_args args{};
+            args.q = q_;
+            args.kv_pool = dec_.base();
+            args.pool_pages = dec_.size();
+            args.plan_dev = plan_arena_dev_ + pw;
+            args.plan = &pl;
+            args.k_new = k_new_;
+            args.v_new = v_new_;
+            args.out = out_;
+            args.lse = nullptr;
+            args.workspace = ws_;
+            args.workspace_bytes = ws_bytes_;
+            args.sm_scale = 0.08838834764831845f;
+            for (int l = 0; l < o_.num_layers; ++l) {
+                args.layer = l;
+                args.launch_index = launch0 + static_cast<uint32_t>(l);
+                args.warp_timestamps = l == 0 ? ts : nullptr;
+                args.pdl = l == 0 ? 0 : o_.pdl;  // layer 0 reads the plan the upload kernel just wrote
+                if (asv_decode_attention(&shape_, &args, compute_) != ASV_OK) throw CudaError(asv_last_error());
+            }
+            ASV_CUDA(cudaEventRecord(att_end_[slot], compute_));
+            flags_.write(compute_, kIter, static_cast<uint32_t>(e + 1));  // executed iterations complete
+        }, "iteration");
         slot_timed_[slot] = timed ? 1 : 0;
         if (tracing_) {
             slot_seq_[slot] = seq;
@@ -543,14 +553,23 @@ class GpuExecutor : public prefixsim::EngineObserver {
 
     void finish(const prefixsim::MetricsLog& log, asv_engine_stats* out) {
         phase_.store(3);
+        if (window_open_) {
+            launcher_.post([this] {
+                ASV_CUDA(cudaSetDevice(o_.decode_device));
+                ASV_CUDA(cudaEventRecord(win_end_, compute_));
+            }, "window_end");
+        }
+        launcher_.drain();
         worker_.drain();
         phase_.store(4);
         if (worker_.failed()) throw CudaError("copy worker: " + worker_.error());
+        if (launcher_.failed()) throw CudaError("launch worker: " + launcher_.error());
         ASV_CUDA(cudaSetDevice(o_.decode_device));
-        if (window_open_) ASV_CUDA(cudaEventRecord(win_end_, compute_));
         ASV_CUDA(cudaStreamSynchronize(compute_));
         ASV_CUDA(cudaSetDevice(xfer_device()));
         ASV_CUDA(cudaStreamSynchronize(xfer_));
+        ASV_CUDA(cudaStreamSynchronize(xfer2_));
+        ASV_CUDA(cudaStreamSynchronize(xfer3_));
         ASV_CUDA(cudaStreamSynchronize(d2h_));
         ASV_CUDA(cudaStreamSynchronize(urgent_));
         ASV_CUDA(cudaSetDevice(o_.decode_device));
@@ -682,9 +701,22 @@ class GpuExecutor : public prefixsim::EngineObserver {
     // urgent_ so they never queue behind a whole batch, D2H on d2h_ (both PCIe
     // directions at once), admits/evicts of a pair on p2p_.  Every operation on
     // those streams is posted to the copy worker thread.
-    enum Lane { kIter = 0, kBulk = 1, kUrgent = 2, kD2H = 3, kP2P = 4, kLanes = 5 };
+    // A batch prefetch is spread over n_bulk_ streams (one request each, round
+    // robin): concurrent H2D streams keep more PCIe reads in flight.
+    enum Lane { kIter = 0, kBulk = 1, kUrgent = 2, kD2H = 3, kP2P = 4, kBulk2 = 5, kBulk3 = 6, kLanes = 7 };
     cudaStream_t lane_stream(int lane) const {
-        return lane == kD2H ? d2h_ : lane == kUrgent ? urgent_ : lane == kP2P ? p2p_ : xfer_;
+        switch (lane) {
+            case kD2H: return d2h_;
+            case kUrgent: return urgent_;
+            case kP2P: return p2p_;
+            case kBulk2: return xfer2_;
+            case kBulk3: return xfer3_;
+            default: return xfer_;
+        }
+    }
+    int bulk_lane(int64_t i) const {
+        static constexpr int kBulkLanes[3] = {kBulk, kBulk2, kBulk3};
+        return kBulkLanes[i % n_bulk_];
     }
     int lane_device(int lane) const { return lane == kP2P ? o_.decode_device : xfer_device(); }
 
@@ -728,12 +760,14 @@ class GpuExecutor : public prefixsim::EngineObserver {
         }, "signal");
         return v;
     }
+    // timer of `lane` inside the open group: started at the lane's first copy
     void timer_begin(int lane, bool p2p) {
         CopyTimer t{};
         t.p2p = p2p;
         t.lane = lane == kD2H ? 'd' : lane == kUrgent ? 'u' : lane == kP2P ? 'p' : 'b';
         t.seq = cur_seq_;
-        t.bytes = -(stats_.h2d_bytes + stats_.d2h_bytes + stats_.p2p_bytes);
+        t.bytes = 0;
+        open_timer_[lane] = static_cast<int64_t>(copy_timers_.size());
         const cudaStream_t st = lane_stream(lane);
         const int dev = lane_device(lane);
         // events are created here (not on the worker) and recorded there
@@ -748,9 +782,13 @@ class GpuExecutor : public prefixsim::EngineObserver {
             ASV_CUDA(cudaEventRecord(ev, st));
         }, "timer_a");
     }
+    void timer_add(int lane, int64_t bytes) {
+        if (open_timer_[lane] >= 0) copy_timers_[static_cast<size_t>(open_timer_[lane])].bytes += bytes;
+    }
     void timer_end(int lane) {
-        CopyTimer& t = copy_timers_.back();
-        t.bytes += stats_.h2d_bytes + stats_.d2h_bytes + stats_.p2p_bytes;
+        if (open_timer_[lane] < 0) return;
+        CopyTimer& t = copy_timers_[static_cast<size_t>(open_timer_[lane])];
+        open_timer_[lane] = -1;
         const cudaStream_t st = lane_stream(lane);
         const int dev = lane_device(lane);
         const cudaEvent_t ev = t.b;
@@ -761,17 +799,22 @@ class GpuExecutor : public prefixsim::EngineObserver {
     }
 
     void begin_xfer_group(int lane = kBulk) {
-        lane_ = lane;
+        group_lane_ = lane_ = lane;
         group_timed_ = copies_active() && in_window();
         if (!copies_active()) return;
         // D2H reads pages the last launched iteration may still use; H2D lanes
         // only wait for the hazards of the pages they allocate (fetch_from_host)
         if (lane == kD2H) lane_wait_iteration(kD2H, executed_ - 1);
-        if (group_timed_) timer_begin(lane, false);
+    }
+    // lane of the next copy of the open group (bulk groups rotate over the bulk streams)
+    void next_copy_lane() {
+        lane_ = group_lane_ == kBulk ? bulk_lane(bulk_rr_++) : group_lane_;
+        if (group_timed_ && open_timer_[lane_] < 0) timer_begin(lane_, false);
     }
     void end_xfer_group() {
         if (!copies_active()) return;
-        if (group_timed_) timer_end(lane_);
+        for (int l = 0; l < kLanes; ++l) timer_end(l);
+        lane_ = group_lane_;
         if (!group_quarantine_.empty()) {
             const uint32_t v = lane_signal(lane_);
             for (auto& q : group_quarantine_) q.first->release_after(lane_, v, std::move(q.second));
@@ -821,8 +864,10 @@ class GpuExecutor : public prefixsim::EngineObserver {
         for (int64_t j = 0; j < n; ++j) r.pages.push_back(pool->alloc(&hz));
         r.where = pool == &dec_ ? ReqKV::kDecode : ReqKV::kPrefetch;
         if (!copies_active()) return;
+        next_copy_lane();
         lane_wait_iteration(lane_, hz);
         const int64_t moved = post_copy_kv(r.pages, *pool, id, q.prefix_len, true);
+        timer_add(lane_, moved);
         stats_.h2d_bytes += moved;
         if (group_timed_) stats_.h2d_bytes_window += moved;
         r.ready_slot = lane_;  // this request is usable as soon as its own pages land
@@ -834,8 +879,10 @@ class GpuExecutor : public prefixsim::EngineObserver {
         const prefixsim::Request& q = (*requests_)[static_cast<std::size_t>(id)];
         PagePool* pool = r.where == ReqKV::kPrefetch ? &pre_ : &dec_;
         if (copies_active() && !r.pages.empty()) {
+            next_copy_lane();
             lane_wait_ready(lane_, r);
             const int64_t moved = post_copy_kv(r.pages, *pool, id, q.prefix_len, false);
+            timer_add(lane_, moved);
             stats_.d2h_bytes += moved;
             if (group_timed_) stats_.d2h_bytes_window += moved;
             group_quarantine_.push_back({pool, std::move(r.pages)});
@@ -868,6 +915,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
             stats_.p2p_bytes += moved;
             if (timed) {
                 stats_.p2p_bytes_window += moved;
+                timer_add(kP2P, moved);
                 timer_end(kP2P);
             }
             const uint32_t v = lane_signal(kP2P);
@@ -969,7 +1017,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
 
     // retire every executed iteration up to and including `e`, in order
     void retire_through(int64_t e) {
-        for (; retired_upto_ <= e; ++retired_upto_) retire(static_cast<size_t>(retired_upto_ % ring_));
+        for (; retired_upto_ <= e; ++retired_upto_) retire(retired_upto_);
         while (!live_plans_.empty() && live_plans_.front().first < retired_upto_) live_plans_.pop_front();
     }
 
@@ -993,10 +1041,16 @@ class GpuExecutor : public prefixsim::EngineObserver {
         return begin % arena_words_;
     }
 
-    void retire(size_t slot) {
-        const auto t0 = clock_now();
-        ASV_CUDA(cudaEventSynchronize(it_end_[slot]));
-        host_wait_ms_ += ms_since(t0);
+    void retire(int64_t e) {
+        const size_t slot = static_cast<size_t>(e % ring_);
+        if (!flags_.reached(kIter, static_cast<uint32_t>(e + 1))) {
+            const auto t0 = clock_now();
+            while (!flags_.reached(kIter, static_cast<uint32_t>(e + 1))) {
+                if (launcher_.failed()) throw CudaError("launch worker: " + launcher_.error());
+                std::this_thread::sleep_for(std::chrono::microseconds(20));
+            }
+            host_wait_ms_ += ms_since(t0);
+        }
         if (slot_timed_[slot]) {
             float ms = 0.f;
             ASV_CUDA(cudaEventElapsedTime(&ms, att_beg_[slot], att_end_[slot]));
@@ -1011,7 +1065,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
             }
             slot_timed_[slot] = 0;
             // measured bubble of the layer-0 launch: idle warp time inside its span
-            std::memcpy(ts_host_.data(), ts_slot(slot), ts_host_.size() * 8);  // mapped, complete at it_end_
+            std::memcpy(ts_host_.data(), ts_slot(slot), ts_host_.size() * 8);  // mapped, complete once kIter passed
             uint64_t lo = UINT64_MAX, hi = 0;
             double busy = 0.0;
             for (int32_t w = 0; w < workers_; ++w) {
@@ -1049,9 +1103,15 @@ class GpuExecutor : public prefixsim::EngineObserver {
     bool pair_ = false;
     int64_t dec_pages_ = 0, pre_pages_ = 0;
     PagePool dec_, pre_;
-    cudaStream_t compute_ = nullptr, p2p_ = nullptr, xfer_ = nullptr, d2h_ = nullptr, urgent_ = nullptr;
+    cudaStream_t compute_ = nullptr, p2p_ = nullptr, xfer_ = nullptr, xfer2_ = nullptr, xfer3_ = nullptr,
+                 d2h_ = nullptr, urgent_ = nullptr;
+    int n_bulk_ = 2;                        // bulk H2D streams (ASV_BULK_STREAMS=1..3)
+    int64_t bulk_rr_ = 0;
+    int group_lane_ = 1;                    // lane the open group was begun on
+    int64_t open_timer_[7] = {-1, -1, -1, -1, -1, -1, -1};  // per lane: timer of the open group
     SeqFlags flags_;
-    CopyWorker worker_;
+    CopyWorker worker_;                     // issues every copy-stream operation
+    CopyWorker launcher_;                   // issues every compute-stream operation (iterations)
     std::thread watchdog_;                  // ASV_WATCHDOG=1: progress report every 5 s (debugging)
     std::atomic<bool> watchdog_stop_{false};
     std::atomic<int> phase_{0};             // 1 decide/copy, 2 iteration launch, 3 finish
@@ -1073,7 +1133,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
     std::deque<std::pair<int64_t, int64_t>> live_plans_;  // (executed index, absolute begin) in issue order
     int64_t retired_upto_ = 0;                   // every executed iteration below this is retired
     uint64_t* ts_arena_ = nullptr;
-    std::vector<cudaEvent_t> it_end_, att_beg_, att_end_;
+    std::vector<cudaEvent_t> att_beg_, att_end_;
     std::vector<int> slot_timed_;
     cudaEvent_t win_beg_ = nullptr, win_end_ = nullptr;
     bool window_open_ = false, last_timed_end_ = false, group_timed_ = false, admit_moved_ = false;
