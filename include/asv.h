@@ -263,6 +263,8 @@ typedef struct asv_engine_stats {
                                      window: time the host link had work (single device only, else 0) */
     double host_wait_ms;          /* host time blocked on the GPU (run-ahead ring, page reclaim) */
     int64_t hazard_waits;         /* copy-stream waits on a page's last iteration (page reuse) */
+    int64_t result_d2h_bytes_window; /* e2e: each iteration's attention output [b][n_h][128] bf16 read back
+                                        to pinned host memory (SM stores, no copy-engine queue) */
 } asv_engine_stats;
 
 int asv_engine_run(const char* config_json, const char* policy_override, const asv_engine_opts* opts,

@@ -118,6 +118,7 @@ class EngineStats(C.Structure):
         ("pcie_union_ms", C.c_double),
         ("host_wait_ms", C.c_double),
         ("hazard_waits", C.c_int64),
+        ("result_d2h_bytes_window", C.c_int64),
     ]
 
     def as_dict(self):

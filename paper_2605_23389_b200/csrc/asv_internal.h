@@ -72,7 +72,8 @@ struct AttnLaunch {
 int attn_warps_per_cta(int group);
 cudaError_t attn_occupancy(int group, int* blocks_per_sm);
 cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st);
-cudaError_t plan_upload(const int32_t* host_plan, int32_t* plan_dev, int64_t n_int32, cudaStream_t st);
+// n_int32 rounded up to a multiple of 4 (16-byte units); both pointers 16-byte aligned
+cudaError_t sm_copy(const int32_t* src, int32_t* dst, int64_t n_int32, cudaStream_t st);
 
 // thread-local last error (asv_last_error)
 void set_error(const std::string& msg);

@@ -265,7 +265,7 @@ int asv_plan_upload(const int32_t* host_plan, int32_t* plan_dev, int64_t n_int32
     if (host_plan == nullptr || plan_dev == nullptr || n_int32 < 0) return fail(ASV_ERR_INVALID, "bad plan upload");
     if ((reinterpret_cast<uintptr_t>(host_plan) | reinterpret_cast<uintptr_t>(plan_dev)) & 15u)
         return fail(ASV_ERR_INVALID, "plan buffers must be 16-byte aligned");
-    cudaError_t e = plan_upload(host_plan, plan_dev, n_int32, static_cast<cudaStream_t>(stream));
+    cudaError_t e = sm_copy(host_plan, plan_dev, n_int32, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "plan upload");
     return ASV_OK;
 }

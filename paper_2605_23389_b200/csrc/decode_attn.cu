@@ -889,7 +889,7 @@ int attn_warps_per_cta(int group) {
     return variant_available(group, v) ? v.nw : 4;
 }
 
-__global__ void plan_fetch_kernel(const int4* __restrict__ src, int4* __restrict__ dst, int64_t n16);
+__global__ void sm_copy_kernel(const int4* __restrict__ src, int4* __restrict__ dst, int64_t n16);
 
 cudaError_t attn_occupancy(int group, int* blocks_per_sm) {
     cudaError_t e = dispatch(group, true, blocks_per_sm, nullptr, 0, false, nullptr);
@@ -900,7 +900,7 @@ cudaError_t attn_occupancy(int group, int* blocks_per_sm) {
     cudaFuncAttributes fa;
     e = cudaFuncGetAttributes(&fa, merge_splits_kernel);
     if (e != cudaSuccess) return e;
-    return cudaFuncGetAttributes(&fa, plan_fetch_kernel);
+    return cudaFuncGetAttributes(&fa, sm_copy_kernel);
 }
 
 cudaError_t merge_launch(const Params& p, const int32_t* merge_reqs, int32_t n_merge, int sms, bool pdl,
@@ -921,17 +921,19 @@ cudaError_t merge_launch(const Params& p, const int32_t* merge_reqs, int32_t n_m
     return cudaLaunchKernelEx(&cfg, merge_splits_kernel, p, merge_reqs, rows);
 }
 
-// Plan upload through SM loads of mapped pinned host memory (asv_plan_upload):
-// 16-byte loads, grid-strided, all in flight at once (one PCIe round trip for a
-// typical 10-100 KB plan).  Keeps the compute stream off the copy-engine queue.
-__global__ void plan_fetch_kernel(const int4* __restrict__ src, int4* __restrict__ dst, int64_t n16) {
+// 16-byte SM copy between any two device-accessible buffers, used where a
+// small transfer must not queue behind multi-GB copy-engine work: the plan
+// upload from mapped pinned host memory (asv_plan_upload) and the e2e result
+// read-back into mapped pinned host memory.  Grid-strided, all loads in flight
+// at once (one PCIe round trip for a typical 10-100 KB buffer).
+__global__ void sm_copy_kernel(const int4* __restrict__ src, int4* __restrict__ dst, int64_t n16) {
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n16;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         dst[i] = src[i];
     }
 }
 
-cudaError_t plan_upload(const int32_t* host_plan, int32_t* plan_dev, int64_t n_int32, cudaStream_t st) {
+cudaError_t sm_copy(const int32_t* src, int32_t* dst, int64_t n_int32, cudaStream_t st) {
     const int64_t n16 = (n_int32 + 3) / 4;
     if (n16 <= 0) return cudaSuccess;
     int dev = 0, sms = 148;
@@ -940,8 +942,8 @@ cudaError_t plan_upload(const int32_t* host_plan, int32_t* plan_dev, int64_t n_i
     const int threads = 256;
     int64_t blocks = (n16 + threads - 1) / threads;
     if (blocks > sms) blocks = sms;
-    plan_fetch_kernel<<<static_cast<unsigned>(blocks), threads, 0, st>>>(reinterpret_cast<const int4*>(host_plan),
-                                                                         reinterpret_cast<int4*>(plan_dev), n16);
+    sm_copy_kernel<<<static_cast<unsigned>(blocks), threads, 0, st>>>(reinterpret_cast<const int4*>(src),
+                                                                      reinterpret_cast<int4*>(dst), n16);
     return cudaGetLastError();
 }
 

@@ -243,6 +243,10 @@ class GpuExecutor : public prefixsim::EngineObserver {
         const int64_t kvbytes = max_rows_ * o.num_kv_heads * 256;
         ASV_CUDA(cudaMalloc(&q_, static_cast<size_t>(qbytes)));
         ASV_CUDA(cudaMalloc(&out_, static_cast<size_t>(qbytes)));
+        if (o.execute_transfers) {  // e2e: every iteration's result lands in host memory
+            ASV_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&result_host_), static_cast<size_t>(qbytes),
+                                   cudaHostAllocMapped));
+        }
         ASV_CUDA(cudaMalloc(&k_new_, static_cast<size_t>(kvbytes)));
         ASV_CUDA(cudaMalloc(&v_new_, static_cast<size_t>(kvbytes)));
         fill_random(q_, qbytes / 2, 11);
@@ -333,6 +337,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
         cudaEventDestroy(win_end_);
         cudaFree(q_);
         cudaFree(out_);
+        if (result_host_) cudaFreeHost(result_host_);
         cudaFree(k_new_);
         cudaFree(v_new_);
         cudaFree(ws_);
@@ -492,9 +497,10 @@ class GpuExecutor : public prefixsim::EngineObserver {
         const uint32_t launch0 = launches_;
         launches_ += static_cast<uint32_t>(o_.num_layers);
         uint64_t* ts = timed ? ts_slot(slot) : nullptr;
+        const int64_t result_bytes = result_host_ ? static_cast<int64_t>(running.size()) * o_.num_q_heads * 256 : 0;
         // The launch worker enqueues the iteration (so a full compute queue never
         // stalls the decisions that issue future KV moves)
-        launcher_.post([this, e, slot, pw, plan, waits = std::move(waits), open_window, launch0, ts] {
+        launcher_.post([this, e, slot, pw, plan, waits = std::move(waits), open_window, launch0, ts, result_bytes] {
             ASV_CUDA(cudaSetDevice(o_.decode_device));
             if (open_window) ASV_CUDA(cudaEventRecord(win_beg_, compute_));
             for (const auto& [lane, v] : waits) flags_.wait(compute_, lane, v);
@@ -523,6 +529,10 @@ class GpuExecutor : public prefixsim::EngineObserver {
                 if (asv_decode_attention(&shape_, &args, compute_) != ASV_OK) throw CudaError(asv_last_error());
             }
             ASV_CUDA(cudaEventRecord(att_end_[slot], compute_));
+            if (result_bytes > 0) {  // the step's result (last layer's output) read back to the host
+                ASV_CUDA(sm_copy(static_cast<const int32_t*>(out_), reinterpret_cast<int32_t*>(result_host_),
+                                     result_bytes / 4, compute_));
+            }
             flags_.write(compute_, kIter, static_cast<uint32_t>(e + 1));  // executed iterations complete
         }, "iteration");
         slot_timed_[slot] = timed ? 1 : 0;
@@ -535,7 +545,8 @@ class GpuExecutor : public prefixsim::EngineObserver {
             ++stats_.iterations_timed;
             stats_.tokens_timed += static_cast<int64_t>(running.size());
             stats_.attn_launches += o_.num_layers;
-            stats_.kernel_launches_timed += o_.num_layers * (plan.n_merge > 0 ? 2 : 1);
+            // attention (+ merge) per layer, the plan upload, and the e2e result read-back
+            stats_.kernel_launches_timed += o_.num_layers * (plan.n_merge > 0 ? 2 : 1) + 1 + (result_bytes > 0 ? 1 : 0);
             if (first_timed_start_ < 0) first_timed_start_ = rec.start_ms;
             last_timed_end_ms_ = rec.end_ms;
             stats_.bubble_ms_timed += rec.bubble_ms;
@@ -546,6 +557,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
                                                   b * 2 * o_.num_kv_heads * 256) +
                                  static_cast<int64_t>(plan.total_int32) * 4;
             last_timed_end_ = true;
+            stats_.result_d2h_bytes_window += result_bytes;
         }
         host_ms_ += ms_since(t0);
         if (exec) host_iter_ms_ += ms_since(t0);
@@ -1122,6 +1134,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
     int64_t arena_pages_ = 1;
     int32_t workers_ = 0;
     int64_t max_rows_ = 0;
+    char* result_host_ = nullptr;           // mapped pinned: per-iteration result read-back (e2e)
     void *q_ = nullptr, *out_ = nullptr, *k_new_ = nullptr, *v_new_ = nullptr, *ws_ = nullptr;
     size_t ws_bytes_ = 0;
     int32_t ws_splits_ = 0;
