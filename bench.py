@@ -70,12 +70,15 @@ class Dist:
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        # testing only: several ranks on one GPU (ASV_BENCH_DEVICE=0 ASV_BENCH_BACKEND=gloo)
+        if os.environ.get("ASV_BENCH_DEVICE"):
+            self.local = int(os.environ["ASV_BENCH_DEVICE"])
         self.pg = None
         if self.world > 1:
             import torch
             import torch.distributed as dist
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            backend = os.environ.get("ASV_BENCH_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
             if backend == "nccl":
                 torch.cuda.set_device(self.local)
             dist.init_process_group(backend)
@@ -236,6 +239,9 @@ def main():
 
     cfg = E.load_config(args.config)
     cfg["_path"] = args.config
+    global WORKLOAD_NAME
+    if os.path.abspath(args.config) != os.path.abspath(WORKLOAD):
+        WORKLOAD_NAME = f"{os.path.basename(args.config)} (not the headline workload)"
     attn = cfg["b200"]
     S, W, K = STEADY_START, args.warmup, args.steps
 
@@ -335,7 +341,8 @@ def main():
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": d.world, "steps": K,
             "warmup": W, "ms_per_step": win / max(1, res["iterations_timed"]), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic: deterministic splitmix64 trace configs/traces/c2_1024x1k-16k.jsonl, random bf16 KV/q",
+            "data": (f"synthetic: deterministic splitmix64 trace {cfg.get('workload', {}).get('path', '?')}, "
+                     "random bf16 KV/q"),
             "config": {"workload": WORKLOAD_NAME, "global_batch": tok / max(1, res["iterations_timed"]),
                        "seq_len": "1K-16K (+ up to 68 generated)", "parallelism": f"dp{d.world}",
                        "steady_start_iteration": S,
