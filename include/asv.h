@@ -194,6 +194,45 @@ int asv_run_config_jsonl_shard(const char* config_json, const char* policy_overr
                                int32_t shard_count, char** out, int64_t* out_len);
 
 /* ------------------------------------------------------------------------ */
+/* Decode-step linear layers on tcgen05 (the GEMM half of */
+/* a decode iteration, priced by the reference as the MLP term of             */
+/* iteration_latency, cost_model.hpp:60-63, 130-131).                         */
+/*   y[b][n] = epilogue( sum_k x[b][k] * w[n][k] ),  b < batch <= 256         */
+/* bf16 in/out, fp32 accumulate (TMEM).  Weights are the MMA M dimension      */
+/* (swap-AB: decode batches are far below the 128-row MMA tile).              */
+/* ------------------------------------------------------------------------ */
+#define ASV_EPI_STORE 0      /* y[b][n] = acc */
+#define ASV_EPI_RESIDUAL 1   /* y[b][n] += acc (residual stream updated in place) */
+#define ASV_EPI_SILU_MUL 2   /* w rows of tile t: [0,64) gate, [64,128) up of outputs 64t..64t+63;
+                                y[b][64t + j] = silu(gate) * up */
+#define ASV_EPI_QKV_ROPE 3   /* w rows: n_q_heads q heads, n_kv_heads k heads, n_kv_heads v heads
+                                (128 rows each); rotate-half RoPE (theta) at positions[b] on q, k */
+typedef struct asv_linear_args {
+    const void* w;           /* [n_out][k] bf16 row-major; n_out % 128 == 0, k % 64 == 0 */
+    int32_t n_out, k;
+    const void* x;           /* [x_rows][k] bf16; x_rows >= batch rounded up to 16 (extra rows: any
+                                finite values, they only feed unused accumulator columns) */
+    int32_t x_rows, batch;
+    void* y;                 /* [batch][y_ld] bf16 (STORE / RESIDUAL / SILU_MUL) */
+    int32_t y_ld;
+    int32_t epilogue;        /* ASV_EPI_* */
+    const int32_t* positions;/* QKV_ROPE: [batch] token positions (= prefix_len) */
+    float rope_theta;        /* QKV_ROPE: 10000 for Llama-2 */
+    void* q;                 /* QKV_ROPE: [batch][n_q_heads][128] */
+    void* k_out;             /* QKV_ROPE: [batch][n_kv_heads][128] */
+    void* v_out;             /* QKV_ROPE: [batch][n_kv_heads][128] */
+    int32_t n_q_heads, n_kv_heads;
+    void* workspace;         /* asv_linear_workspace_bytes(), zero-filled once before first use */
+    size_t workspace_bytes;
+} asv_linear_args;
+
+size_t asv_linear_workspace_bytes(int32_t n_out, int32_t k, int32_t max_batch, int device);
+int asv_linear(const asv_linear_args* args, void* stream);
+/* out[b][:] = h[b][:] * rsqrt(mean(h[b]^2) + eps) * gamma; rows [batch, rows_out) of out zeroed */
+int asv_rmsnorm(const void* h, const void* gamma, void* out, int32_t dim, int32_t batch, int32_t rows_out,
+                float eps, void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* Decode engine on the GPU: the reference engine's decisions (virtual clock, */
 /* bit-exact) executed for real — KV moves as copies, every iteration as      */
 /* page-table build + L decode-attention launches — with measured times.      */

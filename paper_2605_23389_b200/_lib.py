@@ -62,6 +62,32 @@ class AttnArgs(C.Structure):
     ]
 
 
+class LinearArgs(C.Structure):
+    _fields_ = [
+        ("w", C.c_void_p),
+        ("n_out", C.c_int32),
+        ("k", C.c_int32),
+        ("x", C.c_void_p),
+        ("x_rows", C.c_int32),
+        ("batch", C.c_int32),
+        ("y", C.c_void_p),
+        ("y_ld", C.c_int32),
+        ("epilogue", C.c_int32),
+        ("positions", C.c_void_p),
+        ("rope_theta", C.c_float),
+        ("q", C.c_void_p),
+        ("k_out", C.c_void_p),
+        ("v_out", C.c_void_p),
+        ("n_q_heads", C.c_int32),
+        ("n_kv_heads", C.c_int32),
+        ("workspace", C.c_void_p),
+        ("workspace_bytes", C.c_size_t),
+    ]
+
+
+EPI_STORE, EPI_RESIDUAL, EPI_SILU_MUL, EPI_QKV_ROPE = 0, 1, 2, 3
+
+
 class EngineOpts(C.Structure):
     _fields_ = [
         ("decode_device", C.c_int32),
@@ -160,6 +186,10 @@ SIGNATURES = [
     ("asv_kv_copy_d2d", C.c_int,
      [C.POINTER(AttnShape), C.c_void_p, C.c_int64, C.c_int32, C.POINTER(C.c_int32), C.c_void_p, C.c_int64,
       C.c_int32, C.POINTER(C.c_int32), C.c_int64, C.c_void_p, C.POINTER(C.c_int64)]),
+    ("asv_linear_workspace_bytes", C.c_size_t, [C.c_int32, C.c_int32, C.c_int32, C.c_int]),
+    ("asv_linear", C.c_int, [C.POINTER(LinearArgs), C.c_void_p]),
+    ("asv_rmsnorm", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_float,
+                              C.c_void_p]),
     ("asv_run_config_jsonl", C.c_int,
      [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
     ("asv_engine_run", C.c_int,

@@ -1,0 +1,557 @@
+// Decode-step linear layers on the 5th-generation tensor cores (tcgen05) — the
+// GEMM half of a decode iteration that the reference prices as the MLP term of
+// iteration_latency (cost_model.hpp:60-63, 130-131).
+//
+// Decode GEMMs have a tiny M (the batch) and are weight-streaming bound, so the
+// kernel swaps A and B: the weight rows are the MMA M dimension (128 per tile)
+// and the batch is the MMA N dimension (padded to a multiple of 16, <= 256):
+//     D[n_out rows][batch] (TMEM, fp32) = W[n_out][K] · X[batch][K]^T
+// One CTA per (128-row tile, K split); warp 0 lane 0 streams W and X tiles with
+// TMA (2-D tensor maps, 128-byte swizzle) into a multi-stage mbarrier ring,
+// warp 1 lane 0 issues tcgen05.mma (kind::f16, bf16 in, fp32 accumulate in
+// TMEM) and frees each stage with tcgen05.commit; all four warps then read the
+// accumulator with tcgen05.ld (warp w owns TMEM lanes 32w..32w+31 = output
+// rows).  K splits of one tile meet in an fp32 workspace; the last arriving CTA
+// runs the fused epilogue:
+//   STORE     y[b][n]  = acc
+//   RESIDUAL  y[b][n] += acc                         (o_proj / down_proj + residual)
+//   SILU_MUL  y[b][j]  = silu(acc_gate) * acc_up       (gate/up rows interleaved per tile)
+//   QKV_ROPE  q/k/v heads with rotary embedding on q and k (one head per tile)
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <mutex>
+
+#include "../../include/asv.h"
+#include "asv_internal.h"
+
+namespace asv {
+namespace {
+
+constexpr int kBM = 128;              // weight rows per tile (MMA M)
+constexpr int kBK = 64;               // K per stage: one 128-byte swizzle row of bf16
+constexpr int kUmmaK = 16;            // K per tcgen05.mma (kind::f16)
+constexpr int kMaxStages = 8;
+constexpr int kSmemBudget = 100 * 1024;  // ring <= ~100 KiB: two CTAs per SM keep more of W in flight
+constexpr int kABytes = kBM * kBK * 2;   // 16 KiB
+// workspace: a fixed counter area (tile arrival counters stay zero between calls
+// whatever the shape) followed by the fp32 split partials
+constexpr int kMaxTiles = 16384;
+constexpr size_t kCounterBytes = kMaxTiles * 4;
+
+struct LinearParams {
+    int32_t n_out, k, batch, bn;     // bn: batch padded to a multiple of 16 (MMA N)
+    int32_t kb_per_split, splits, stages;
+    int32_t epi;
+    __nv_bfloat16* y;
+    int32_t y_ld;
+    float* ws;                       // [tiles][splits][bn][128] fp32 partials
+    int32_t* counters;               // [tiles] arrival counters (self-resetting)
+    // QKV_ROPE
+    const int32_t* positions;        // [batch] position of the new token
+    float rope_log2_theta;           // log2(theta)
+    __nv_bfloat16 *q, *kk, *v;       // [batch][heads][128]
+    int32_t n_q_heads, n_kv_heads;
+};
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t phase) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(phase)
+        : "memory");
+    return ok != 0;
+}
+// bounded wait: a protocol bug traps (kernel error) instead of hanging the GPU
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+    uint32_t n = 0;
+    while (!mbar_try_wait(bar, phase)) {
+        if (++n > (1u << 28)) __trap();
+    }
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                            uint32_t bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// UMMA shared-memory descriptor: K-major operand, 128-byte swizzle, 8-row groups
+// 1024 bytes apart (SBO), Blackwell descriptor version 1.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+    return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (static_cast<uint64_t>(1) << 16) |
+           (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
+           (static_cast<uint64_t>(2) << 61);
+}
+// instruction descriptor: bf16 x bf16 -> f32, A and B K-major, M = 128, N = n
+__host__ __device__ constexpr uint32_t umma_idesc(uint32_t n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((n >> 3) << 17) | ((kBM >> 4) << 24);
+}
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+}
+// 16 consecutive fp32 accumulator columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float silu(float g) { return g / (1.f + __expf(-g)); }
+
+// ------------------------------------------------------------------ kernel
+// smem: [stages][A 16 KiB][B bn*128 B] (1024-aligned) | full[stages] empty[stages] done | tmem base
+template <int EPI>
+__global__ void __launch_bounds__(128, 2)
+    linear_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
+                  const LinearParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int stage_bytes = kABytes + p.bn * 128;
+    const int nst = p.stages;
+    // the epilogue reuses the ring for the [bn][128] fp32 accumulator tile: barriers after both
+    const int ring = nst * stage_bytes > p.bn * 512 ? nst * stage_bytes : p.bn * 512;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kMaxStages + 1);
+    __shared__ int s_last;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tile = blockIdx.x / p.splits, split = blockIdx.x % p.splits;
+    const int kb0 = split * p.kb_per_split;
+    const int kb1 = min(kb0 + p.kb_per_split, p.k / kBK);
+    const uint32_t ncols = p.bn <= 32 ? 32 : p.bn <= 64 ? 64 : p.bn <= 128 ? 128 : 256;
+
+    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + kMaxStages), done = smem_u32(bars + 2 * kMaxStages);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < nst; ++s) {
+            mbar_init(full0 + 8 * s, 1);
+            mbar_init(empty0 + 8 * s, 1);
+        }
+        mbar_init(done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_w)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_x)) : "memory");
+    }
+    if (warp == 1) {  // TMEM accumulator: 128 lanes x ncols fp32
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(ncols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0 && lane == 0) {
+        // ---- TMA producer: W tiles (streamed once: evict-first), X tiles (reused by every tile: evict-last)
+        const uint64_t pw = policy_evict_first(), px = policy_evict_last();
+        int s = 0;
+        uint32_t ph = 0;
+        for (int kb = kb0; kb < kb1; ++kb) {
+            mbar_wait(empty0 + 8 * s, ph ^ 1);
+            const uint32_t a = smem_u32(smem + s * stage_bytes);
+            mbar_expect_tx(full0 + 8 * s, static_cast<uint32_t>(stage_bytes));
+            tma_load_2d(a, &tm_w, kb * kBK, tile * kBM, full0 + 8 * s, pw);
+            tma_load_2d(a + kABytes, &tm_x, kb * kBK, 0, full0 + 8 * s, px);
+            if (++s == nst) {
+                s = 0;
+                ph ^= 1;
+            }
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ---- MMA issuer: one thread drives the tensor core for the whole CTA
+        const uint32_t idesc = umma_idesc(static_cast<uint32_t>(p.bn));
+        int s = 0;
+        uint32_t ph = 0;
+        for (int kb = kb0; kb < kb1; ++kb) {
+            mbar_wait(full0 + 8 * s, ph);
+            tc_fence_after();
+            const uint32_t a = smem_u32(smem + s * stage_bytes);
+            const uint64_t ad = umma_desc_sw128(a), bd = umma_desc_sw128(a + kABytes);
+#pragma unroll
+            for (int kk = 0; kk < kBK / kUmmaK; ++kk) {
+                // +32 bytes of K per step inside the 128-byte swizzle row: +2 in the >>4 address field
+                umma_f16(tmem, ad + 2 * kk, bd + 2 * kk, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+            }
+            umma_commit(empty0 + 8 * s);  // stage reusable once these MMAs have read it
+            if (++s == nst) {
+                s = 0;
+                ph ^= 1;
+            }
+        }
+        umma_commit(done);  // accumulator complete
+    }
+    __syncwarp();
+
+    // ---- epilogue: thread t owns accumulator lane t = output row tile*128 + t
+    mbar_wait(done, 0);
+    tc_fence_after();
+    const int row = threadIdx.x;
+    const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    const int tiles = p.n_out / kBM;
+    float* part = p.ws + (static_cast<int64_t>(tile) * p.splits + split) * p.bn * kBM;
+    const bool split_k = p.splits > 1;
+    // stage the accumulator (or this split's partial) as [bn][128] fp32: in smem for a
+    // single split (the pipeline ring is free now), in the workspace otherwise
+    float* acc = split_k ? part : reinterpret_cast<float*>(smem);
+    for (int c0 = 0; c0 < p.bn; c0 += 16) {
+        float v[16];
+        tmem_ld16(taddr + static_cast<uint32_t>(c0), v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[(c0 + i) * kBM + row] = v[i];
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols) : "memory");
+    }
+    if (split_k) {
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int prev = atomicAdd(p.counters + tile, 1);
+            s_last = prev == p.splits - 1;
+            if (s_last) p.counters[tile] = 0;  // self-reset for the next launch
+        }
+        __syncthreads();
+        if (!s_last) return;
+        __threadfence();
+        // sum every split's partial into smem (this CTA's own included)
+        float* sum = reinterpret_cast<float*>(smem);
+        const float* base = p.ws + static_cast<int64_t>(tile) * p.splits * p.bn * kBM;
+        for (int b = 0; b < p.batch; ++b) {
+            float a = 0.f;
+            for (int s2 = 0; s2 < p.splits; ++s2) a += __ldcg(base + (static_cast<int64_t>(s2) * p.bn + b) * kBM + row);
+            sum[b * kBM + row] = a;
+        }
+        acc = sum;
+        __syncthreads();
+    }
+    (void)tiles;
+
+    // ---- fused epilogues (acc: [bn][128] fp32 in smem, rows >= batch unused)
+    if constexpr (EPI == ASV_EPI_STORE || EPI == ASV_EPI_RESIDUAL) {
+        const int n = tile * kBM + row;
+        for (int b = 0; b < p.batch; ++b) {
+            __nv_bfloat16* dst = p.y + static_cast<int64_t>(b) * p.y_ld + n;
+            float v = acc[b * kBM + row];
+            if constexpr (EPI == ASV_EPI_RESIDUAL) v += __bfloat162float(*dst);
+            *dst = __float2bfloat16(v);
+        }
+    } else if constexpr (EPI == ASV_EPI_SILU_MUL) {
+        // tile rows [0,64) are gate rows, [64,128) the matching up rows of the same 64 outputs
+        if (row < 64) {
+            const int n = tile * 64 + row;
+            for (int b = 0; b < p.batch; ++b) {
+                const float g = acc[b * kBM + row], u = acc[b * kBM + row + 64];
+                p.y[static_cast<int64_t>(b) * p.y_ld + n] = __float2bfloat16(silu(g) * u);
+            }
+        }
+    } else if constexpr (EPI == ASV_EPI_QKV_ROPE) {
+        // one head per tile: [q heads | k heads | v heads]; rotate-half RoPE on q and k
+        const int head = tile;
+        const bool is_q = head < p.n_q_heads, is_k = !is_q && head < p.n_q_heads + p.n_kv_heads;
+        __nv_bfloat16* dst;
+        int h, nh;
+        if (is_q) {
+            dst = p.q;
+            h = head;
+            nh = p.n_q_heads;
+        } else if (is_k) {
+            dst = p.kk;
+            h = head - p.n_q_heads;
+            nh = p.n_kv_heads;
+        } else {
+            dst = p.v;
+            h = head - p.n_q_heads - p.n_kv_heads;
+            nh = p.n_kv_heads;
+        }
+        const int d = row & 63;
+        // inv_freq = theta^(-2d/128)
+        const float inv_freq = exp2f(-p.rope_log2_theta * (2.f * d / 128.f));
+        for (int b = 0; b < p.batch; ++b) {
+            float v = acc[b * kBM + row];
+            if (is_q || is_k) {
+                float sn, cs;
+                sincosf(static_cast<float>(p.positions[b]) * inv_freq, &sn, &cs);
+                const float other = acc[b * kBM + (row ^ 64)];
+                v = row < 64 ? v * cs - other * sn : v * cs + other * sn;
+            }
+            dst[(static_cast<int64_t>(b) * nh + h) * 128 + row] = __float2bfloat16(v);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ host side
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q{};
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess) {
+            fn = reinterpret_cast<EncodeFn>(p);
+        }
+    });
+    return fn;
+}
+
+// 2-D bf16 row-major [rows][cols] map with a {64, box_rows} box and 128-byte swizzle
+bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+    EncodeFn fn = encode_fn();
+    if (fn == nullptr) return false;
+    const cuuint64_t dims[2] = {cols, rows};
+    const cuuint64_t strides[1] = {cols * 2};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int stages_for(int bn) {
+    const int st = kSmemBudget / (kABytes + bn * 128);
+    return st < 2 ? 2 : st > kMaxStages ? kMaxStages : st;
+}
+// the epilogue reuses the ring for the [bn][128] fp32 accumulator tile
+int smem_bytes(int bn) {
+    const int ring = stages_for(bn) * (kABytes + bn * 128);
+    return (ring > bn * 512 ? ring : bn * 512) + 1024 + (2 * kMaxStages + 1) * 8 + 16;
+}
+
+template <int EPI>
+cudaError_t launch_epi(const CUtensorMap& tw, const CUtensorMap& tx, const LinearParams& p, int grid, cudaStream_t st) {
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(linear_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             smem_bytes(256));
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    linear_kernel<EPI><<<grid, 128, smem_bytes(p.bn), st>>>(tw, tx, p);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+// split count: enough CTAs to cover the SMs about twice, each split >= 4 stages
+// (every split gets at least one K block: splits = ceil(kbs / ceil(kbs / splits)))
+int linear_splits(int n_out, int k, int sms) {
+    const int tiles = n_out / kBM, kbs = k / kBK;
+    int splits = 1;
+    while (tiles * splits < 2 * sms && kbs / (splits * 2) >= 4) splits *= 2;
+    const int per = (kbs + splits - 1) / splits;
+    return (kbs + per - 1) / per;
+}
+
+size_t linear_workspace_bytes(int n_out, int k, int max_batch, int sms) {
+    const int bn = ((max_batch + 15) / 16) * 16;
+    const int tiles = n_out / kBM;
+    const int splits = linear_splits(n_out, k, sms);
+    return kCounterBytes + static_cast<size_t>(tiles) * splits * bn * kBM * 4;
+}
+
+cudaError_t linear_preload() {
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, linear_kernel<ASV_EPI_STORE>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, linear_kernel<ASV_EPI_RESIDUAL>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, linear_kernel<ASV_EPI_SILU_MUL>);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, linear_kernel<ASV_EPI_QKV_ROPE>);
+    return e;
+}
+
+static int linear_run(const asv_linear_args* a, cudaStream_t st) {
+    if (a == nullptr || a->w == nullptr || a->x == nullptr || a->workspace == nullptr)
+        return fail(ASV_ERR_INVALID, "linear: null pointer");
+    if (a->n_out <= 0 || a->n_out % kBM != 0) return fail(ASV_ERR_INVALID, "linear: n_out must be a multiple of 128");
+    if (a->n_out / kBM > kMaxTiles) return fail(ASV_ERR_INVALID, "linear: n_out too large");
+    if (a->k <= 0 || a->k % kBK != 0) return fail(ASV_ERR_INVALID, "linear: k must be a multiple of 64");
+    if (a->batch < 1 || a->batch > 256) return fail(ASV_ERR_INVALID, "linear: batch must be in [1, 256]");
+    const int bn = ((a->batch + 15) / 16) * 16;
+    if (a->x_rows < bn) return fail(ASV_ERR_INVALID, "linear: x must have >= batch rounded up to 16 rows");
+    if (a->epilogue == ASV_EPI_QKV_ROPE) {
+        if (a->positions == nullptr || a->q == nullptr || a->k_out == nullptr || a->v_out == nullptr ||
+            a->n_out != 128 * (a->n_q_heads + 2 * a->n_kv_heads))
+            return fail(ASV_ERR_INVALID, "linear: bad QKV/RoPE arguments");
+    } else if (a->y == nullptr) {
+        return fail(ASV_ERR_INVALID, "linear: null y");
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int tiles = a->n_out / kBM, kbs = a->k / kBK;
+    const int splits = linear_splits(a->n_out, a->k, sms);
+    if (a->workspace_bytes < linear_workspace_bytes(a->n_out, a->k, a->batch, sms))
+        return fail(ASV_ERR_INVALID, "linear: workspace too small");
+    CUtensorMap tw, tx;
+    if (!make_map(&tw, a->w, static_cast<uint64_t>(a->n_out), static_cast<uint64_t>(a->k), kBM) ||
+        !make_map(&tx, a->x, static_cast<uint64_t>(a->x_rows), static_cast<uint64_t>(a->k), static_cast<uint32_t>(bn)))
+        return fail(ASV_ERR_CUDA, "linear: cuTensorMapEncodeTiled failed");
+    LinearParams p{};
+    p.n_out = a->n_out;
+    p.k = a->k;
+    p.batch = a->batch;
+    p.bn = bn;
+    p.splits = splits;
+    p.stages = stages_for(bn);
+    p.kb_per_split = (kbs + splits - 1) / splits;
+    p.epi = a->epilogue;
+    p.y = static_cast<__nv_bfloat16*>(a->y);
+    p.y_ld = a->y_ld;
+    p.counters = static_cast<int32_t*>(a->workspace);
+    p.ws = reinterpret_cast<float*>(static_cast<char*>(a->workspace) + kCounterBytes);
+    p.positions = a->positions;
+    p.rope_log2_theta = log2f(a->rope_theta > 0.f ? a->rope_theta : 10000.f);
+    p.q = static_cast<__nv_bfloat16*>(a->q);
+    p.kk = static_cast<__nv_bfloat16*>(a->k_out);
+    p.v = static_cast<__nv_bfloat16*>(a->v_out);
+    p.n_q_heads = a->n_q_heads;
+    p.n_kv_heads = a->n_kv_heads;
+    const int grid = tiles * splits;
+    cudaError_t e;
+    switch (a->epilogue) {
+        case ASV_EPI_STORE: e = launch_epi<ASV_EPI_STORE>(tw, tx, p, grid, st); break;
+        case ASV_EPI_RESIDUAL: e = launch_epi<ASV_EPI_RESIDUAL>(tw, tx, p, grid, st); break;
+        case ASV_EPI_SILU_MUL: e = launch_epi<ASV_EPI_SILU_MUL>(tw, tx, p, grid, st); break;
+        case ASV_EPI_QKV_ROPE: e = launch_epi<ASV_EPI_QKV_ROPE>(tw, tx, p, grid, st); break;
+        default: return fail(ASV_ERR_INVALID, "linear: unknown epilogue");
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "linear launch");
+    return ASV_OK;
+}
+
+// ------------------------------------------------------------------ RMSNorm
+// out[b][:] = h[b][:] * rsqrt(mean(h^2) + eps) * gamma, rows [batch, rows_out) zeroed
+// (they are the MMA-N padding of the next linear layer's activation tile)
+__global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ h, const __nv_bfloat16* __restrict__ gamma,
+                               __nv_bfloat16* __restrict__ out, int dim, int batch, float eps) {
+    const int b = blockIdx.x;
+    __nv_bfloat16* o = out + static_cast<int64_t>(b) * dim;
+    if (b >= batch) {
+        for (int i = threadIdx.x * 8; i < dim; i += blockDim.x * 8) *reinterpret_cast<uint4*>(o + i) = make_uint4(0, 0, 0, 0);
+        return;
+    }
+    const __nv_bfloat16* x = h + static_cast<int64_t>(b) * dim;
+    float ss = 0.f;
+    for (int i = threadIdx.x * 8; i < dim; i += blockDim.x * 8) {
+        const uint4 u = *reinterpret_cast<const uint4*>(x + i);
+        const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float f = __bfloat162float(e[j]);
+            ss += f * f;
+        }
+    }
+    __shared__ float red[32];
+    for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+        for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+        if (threadIdx.x == 0) red[0] = t;
+    }
+    __syncthreads();
+    const float inv = rsqrtf(red[0] / dim + eps);
+    for (int i = threadIdx.x * 8; i < dim; i += blockDim.x * 8) {
+        const uint4 u = *reinterpret_cast<const uint4*>(x + i);
+        const uint4 g = *reinterpret_cast<const uint4*>(gamma + i);
+        const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&u);
+        const __nv_bfloat16* ge = reinterpret_cast<const __nv_bfloat16*>(&g);
+        uint4 r;
+        __nv_bfloat16* re = reinterpret_cast<__nv_bfloat16*>(&r);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) re[j] = __float2bfloat16(__bfloat162float(e[j]) * inv * __bfloat162float(ge[j]));
+        *reinterpret_cast<uint4*>(o + i) = r;
+    }
+}
+
+cudaError_t rmsnorm_launch(const void* h, const void* gamma, void* out, int dim, int batch, int rows_out, float eps,
+                           cudaStream_t st) {
+    rmsnorm_kernel<<<rows_out, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(h),
+                                             static_cast<const __nv_bfloat16*>(gamma),
+                                             static_cast<__nv_bfloat16*>(out), dim, batch, eps);
+    return cudaGetLastError();
+}
+
+cudaError_t rmsnorm_preload() {
+    cudaFuncAttributes fa;
+    return cudaFuncGetAttributes(&fa, rmsnorm_kernel);
+}
+
+}  // namespace asv
+
+// ------------------------------------------------------------------ C ABI
+extern "C" {
+
+size_t asv_linear_workspace_bytes(int32_t n_out, int32_t k, int32_t max_batch, int device) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    if (n_out <= 0 || k <= 0 || max_batch <= 0) return 0;
+    return asv::linear_workspace_bytes(n_out, k, max_batch, sms);
+}
+
+int asv_linear(const asv_linear_args* args, void* stream) {
+    return asv::linear_run(args, static_cast<cudaStream_t>(stream));
+}
+
+int asv_rmsnorm(const void* h, const void* gamma, void* out, int32_t dim, int32_t batch, int32_t rows_out, float eps,
+                void* stream) {
+    if (h == nullptr || gamma == nullptr || out == nullptr || dim <= 0 || dim % 8 != 0 || batch < 1 ||
+        rows_out < batch)
+        return asv::fail(ASV_ERR_INVALID, "rmsnorm: bad arguments");
+    cudaError_t e = asv::rmsnorm_launch(h, gamma, out, dim, batch, rows_out, eps, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return asv::cuda_fail(e, "rmsnorm launch");
+    return ASV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,137 @@
+"""GPU: decode-step linear layers on tcgen05 (asv_linear, asv_rmsnorm) against a
+plain torch fp32 reference of the same op (floating-point kernel: the CPU oracle
+of this repo covers attention; these layers are SURVEY §8(f) rank 1).
+
+Tolerance (bf16 inputs and output, fp32 accumulation in TMEM):
+    |gpu - ref| <= 2e-2 + 2e-2 * |ref| elementwise and rel-L2 <= 8e-3,
+where ref is computed in fp32 from the same bf16 inputs and the output is
+rounded to bf16 once (rel. rounding error 2^-9).
+"""
+import math
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+ATOL, RTOL, RL2 = 2e-2, 2e-2, 8e-3
+
+
+def _rand(shape, seed, scale=1.0):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    return ((torch.rand(shape, generator=g) * 2 - 1) * scale).to(torch.bfloat16).cuda()
+
+
+def _check(got, ref, what):
+    got, ref = got.float(), ref.float()
+    err = (got - ref).abs()
+    rl2 = float((got - ref).norm() / ref.norm().clamp_min(1e-30))
+    print(f"{what}: max_abs={float(err.max()):.3e} rel_l2={rl2:.3e}")
+    assert torch.isfinite(got).all()
+    assert bool((err <= ATOL + RTOL * ref.abs()).all()), f"{what}: max abs err {float(err.max())}"
+    assert rl2 <= RL2, f"{what}: rel-L2 {rl2}"
+
+
+def _x(batch, k, seed):
+    rows = (batch + 15) // 16 * 16
+    x = torch.zeros(rows, k, dtype=torch.bfloat16, device="cuda")
+    x[:batch] = _rand((batch, k), seed)
+    return x
+
+
+@pytest.mark.parametrize("n_out,k,batch", [(128, 64, 1), (256, 512, 5), (4096, 4096, 16), (1024, 11008, 33),
+                                           (12288, 4096, 64), (512, 4096, 256), (384, 1024, 100)])
+def test_store_matches_torch(n_out, k, batch):
+    from paper_2605_23389_b200 import linear as L
+    x = _x(batch, k, 1)
+    w = _rand((n_out, k), 2, 1 / math.sqrt(k))
+    y = torch.full((batch, n_out), float("nan"), dtype=torch.bfloat16, device="cuda")
+    L.linear(x, w, batch, y, L.STORE)
+    torch.cuda.synchronize()
+    ref = x[:batch].float() @ w.float().T
+    _check(y, ref, f"store {n_out}x{k} b{batch}")
+    # repeated call: split-K tile counters self-reset
+    L.linear(x, w, batch, y, L.STORE)
+    torch.cuda.synchronize()
+    _check(y, ref, "store (second call)")
+
+
+@pytest.mark.parametrize("batch", [3, 48])
+def test_residual_adds_in_place(batch):
+    from paper_2605_23389_b200 import linear as L
+    n_out, k = 4096, 4096
+    x = _x(batch, k, 3)
+    w = _rand((n_out, k), 4, 1 / math.sqrt(k))
+    h0 = _rand((batch, n_out), 5)
+    h = h0.clone()
+    L.linear(x, w, batch, h, L.RESIDUAL)
+    torch.cuda.synchronize()
+    _check(h, h0.float() + x[:batch].float() @ w.float().T, f"residual b{batch}")
+
+
+def test_silu_mul_interleaved_gate_up():
+    from paper_2605_23389_b200 import linear as L
+    inter, k, batch = 11008, 4096, 7
+    x = _x(batch, k, 6)
+    gate = _rand((inter, k), 7, 1 / math.sqrt(k))
+    up = _rand((inter, k), 8, 1 / math.sqrt(k))
+    # tile t of the fused weight: 64 gate rows then the 64 up rows of outputs 64t..64t+63
+    w = torch.stack([gate.view(-1, 64, k), up.view(-1, 64, k)], dim=1).reshape(2 * inter, k).contiguous()
+    y = torch.empty(batch, inter, dtype=torch.bfloat16, device="cuda")
+    L.linear(x, w, batch, y, L.SILU_MUL)
+    torch.cuda.synchronize()
+    xf = x[:batch].float()
+    g, u = xf @ gate.float().T, xf @ up.float().T
+    _check(y, torch.nn.functional.silu(g) * u, "silu_mul")
+
+
+@pytest.mark.parametrize("n_q,n_kv,batch", [(32, 32, 4), (40, 8, 19)])
+def test_qkv_rope(n_q, n_kv, batch):
+    from paper_2605_23389_b200 import linear as L
+    k = 128 * n_q
+    n_out = 128 * (n_q + 2 * n_kv)
+    x = _x(batch, k, 9)
+    w = _rand((n_out, k), 10, 1 / math.sqrt(k))
+    pos = torch.randint(0, 20000, (batch,), dtype=torch.int32, device="cuda")
+    q = torch.empty(batch, n_q, 128, dtype=torch.bfloat16, device="cuda")
+    kk = torch.empty(batch, n_kv, 128, dtype=torch.bfloat16, device="cuda")
+    v = torch.empty(batch, n_kv, 128, dtype=torch.bfloat16, device="cuda")
+    L.linear(x, w, batch, None, L.QKV_ROPE, positions=pos, rope_theta=10000.0, q=q, k_out=kk, v_out=v,
+             n_q_heads=n_q, n_kv_heads=n_kv)
+    torch.cuda.synchronize()
+    y = (x[:batch].float() @ w.float().T).view(batch, n_q + 2 * n_kv, 128)
+    inv = 10000.0 ** (-torch.arange(0, 64, device="cuda", dtype=torch.float64) * 2 / 128)
+    ang = pos.double()[:, None] * inv[None, :]
+    cos, sin = torch.cos(ang).float()[:, None, :], torch.sin(ang).float()[:, None, :]
+
+    def rope(t):
+        a, b = t[..., :64], t[..., 64:]
+        return torch.cat([a * cos - b * sin, b * cos + a * sin], dim=-1)
+
+    _check(q, rope(y[:, :n_q]), "rope q")
+    _check(kk, rope(y[:, n_q:n_q + n_kv]), "rope k")
+    _check(v, y[:, n_q + n_kv:], "v")
+
+
+def test_rmsnorm():
+    from paper_2605_23389_b200 import linear as L
+    batch, dim = 9, 4096
+    h = _rand((batch, dim), 11, 3.0)
+    gamma = _rand((dim,), 12)
+    out = torch.full((16, dim), 7.0, dtype=torch.bfloat16, device="cuda")
+    L.rmsnorm(h, gamma, out, batch, 1e-5)
+    torch.cuda.synchronize()
+    hf = h.float()
+    ref = hf * torch.rsqrt(hf.pow(2).mean(-1, keepdim=True) + 1e-5) * gamma.float()
+    _check(out[:batch], ref, "rmsnorm")
+    assert not out[batch:].float().abs().any()  # MMA-N padding rows zeroed
+
+
+def test_bad_arguments_fail_loudly():
+    from paper_2605_23389_b200 import _lib
+    from paper_2605_23389_b200 import linear as L
+    x = _x(4, 128, 1)
+    w = _rand((100, 128), 2)  # n_out not a multiple of 128
+    with pytest.raises(ValueError, match="multiple of 128"):
+        L.linear(x, w, 4, torch.empty(4, 100, dtype=torch.bfloat16, device="cuda"))
