@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=WORKLOAD)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-full-step", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=12.0)
     return ap.parse_args()
@@ -269,6 +270,12 @@ def main():
         res = E.engine_run(cfg, execute_transfers=False, **run_kw)
     clocks = clk.summary()
     d.barrier()
+    # the whole decoder layer stack per step (RMSNorm, QKV+RoPE / O / gate-up / down GEMMs on
+    # tcgen05 with synthetic weights, attention), KV resident: SURVEY §8(f) rank 1
+    full = None
+    if not args.no_full_step:
+        full = E.engine_run(cfg, execute_transfers=False, full_step=True, **run_kw)
+        d.barrier()
     e2e = None
     if not args.no_e2e:
         ek = max(K, E2E_MIN_STEPS)
@@ -328,6 +335,24 @@ def main():
                     "hidden_fraction_def": "overlap of PCIe-busy and attention time / the shorter of the two",
                     "bound": "pcie" if link_ms >= e2e["attn_ms"] else "hbm"}
 
+    full_obj = None
+    if full is not None:
+        fwin = d.reduce([full["window_ms"]], "MAX")[0]
+        ftok = d.reduce([float(full["tokens_timed"])], "SUM")[0]
+        f_steps = max(1, full["iterations_timed"])
+        f_bytes = full["attn_bytes"] + full["weight_bytes"]
+        full_obj = {"value": ftok / (fwin / 1e3) if fwin > 0 else 0.0, "unit": "tokens/s",
+                    "ms_per_step": fwin / f_steps,
+                    "what": "per step and layer: RMSNorm, QKV GEMM + RoPE, paged attention + KV append, O GEMM + "
+                            "residual, RMSNorm, gate/up GEMM + SiLU, down GEMM + residual (bf16, fp32 accumulate; "
+                            "GEMMs on tcgen05, synthetic Llama-2-7B-shape weights)",
+                    "weight_gb_per_step": full["weight_bytes"] / f_steps / 1e9,
+                    "kv_gb_per_step": full["attn_bytes"] / f_steps / 1e9,
+                    "hbm_gbps": f_bytes / (full["window_ms"] * 1e-3) / 1e9 if full["window_ms"] > 0 else None,
+                    "frac_of_hbm_peak": (f_bytes / (full["window_ms"] * 1e-3) / 1e9 / peak
+                                         if full["window_ms"] > 0 else None),
+                    "gpu_launches": int(full["kernel_launches_timed"])}
+
     cpu = None
     if d.rank == 0 and d.world == 1 and not args.no_cpu_baseline:
         try:
@@ -348,6 +373,7 @@ def main():
                        "steady_start_iteration": S,
                        "l2": "inputs larger than L2: every step reads ~10-60 GB of KV (L2 is 126 MB)"},
             "e2e": e2e_obj, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
+            "full_decode_step": full_obj,
             "gpu_launches": int(res["kernel_launches_timed"]),
             "decode_attn_hbm_gbps": achieved, "kv_prefetch": prefetch,
             "virtual_clock_tok_s": res["virtual_decode_tok_s"],

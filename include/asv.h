@@ -222,15 +222,17 @@ typedef struct asv_linear_args {
     void* k_out;             /* QKV_ROPE: [batch][n_kv_heads][128] */
     void* v_out;             /* QKV_ROPE: [batch][n_kv_heads][128] */
     int32_t n_q_heads, n_kv_heads;
-    void* workspace;         /* asv_linear_workspace_bytes(), zero-filled once before first use */
-    size_t workspace_bytes;
+    int32_t pdl;             /* 1: programmatic dependent launch — W streams into the ring while the
+                                previous kernel on the stream finishes; X, y wait for it */
 } asv_linear_args;
 
-size_t asv_linear_workspace_bytes(int32_t n_out, int32_t k, int32_t max_batch, int device);
+/* One launch: one CTA per (128-row tile, K split); the K splits of a tile are one
+ * thread-block cluster and reduce through distributed shared memory, so no
+ * workspace is needed.  Stream-ordered; no host synchronisation. */
 int asv_linear(const asv_linear_args* args, void* stream);
 /* out[b][:] = h[b][:] * rsqrt(mean(h[b]^2) + eps) * gamma; rows [batch, rows_out) of out zeroed */
 int asv_rmsnorm(const void* h, const void* gamma, void* out, int32_t dim, int32_t batch, int32_t rows_out,
-                float eps, void* stream);
+                float eps, int32_t pdl, void* stream);
 
 /* ------------------------------------------------------------------------ */
 /* Decode engine on the GPU: the reference engine's decisions (virtual clock, */
@@ -257,6 +259,11 @@ typedef struct asv_engine_opts {
                                    lets prefetches issued before the executed span reach steady state) */
     int32_t pair_mode;          /* 1: separate candidate-buffer pool even when prefetch_device ==
                                    decode_device (exercises the admit/evict copy path on one GPU) */
+    int32_t full_step;          /* 1: every iteration runs the whole decoder layer stack (RMSNorm,
+                                   QKV+RoPE, attention, O + residual, RMSNorm, gate/up SiLU, down +
+                                   residual) with synthetic weights, not attention alone */
+    int32_t intermediate_size;  /* MLP width for full_step (0: 11008 for hidden 4096, 13824 for 5120,
+                                   else 8/3 hidden rounded up to 128) */
 } asv_engine_opts;
 
 /* transfer kinds for the per-kind byte counters */
@@ -304,6 +311,7 @@ typedef struct asv_engine_stats {
     int64_t hazard_waits;         /* copy-stream waits on a page's last iteration (page reuse) */
     int64_t result_d2h_bytes_window; /* e2e: each iteration's attention output [b][n_h][128] bf16 read back
                                         to pinned host memory (SM stores, no copy-engine queue) */
+    int64_t weight_bytes;         /* full_step: decoder weight bytes streamed inside the window */
 } asv_engine_stats;
 
 int asv_engine_run(const char* config_json, const char* policy_override, const asv_engine_opts* opts,

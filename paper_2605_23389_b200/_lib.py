@@ -80,8 +80,7 @@ class LinearArgs(C.Structure):
         ("v_out", C.c_void_p),
         ("n_q_heads", C.c_int32),
         ("n_kv_heads", C.c_int32),
-        ("workspace", C.c_void_p),
-        ("workspace_bytes", C.c_size_t),
+        ("pdl", C.c_int32),
     ]
 
 
@@ -106,6 +105,8 @@ class EngineOpts(C.Structure):
         ("run_ahead", C.c_int32),
         ("copy_begin", C.c_int64),
         ("pair_mode", C.c_int32),
+        ("full_step", C.c_int32),
+        ("intermediate_size", C.c_int32),
     ]
 
 
@@ -145,6 +146,7 @@ class EngineStats(C.Structure):
         ("host_wait_ms", C.c_double),
         ("hazard_waits", C.c_int64),
         ("result_d2h_bytes_window", C.c_int64),
+        ("weight_bytes", C.c_int64),
     ]
 
     def as_dict(self):
@@ -186,10 +188,9 @@ SIGNATURES = [
     ("asv_kv_copy_d2d", C.c_int,
      [C.POINTER(AttnShape), C.c_void_p, C.c_int64, C.c_int32, C.POINTER(C.c_int32), C.c_void_p, C.c_int64,
       C.c_int32, C.POINTER(C.c_int32), C.c_int64, C.c_void_p, C.POINTER(C.c_int64)]),
-    ("asv_linear_workspace_bytes", C.c_size_t, [C.c_int32, C.c_int32, C.c_int32, C.c_int]),
     ("asv_linear", C.c_int, [C.POINTER(LinearArgs), C.c_void_p]),
     ("asv_rmsnorm", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_float,
-                              C.c_void_p]),
+                              C.c_int32, C.c_void_p]),
     ("asv_run_config_jsonl", C.c_int,
      [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
     ("asv_engine_run", C.c_int,

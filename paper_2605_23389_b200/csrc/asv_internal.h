@@ -76,12 +76,11 @@ cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st);
 cudaError_t sm_copy(const int32_t* src, int32_t* dst, int64_t n_int32, cudaStream_t st);
 
 // decode-step linear layers (decode_gemm.cu)
-int linear_splits(int n_out, int k, int sms);
-size_t linear_workspace_bytes(int n_out, int k, int max_batch, int sms);
 cudaError_t linear_preload();
 cudaError_t rmsnorm_launch(const void* h, const void* gamma, void* out, int dim, int batch, int rows_out, float eps,
-                           cudaStream_t st);
+                           bool pdl, cudaStream_t st);
 cudaError_t rmsnorm_preload();
+cudaError_t fill_random_bf16(void* p, int64_t n, uint64_t seed, float scale, float offset, cudaStream_t st);
 
 // thread-local last error (asv_last_error)
 void set_error(const std::string& msg);

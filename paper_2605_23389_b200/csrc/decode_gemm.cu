@@ -11,8 +11,9 @@
 // warp 1 lane 0 issues tcgen05.mma (kind::f16, bf16 in, fp32 accumulate in
 // TMEM) and frees each stage with tcgen05.commit; all four warps then read the
 // accumulator with tcgen05.ld (warp w owns TMEM lanes 32w..32w+31 = output
-// rows).  K splits of one tile meet in an fp32 workspace; the last arriving CTA
-// runs the fused epilogue:
+// rows).  The K splits of one tile are one thread-block cluster: partials meet
+// in distributed shared memory, each CTA reduces a slice of the batch columns
+// and runs the fused epilogue on it:
 //   STORE     y[b][n]  = acc
 //   RESIDUAL  y[b][n] += acc                         (o_proj / down_proj + residual)
 //   SILU_MUL  y[b][j]  = silu(acc_gate) * acc_up       (gate/up rows interleaved per tile)
@@ -21,6 +22,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <mutex>
 
@@ -36,10 +38,7 @@ constexpr int kUmmaK = 16;            // K per tcgen05.mma (kind::f16)
 constexpr int kMaxStages = 8;
 constexpr int kSmemBudget = 100 * 1024;  // ring <= ~100 KiB: two CTAs per SM keep more of W in flight
 constexpr int kABytes = kBM * kBK * 2;   // 16 KiB
-// workspace: a fixed counter area (tile arrival counters stay zero between calls
-// whatever the shape) followed by the fp32 split partials
-constexpr int kMaxTiles = 16384;
-constexpr size_t kCounterBytes = kMaxTiles * 4;
+constexpr int kMaxSplits = 8;            // K splits of a tile = one portable thread-block cluster
 
 struct LinearParams {
     int32_t n_out, k, batch, bn;     // bn: batch padded to a multiple of 16 (MMA N)
@@ -47,8 +46,6 @@ struct LinearParams {
     int32_t epi;
     __nv_bfloat16* y;
     int32_t y_ld;
-    float* ws;                       // [tiles][splits][bn][128] fp32 partials
-    int32_t* counters;               // [tiles] arrival counters (self-resetting)
     // QKV_ROPE
     const int32_t* positions;        // [batch] position of the new token
     float rope_log2_theta;           // log2(theta)
@@ -101,6 +98,8 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -156,7 +155,6 @@ __global__ void __launch_bounds__(128, 2)
     const int ring = nst * stage_bytes > p.bn * 512 ? nst * stage_bytes : p.bn * 512;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kMaxStages + 1);
-    __shared__ int s_last;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tile = blockIdx.x / p.splits, split = blockIdx.x % p.splits;
@@ -185,13 +183,28 @@ __global__ void __launch_bounds__(128, 2)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // the next kernel may start its own prologue / weight prefetch now (it waits for
+    // this grid's completion before touching what this grid writes)
+    grid_dep_launch();
 
     if (warp == 0 && lane == 0) {
         // ---- TMA producer: W tiles (streamed once: evict-first), X tiles (reused by every tile: evict-last)
+        // The weights never depend on the previous kernel: the first ring's worth
+        // of W is requested BEFORE griddepcontrol.wait (with PDL this overlaps the
+        // producing kernel's tail); the activations X only after it.
         const uint64_t pw = policy_evict_first(), px = policy_evict_last();
-        int s = 0;
-        uint32_t ph = 0;
-        for (int kb = kb0; kb < kb1; ++kb) {
+        const int pre = min(nst, kb1 - kb0);
+        for (int i = 0; i < pre; ++i) {
+            mbar_expect_tx(full0 + 8 * i, static_cast<uint32_t>(stage_bytes));
+            tma_load_2d(smem_u32(smem + i * stage_bytes), &tm_w, (kb0 + i) * kBK, tile * kBM, full0 + 8 * i, pw);
+        }
+        grid_dep_wait();
+        for (int i = 0; i < pre; ++i) {
+            tma_load_2d(smem_u32(smem + i * stage_bytes) + kABytes, &tm_x, (kb0 + i) * kBK, 0, full0 + 8 * i, px);
+        }
+        int s = pre == nst ? 0 : pre;
+        uint32_t ph = pre == nst ? 1 : 0;
+        for (int kb = kb0 + pre; kb < kb1; ++kb) {
             mbar_wait(empty0 + 8 * s, ph ^ 1);
             const uint32_t a = smem_u32(smem + s * stage_bytes);
             mbar_expect_tx(full0 + 8 * s, static_cast<uint32_t>(stage_bytes));
@@ -227,102 +240,87 @@ __global__ void __launch_bounds__(128, 2)
     }
     __syncwarp();
 
-    // ---- epilogue: thread t owns accumulator lane t = output row tile*128 + t
+    // ---- epilogue 1: TMEM -> this CTA's smem as [bn][128] fp32 (the ring is free:
+    // every stage was consumed by an MMA that has completed)
     mbar_wait(done, 0);
     tc_fence_after();
-    const int row = threadIdx.x;
     const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-    const int tiles = p.n_out / kBM;
-    float* part = p.ws + (static_cast<int64_t>(tile) * p.splits + split) * p.bn * kBM;
-    const bool split_k = p.splits > 1;
-    // stage the accumulator (or this split's partial) as [bn][128] fp32: in smem for a
-    // single split (the pipeline ring is free now), in the workspace otherwise
-    float* acc = split_k ? part : reinterpret_cast<float*>(smem);
+    float* part = reinterpret_cast<float*>(smem);
     for (int c0 = 0; c0 < p.bn; c0 += 16) {
         float v[16];
         tmem_ld16(taddr + static_cast<uint32_t>(c0), v);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) acc[(c0 + i) * kBM + row] = v[i];
+        for (int i = 0; i < 16; ++i) part[(c0 + i) * kBM + threadIdx.x] = v[i];
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols) : "memory");
     }
-    if (split_k) {
-        __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            const int prev = atomicAdd(p.counters + tile, 1);
-            s_last = prev == p.splits - 1;
-            if (s_last) p.counters[tile] = 0;  // self-reset for the next launch
-        }
-        __syncthreads();
-        if (!s_last) return;
-        __threadfence();
-        // sum every split's partial into smem (this CTA's own included)
-        float* sum = reinterpret_cast<float*>(smem);
-        const float* base = p.ws + static_cast<int64_t>(tile) * p.splits * p.bn * kBM;
-        for (int b = 0; b < p.batch; ++b) {
-            float a = 0.f;
-            for (int s2 = 0; s2 < p.splits; ++s2) a += __ldcg(base + (static_cast<int64_t>(s2) * p.bn + b) * kBM + row);
-            sum[b * kBM + row] = a;
-        }
-        acc = sum;
-        __syncthreads();
+    // ---- epilogue 2: the K splits of this tile form one thread-block cluster; after a
+    // cluster barrier every CTA reduces a slice of the batch columns straight out of
+    // the other CTAs' shared memory (DSMEM) and applies the fused epilogue to it.
+    // Thread t handles row pair (r, r + 64), r = t & 63, so the SiLU gate/up and
+    // RoPE rotate-half partners are in one thread's registers.
+    if (p.splits > 1) {
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     }
-    (void)tiles;
-
-    // ---- fused epilogues (acc: [bn][128] fp32 in smem, rows >= batch unused)
-    if constexpr (EPI == ASV_EPI_STORE || EPI == ASV_EPI_RESIDUAL) {
-        const int n = tile * kBM + row;
-        for (int b = 0; b < p.batch; ++b) {
-            __nv_bfloat16* dst = p.y + static_cast<int64_t>(b) * p.y_ld + n;
-            float v = acc[b * kBM + row];
-            if constexpr (EPI == ASV_EPI_RESIDUAL) v += __bfloat162float(*dst);
-            *dst = __float2bfloat16(v);
-        }
-    } else if constexpr (EPI == ASV_EPI_SILU_MUL) {
-        // tile rows [0,64) are gate rows, [64,128) the matching up rows of the same 64 outputs
-        if (row < 64) {
-            const int n = tile * 64 + row;
-            for (int b = 0; b < p.batch; ++b) {
-                const float g = acc[b * kBM + row], u = acc[b * kBM + row + 64];
-                p.y[static_cast<int64_t>(b) * p.y_ld + n] = __float2bfloat16(silu(g) * u);
+    grid_dep_wait();  // outputs / residual / positions may belong to the previous kernel
+    const int per = (p.batch + p.splits - 1) / p.splits;
+    const int cb = split * per, ce = min(cb + per, p.batch);
+    const int r = threadIdx.x & 63;
+    const uint32_t part_s = smem_u32(part);
+    for (int c = cb + (threadIdx.x >> 6); c < ce; c += 2) {
+        float lo = 0.f, hi = 0.f;
+        const uint32_t off_lo = part_s + static_cast<uint32_t>((c * kBM + r) * 4);
+        for (int s2 = 0; s2 < p.splits; ++s2) {
+            uint32_t ra = off_lo, rb = off_lo + 64 * 4;
+            if (p.splits > 1) {
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(off_lo), "r"(s2));
+                rb = ra + 64 * 4;
             }
+            float x0, x1;
+            asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(x0) : "r"(ra) : "memory");
+            asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(x1) : "r"(rb) : "memory");
+            lo += x0;
+            hi += x1;
         }
-    } else if constexpr (EPI == ASV_EPI_QKV_ROPE) {
-        // one head per tile: [q heads | k heads | v heads]; rotate-half RoPE on q and k
-        const int head = tile;
-        const bool is_q = head < p.n_q_heads, is_k = !is_q && head < p.n_q_heads + p.n_kv_heads;
-        __nv_bfloat16* dst;
-        int h, nh;
-        if (is_q) {
-            dst = p.q;
-            h = head;
-            nh = p.n_q_heads;
-        } else if (is_k) {
-            dst = p.kk;
-            h = head - p.n_q_heads;
-            nh = p.n_kv_heads;
-        } else {
-            dst = p.v;
-            h = head - p.n_q_heads - p.n_kv_heads;
-            nh = p.n_kv_heads;
-        }
-        const int d = row & 63;
-        // inv_freq = theta^(-2d/128)
-        const float inv_freq = exp2f(-p.rope_log2_theta * (2.f * d / 128.f));
-        for (int b = 0; b < p.batch; ++b) {
-            float v = acc[b * kBM + row];
+        const int b = c;
+        if constexpr (EPI == ASV_EPI_STORE || EPI == ASV_EPI_RESIDUAL) {
+            __nv_bfloat16* dst = p.y + static_cast<int64_t>(b) * p.y_ld + tile * kBM + r;
+            if constexpr (EPI == ASV_EPI_RESIDUAL) {
+                lo += __bfloat162float(dst[0]);
+                hi += __bfloat162float(dst[64]);
+            }
+            dst[0] = __float2bfloat16(lo);
+            dst[64] = __float2bfloat16(hi);
+        } else if constexpr (EPI == ASV_EPI_SILU_MUL) {
+            // tile rows [0,64) gate, [64,128) the matching up rows of outputs 64*tile + r
+            p.y[static_cast<int64_t>(b) * p.y_ld + tile * 64 + r] = __float2bfloat16(silu(lo) * hi);
+        } else if constexpr (EPI == ASV_EPI_QKV_ROPE) {
+            // one head per tile: [q heads | k heads | v heads]; rotate-half RoPE on q and k
+            const int head = tile;
+            const bool is_q = head < p.n_q_heads, is_k = !is_q && head < p.n_q_heads + p.n_kv_heads;
+            __nv_bfloat16* dst = is_q ? p.q : is_k ? p.kk : p.v;
+            const int h = is_q ? head : is_k ? head - p.n_q_heads : head - p.n_q_heads - p.n_kv_heads;
+            const int nh = is_q ? p.n_q_heads : p.n_kv_heads;
             if (is_q || is_k) {
+                const float inv_freq = exp2f(-p.rope_log2_theta * (2.f * r / 128.f));  // theta^(-2r/128)
                 float sn, cs;
                 sincosf(static_cast<float>(p.positions[b]) * inv_freq, &sn, &cs);
-                const float other = acc[b * kBM + (row ^ 64)];
-                v = row < 64 ? v * cs - other * sn : v * cs + other * sn;
+                const float a0 = lo * cs - hi * sn, a1 = hi * cs + lo * sn;
+                lo = a0;
+                hi = a1;
             }
-            dst[(static_cast<int64_t>(b) * nh + h) * 128 + row] = __float2bfloat16(v);
+            __nv_bfloat16* o = dst + (static_cast<int64_t>(b) * nh + h) * 128;
+            o[r] = __float2bfloat16(lo);
+            o[r + 64] = __float2bfloat16(hi);
         }
+    }
+    if (p.splits > 1) {  // no CTA may exit while a peer still reads its shared memory
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     }
 }
 
@@ -369,7 +367,8 @@ int smem_bytes(int bn) {
 }
 
 template <int EPI>
-cudaError_t launch_epi(const CUtensorMap& tw, const CUtensorMap& tx, const LinearParams& p, int grid, cudaStream_t st) {
+cudaError_t launch_epi(const CUtensorMap& tw, const CUtensorMap& tx, const LinearParams& p, int grid, bool pdl,
+                       cudaStream_t st) {
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(linear_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -377,27 +376,86 @@ cudaError_t launch_epi(const CUtensorMap& tw, const CUtensorMap& tx, const Linea
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    linear_kernel<EPI><<<grid, 128, smem_bytes(p.bn), st>>>(tw, tx, p);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = smem_bytes(p.bn);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int n = 0;
+    if (p.splits > 1) {
+        attr[n].id = cudaLaunchAttributeClusterDimension;  // the K splits of a tile form a cluster
+        attr[n].val.clusterDim.x = p.splits;
+        attr[n].val.clusterDim.y = 1;
+        attr[n].val.clusterDim.z = 1;
+        ++n;
+    }
+    if (pdl) {
+        attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = n;
+    return cudaLaunchKernelEx(&cfg, linear_kernel<EPI>, tw, tx, p);
 }
 
 }  // namespace
 
-// split count: enough CTAs to cover the SMs about twice, each split >= 4 stages
-// (every split gets at least one K block: splits = ceil(kbs / ceil(kbs / splits)))
-int linear_splits(int n_out, int k, int sms) {
-    const int tiles = n_out / kBM, kbs = k / kBK;
-    int splits = 1;
-    while (tiles * splits < 2 * sms && kbs / (splits * 2) >= 4) splits *= 2;
-    const int per = (kbs + splits - 1) / splits;
-    return (kbs + per - 1) / per;
+// CTAs per SM at this batch (shared memory of the ring / accumulator staging)
+int ctas_per_sm(int bn) {
+    const int per = smem_bytes(bn) + 1024;
+    const int n = 232448 / per;
+    return n < 1 ? 1 : n > 2 ? 2 : n;
 }
 
-size_t linear_workspace_bytes(int n_out, int k, int max_batch, int sms) {
-    const int bn = ((max_batch + 15) / 16) * 16;
-    const int tiles = n_out / kBM;
-    const int splits = linear_splits(n_out, k, sms);
-    return kCounterBytes + static_cast<size_t>(tiles) * splits * bn * kBM * 4;
+// Clusters of `splits` CTAs (at batch tile bn) the device holds at once.
+int active_clusters(int bn, int splits) {
+    static std::mutex mu;
+    static int cache[17][kMaxSplits + 1] = {};
+    std::lock_guard<std::mutex> lk(mu);
+    int& c = cache[bn / 16][splits];
+    if (c == 0) {
+        // every epilogue instantiation has the same resources: query one
+        static bool configured = false;
+        if (!configured) {
+            cudaFuncSetAttribute(linear_kernel<ASV_EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem_bytes(256));
+            cudaFuncSetAttribute(linear_kernel<ASV_EPI_STORE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+            configured = true;
+        }
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(splits * 64);
+        cfg.blockDim = dim3(128);
+        cfg.dynamicSmemBytes = smem_bytes(bn);
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = splits;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, linear_kernel<ASV_EPI_STORE>, &cfg) != cudaSuccess || n < 1) {
+            cudaGetLastError();
+            n = 148 * ctas_per_sm(bn) / splits;
+        }
+        c = n;
+    }
+    return c;
+}
+
+// K splits per tile: the most splits (<= kMaxSplits = one portable cluster, each
+// >= 2 K blocks, none empty) whose tiles x clusters still run in ONE wave
+// (measured: a second partial wave of short CTAs costs more than it saves).
+int linear_splits(int n_out, int k, int bn) {
+    const int tiles = n_out / kBM, kbs = k / kBK;
+    int best = 1;
+    for (int sp = 2; sp <= kMaxSplits && sp <= kbs / 2; ++sp) {
+        if (tiles <= active_clusters(bn, sp)) best = sp;
+    }
+    const int per = (kbs + best - 1) / best;
+    return (kbs + per - 1) / per;
 }
 
 cudaError_t linear_preload() {
@@ -410,10 +468,8 @@ cudaError_t linear_preload() {
 }
 
 static int linear_run(const asv_linear_args* a, cudaStream_t st) {
-    if (a == nullptr || a->w == nullptr || a->x == nullptr || a->workspace == nullptr)
-        return fail(ASV_ERR_INVALID, "linear: null pointer");
+    if (a == nullptr || a->w == nullptr || a->x == nullptr) return fail(ASV_ERR_INVALID, "linear: null pointer");
     if (a->n_out <= 0 || a->n_out % kBM != 0) return fail(ASV_ERR_INVALID, "linear: n_out must be a multiple of 128");
-    if (a->n_out / kBM > kMaxTiles) return fail(ASV_ERR_INVALID, "linear: n_out too large");
     if (a->k <= 0 || a->k % kBK != 0) return fail(ASV_ERR_INVALID, "linear: k must be a multiple of 64");
     if (a->batch < 1 || a->batch > 256) return fail(ASV_ERR_INVALID, "linear: batch must be in [1, 256]");
     const int bn = ((a->batch + 15) / 16) * 16;
@@ -429,9 +485,14 @@ static int linear_run(const asv_linear_args* a, cudaStream_t st) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int tiles = a->n_out / kBM, kbs = a->k / kBK;
-    const int splits = linear_splits(a->n_out, a->k, sms);
-    if (a->workspace_bytes < linear_workspace_bytes(a->n_out, a->k, a->batch, sms))
-        return fail(ASV_ERR_INVALID, "linear: workspace too small");
+    int splits = linear_splits(a->n_out, a->k, bn);
+    if (const char* e = getenv("ASV_LINEAR_SPLITS")) {  // tuning experiments only
+        const int kbs_ = a->k / kBK, want = atoi(e);
+        if (want >= 1 && want <= kMaxSplits && want <= kbs_) {
+            const int per = (kbs_ + want - 1) / want;
+            splits = (kbs_ + per - 1) / per;
+        }
+    }
     CUtensorMap tw, tx;
     if (!make_map(&tw, a->w, static_cast<uint64_t>(a->n_out), static_cast<uint64_t>(a->k), kBM) ||
         !make_map(&tx, a->x, static_cast<uint64_t>(a->x_rows), static_cast<uint64_t>(a->k), static_cast<uint32_t>(bn)))
@@ -447,8 +508,6 @@ static int linear_run(const asv_linear_args* a, cudaStream_t st) {
     p.epi = a->epilogue;
     p.y = static_cast<__nv_bfloat16*>(a->y);
     p.y_ld = a->y_ld;
-    p.counters = static_cast<int32_t*>(a->workspace);
-    p.ws = reinterpret_cast<float*>(static_cast<char*>(a->workspace) + kCounterBytes);
     p.positions = a->positions;
     p.rope_log2_theta = log2f(a->rope_theta > 0.f ? a->rope_theta : 10000.f);
     p.q = static_cast<__nv_bfloat16*>(a->q);
@@ -459,10 +518,10 @@ static int linear_run(const asv_linear_args* a, cudaStream_t st) {
     const int grid = tiles * splits;
     cudaError_t e;
     switch (a->epilogue) {
-        case ASV_EPI_STORE: e = launch_epi<ASV_EPI_STORE>(tw, tx, p, grid, st); break;
-        case ASV_EPI_RESIDUAL: e = launch_epi<ASV_EPI_RESIDUAL>(tw, tx, p, grid, st); break;
-        case ASV_EPI_SILU_MUL: e = launch_epi<ASV_EPI_SILU_MUL>(tw, tx, p, grid, st); break;
-        case ASV_EPI_QKV_ROPE: e = launch_epi<ASV_EPI_QKV_ROPE>(tw, tx, p, grid, st); break;
+        case ASV_EPI_STORE: e = launch_epi<ASV_EPI_STORE>(tw, tx, p, grid, a->pdl != 0, st); break;
+        case ASV_EPI_RESIDUAL: e = launch_epi<ASV_EPI_RESIDUAL>(tw, tx, p, grid, a->pdl != 0, st); break;
+        case ASV_EPI_SILU_MUL: e = launch_epi<ASV_EPI_SILU_MUL>(tw, tx, p, grid, a->pdl != 0, st); break;
+        case ASV_EPI_QKV_ROPE: e = launch_epi<ASV_EPI_QKV_ROPE>(tw, tx, p, grid, a->pdl != 0, st); break;
         default: return fail(ASV_ERR_INVALID, "linear: unknown epilogue");
     }
     if (e != cudaSuccess) return cuda_fail(e, "linear launch");
@@ -474,6 +533,8 @@ static int linear_run(const asv_linear_args* a, cudaStream_t st) {
 // (they are the MMA-N padding of the next linear layer's activation tile)
 __global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ h, const __nv_bfloat16* __restrict__ gamma,
                                __nv_bfloat16* __restrict__ out, int dim, int batch, float eps) {
+    grid_dep_wait();  // h is the previous kernel's output (no-op without PDL)
+    grid_dep_launch();
     const int b = blockIdx.x;
     __nv_bfloat16* o = out + static_cast<int64_t>(b) * dim;
     if (b >= batch) {
@@ -516,10 +577,37 @@ __global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ h, const __nv_b
 }
 
 cudaError_t rmsnorm_launch(const void* h, const void* gamma, void* out, int dim, int batch, int rows_out, float eps,
-                           cudaStream_t st) {
-    rmsnorm_kernel<<<rows_out, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(h),
-                                             static_cast<const __nv_bfloat16*>(gamma),
-                                             static_cast<__nv_bfloat16*>(out), dim, batch, eps);
+                           bool pdl, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(rows_out);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, rmsnorm_kernel, static_cast<const __nv_bfloat16*>(h),
+                              static_cast<const __nv_bfloat16*>(gamma), static_cast<__nv_bfloat16*>(out), dim, batch,
+                              eps);
+}
+
+// synthetic weights / activations: splitmix64(seed + i) -> U[-1, 1) * scale + offset, bf16
+__global__ void fill_random_kernel(__nv_bfloat16* p, int64_t n, uint64_t seed, float scale, float offset) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        uint64_t z = seed + static_cast<uint64_t>(i) * 0x9e3779b97f4a7c15ULL;
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+        z ^= z >> 31;
+        const float u = static_cast<float>(z >> 40) * (1.0f / 16777216.0f) * 2.f - 1.f;
+        p[i] = __float2bfloat16(u * scale + offset);
+    }
+}
+
+cudaError_t fill_random_bf16(void* p, int64_t n, uint64_t seed, float scale, float offset, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    fill_random_kernel<<<148 * 8, 256, 0, st>>>(static_cast<__nv_bfloat16*>(p), n, seed, scale, offset);
     return cudaGetLastError();
 }
 
@@ -533,23 +621,17 @@ cudaError_t rmsnorm_preload() {
 // ------------------------------------------------------------------ C ABI
 extern "C" {
 
-size_t asv_linear_workspace_bytes(int32_t n_out, int32_t k, int32_t max_batch, int device) {
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    if (n_out <= 0 || k <= 0 || max_batch <= 0) return 0;
-    return asv::linear_workspace_bytes(n_out, k, max_batch, sms);
-}
-
 int asv_linear(const asv_linear_args* args, void* stream) {
     return asv::linear_run(args, static_cast<cudaStream_t>(stream));
 }
 
 int asv_rmsnorm(const void* h, const void* gamma, void* out, int32_t dim, int32_t batch, int32_t rows_out, float eps,
-                void* stream) {
+                int32_t pdl, void* stream) {
     if (h == nullptr || gamma == nullptr || out == nullptr || dim <= 0 || dim % 8 != 0 || batch < 1 ||
         rows_out < batch)
         return asv::fail(ASV_ERR_INVALID, "rmsnorm: bad arguments");
-    cudaError_t e = asv::rmsnorm_launch(h, gamma, out, dim, batch, rows_out, eps, static_cast<cudaStream_t>(stream));
+    cudaError_t e =
+        asv::rmsnorm_launch(h, gamma, out, dim, batch, rows_out, eps, pdl != 0, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return asv::cuda_fail(e, "rmsnorm launch");
     return ASV_OK;
 }

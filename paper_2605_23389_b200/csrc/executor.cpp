@@ -39,6 +39,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cmath>
 #include <thread>
 #include <cstdio>
 #include <cstdlib>
@@ -252,6 +253,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
         fill_random(q_, qbytes / 2, 11);
         fill_random(k_new_, kvbytes / 2, 12);
         fill_random(v_new_, kvbytes / 2, 13);
+        if (o.full_step) init_full_step();
         // Run-ahead ring of in-flight iterations (events, timestamps) and a plan
         // arena: each iteration's plan occupies exactly its size in a circular
         // mapped-host + device arena, so the host can run hundreds of iterations
@@ -338,6 +340,10 @@ class GpuExecutor : public prefixsim::EngineObserver {
         cudaFree(q_);
         cudaFree(out_);
         if (result_host_) cudaFreeHost(result_host_);
+        if (weights_) cudaFree(weights_);
+        if (h_) cudaFree(h_);
+        if (x_) cudaFree(x_);
+        if (act_) cudaFree(act_);
         cudaFree(k_new_);
         cudaFree(v_new_);
         cudaFree(ws_);
@@ -490,21 +496,29 @@ class GpuExecutor : public prefixsim::EngineObserver {
             }
         }
         const int64_t ready_waits = static_cast<int64_t>(waits.size());
-        const int64_t pw = plan_region(e, (static_cast<int64_t>(plan.total_int32) + 3) & ~int64_t(3));
+        // plan (+ for full steps the token positions = prefix lengths, for RoPE) in one upload
+        const int64_t plan_words = (static_cast<int64_t>(plan.total_int32) + 3) & ~int64_t(3);
+        const int64_t pos_words = o_.full_step ? static_cast<int64_t>(running.size()) : 0;
+        const int64_t pw = plan_region(e, plan_words + ((pos_words + 3) & ~int64_t(3)));
         std::memcpy(plan_arena_host_ + pw, plan_scratch_.data(), static_cast<size_t>(plan.total_int32) * 4);
+        for (int64_t i = 0; i < pos_words; ++i) plan_arena_host_[pw + plan_words + i] = seq_[static_cast<size_t>(i)];
         const bool open_window = timed && !window_open_;
         window_open_ = window_open_ || timed;
         const uint32_t launch0 = launches_;
         launches_ += static_cast<uint32_t>(o_.num_layers);
         uint64_t* ts = timed ? ts_slot(slot) : nullptr;
         const int64_t result_bytes = result_host_ ? static_cast<int64_t>(running.size()) * o_.num_q_heads * 256 : 0;
+        if (o_.full_step && static_cast<int64_t>(running.size()) > max_rows_full_)
+            throw std::runtime_error("full_step: batch exceeds the activation buffers");
         // The launch worker enqueues the iteration (so a full compute queue never
         // stalls the decisions that issue future KV moves)
-        launcher_.post([this, e, slot, pw, plan, waits = std::move(waits), open_window, launch0, ts, result_bytes] {
+        const int64_t upload_words = plan_words + pos_words;
+        launcher_.post([this, e, slot, pw, plan, waits = std::move(waits), open_window, launch0, ts, result_bytes,
+                        upload_words] {
             ASV_CUDA(cudaSetDevice(o_.decode_device));
             if (open_window) ASV_CUDA(cudaEventRecord(win_beg_, compute_));
             for (const auto& [lane, v] : waits) flags_.wait(compute_, lane, v);
-            if (asv_plan_upload(plan_arena_host_ + pw, plan_arena_dev_ + pw, plan.total_int32, compute_) != ASV_OK)
+            if (asv_plan_upload(plan_arena_host_ + pw, plan_arena_dev_ + pw, upload_words, compute_) != ASV_OK)
                 throw CudaError(asv_last_error());
             ASV_CUDA(cudaEventRecord(att_beg_[slot], compute_));
             asv_attn_plan pl = plan;
@@ -521,17 +535,22 @@ class GpuExecutor : public prefixsim::EngineObserver {
             args.workspace = ws_;
             args.workspace_bytes = ws_bytes_;
             args.sm_scale = 0.08838834764831845f;
+            const int32_t b = pl.batch;
+            const int32_t* positions = plan_arena_dev_ + pw + ((pl.total_int32 + 3) & ~3);
             for (int l = 0; l < o_.num_layers; ++l) {
+                if (o_.full_step) layer_front(l, b, positions);  // RMSNorm, QKV + RoPE -> q_, k_new_, v_new_
                 args.layer = l;
                 args.launch_index = launch0 + static_cast<uint32_t>(l);
                 args.warp_timestamps = l == 0 ? ts : nullptr;
-                args.pdl = l == 0 ? 0 : o_.pdl;  // layer 0 reads the plan the upload kernel just wrote
+                // layer 0 of attention-only steps reads the plan the upload kernel just wrote
+                args.pdl = (l == 0 && !o_.full_step) ? 0 : o_.pdl;
                 if (asv_decode_attention(&shape_, &args, compute_) != ASV_OK) throw CudaError(asv_last_error());
+                if (o_.full_step) layer_back(l, b);  // O + residual, RMSNorm, gate/up SiLU, down + residual
             }
             ASV_CUDA(cudaEventRecord(att_end_[slot], compute_));
-            if (result_bytes > 0) {  // the step's result (last layer's output) read back to the host
-                ASV_CUDA(sm_copy(static_cast<const int32_t*>(out_), reinterpret_cast<int32_t*>(result_host_),
-                                     result_bytes / 4, compute_));
+            if (result_bytes > 0) {  // the step's result (last layer's output / hidden state) read back
+                ASV_CUDA(sm_copy(static_cast<const int32_t*>(o_.full_step ? h_ : out_),
+                                 reinterpret_cast<int32_t*>(result_host_), result_bytes / 4, compute_));
             }
             flags_.write(compute_, kIter, static_cast<uint32_t>(e + 1));  // executed iterations complete
         }, "iteration");
@@ -547,6 +566,11 @@ class GpuExecutor : public prefixsim::EngineObserver {
             stats_.attn_launches += o_.num_layers;
             // attention (+ merge) per layer, the plan upload, and the e2e result read-back
             stats_.kernel_launches_timed += o_.num_layers * (plan.n_merge > 0 ? 2 : 1) + 1 + (result_bytes > 0 ? 1 : 0);
+            if (o_.full_step) {  // per layer: 2 RMSNorm + 4 linear launches per 256-row chunk
+                const int64_t chunks = (static_cast<int64_t>(running.size()) + 255) / 256;
+                stats_.kernel_launches_timed += o_.num_layers * (2 + 4 * chunks);
+                stats_.weight_bytes += o_.num_layers * weights_bytes_per_layer_;
+            }
             if (first_timed_start_ < 0) first_timed_start_ = rec.start_ms;
             last_timed_end_ms_ = rec.end_ms;
             stats_.bubble_ms_timed += rec.bubble_ms;
@@ -1025,6 +1049,129 @@ class GpuExecutor : public prefixsim::EngineObserver {
         ASV_CUDA(cudaStreamSynchronize(p2p_));
     }
 
+    // ---------------------------------------------------------------- full decode step
+    // Synthetic Llama-style decoder weights (random bf16, fan-in scaled) and the
+    // activation buffers of one decode step; the GEMMs run on tcgen05 (asv_linear).
+    void init_full_step() {
+        hidden_ = o_.num_q_heads * 128;
+        inter_ = o_.intermediate_size > 0        ? o_.intermediate_size
+                 : hidden_ == 4096 ? 11008 : hidden_ == 5120 ? 13824 : ((hidden_ * 8 / 3 + 127) / 128) * 128;
+        if (inter_ % 64 != 0) throw std::invalid_argument("intermediate_size must be a multiple of 64");
+        const int64_t n_qkv = 128LL * (o_.num_q_heads + 2 * o_.num_kv_heads);
+        const int64_t per_layer = n_qkv * hidden_ + int64_t(hidden_) * hidden_ + 2LL * inter_ * hidden_ +
+                                  int64_t(hidden_) * inter_ + 2LL * hidden_;
+        max_rows_full_ = std::min<int64_t>(max_rows_, 4096);
+        const int64_t rows_pad = (max_rows_full_ + 15) / 16 * 16;
+        const int64_t elems = per_layer * o_.num_layers;
+        size_t fr = 0, tot = 0;
+        ASV_CUDA(cudaMemGetInfo(&fr, &tot));
+        const int64_t act = rows_pad * (2LL * hidden_ + inter_) * 2;
+        if (static_cast<double>(elems * 2 + act) > 0.9 * static_cast<double>(fr))
+            throw std::invalid_argument("full_step: decoder weights do not fit next to the KV pool");
+        ASV_CUDA(cudaMalloc(&weights_, static_cast<size_t>(elems) * 2));
+        ASV_CUDA(cudaMalloc(&h_, static_cast<size_t>(rows_pad * hidden_ * 2)));
+        ASV_CUDA(cudaMalloc(&x_, static_cast<size_t>(rows_pad * hidden_ * 2)));
+        ASV_CUDA(cudaMalloc(&act_, static_cast<size_t>(rows_pad * inter_ * 2)));
+        ASV_CUDA(cudaMemset(x_, 0, static_cast<size_t>(rows_pad * hidden_ * 2)));
+        ASV_CUDA(cudaMemset(act_, 0, static_cast<size_t>(rows_pad * inter_ * 2)));
+        weights_bytes_per_layer_ = per_layer * 2;
+        auto* w = static_cast<__nv_bfloat16*>(weights_);
+        for (int l = 0; l < o_.num_layers; ++l) {
+            LayerW lw;
+            lw.qkv = w;
+            w += n_qkv * hidden_;
+            lw.o = w;
+            w += int64_t(hidden_) * hidden_;
+            lw.gate_up = w;  // tile t: 64 gate rows then the 64 up rows of outputs 64t..64t+63
+            w += 2LL * inter_ * hidden_;
+            lw.down = w;
+            w += int64_t(hidden_) * inter_;
+            lw.g1 = w;
+            w += hidden_;
+            lw.g2 = w;
+            w += hidden_;
+            const uint64_t sd = 1000 + 16 * static_cast<uint64_t>(l);
+            ASV_CUDA(fill_random_bf16(lw.qkv, n_qkv * hidden_, sd, 1.f / std::sqrt(float(hidden_)), 0.f, compute_));
+            ASV_CUDA(fill_random_bf16(lw.o, int64_t(hidden_) * hidden_, sd + 1, 1.f / std::sqrt(float(hidden_)), 0.f,
+                                      compute_));
+            ASV_CUDA(fill_random_bf16(lw.gate_up, 2LL * inter_ * hidden_, sd + 2, 1.f / std::sqrt(float(hidden_)), 0.f,
+                                      compute_));
+            ASV_CUDA(fill_random_bf16(lw.down, int64_t(hidden_) * inter_, sd + 3, 1.f / std::sqrt(float(inter_)), 0.f,
+                                      compute_));
+            ASV_CUDA(fill_random_bf16(lw.g1, hidden_, sd + 4, 0.1f, 1.f, compute_));
+            ASV_CUDA(fill_random_bf16(lw.g2, hidden_, sd + 5, 0.1f, 1.f, compute_));
+            layers_.push_back(lw);
+        }
+        ASV_CUDA(fill_random_bf16(h_, rows_pad * hidden_, 7, 1.f, 0.f, compute_));
+        ASV_CUDA(cudaStreamSynchronize(compute_));
+        if (linear_preload() != cudaSuccess || rmsnorm_preload() != cudaSuccess)
+            throw CudaError("full_step: kernel preload failed");
+    }
+
+    asv_linear_args lin(const void* w, int32_t n_out, int32_t k, const void* x, int32_t batch, void* y, int32_t y_ld,
+                        int32_t epi) const {
+        asv_linear_args a{};
+        a.w = w;
+        a.n_out = n_out;
+        a.k = k;
+        a.x = x;
+        a.x_rows = (batch + 15) / 16 * 16;
+        a.batch = batch;
+        a.y = y;
+        a.y_ld = y_ld;
+        a.epilogue = epi;
+        a.pdl = o_.pdl;
+        return a;
+    }
+    // GEMMs take <= 256 batch rows per launch
+    template <typename F>
+    static void row_chunks(int32_t b, F&& f) {
+        for (int32_t r0 = 0; r0 < b; r0 += 256) f(r0, std::min<int32_t>(256, b - r0));
+    }
+    void layer_front(int l, int32_t b, const int32_t* positions) {
+        const LayerW& lw = layers_[static_cast<size_t>(l)];
+        const int32_t rows = (b + 15) / 16 * 16;
+        if (asv_rmsnorm(h_, lw.g1, x_, hidden_, b, rows, 1e-5f, o_.pdl, compute_) != ASV_OK)
+            throw CudaError(asv_last_error());
+        row_chunks(b, [&](int32_t r0, int32_t n) {
+            asv_linear_args a = lin(lw.qkv, 128 * (o_.num_q_heads + 2 * o_.num_kv_heads), hidden_,
+                                    static_cast<const __nv_bfloat16*>(x_) + int64_t(r0) * hidden_, n, nullptr, 0,
+                                    ASV_EPI_QKV_ROPE);
+            a.positions = positions + r0;
+            a.rope_theta = 10000.f;
+            a.q = static_cast<__nv_bfloat16*>(q_) + int64_t(r0) * o_.num_q_heads * 128;
+            a.k_out = static_cast<__nv_bfloat16*>(k_new_) + int64_t(r0) * o_.num_kv_heads * 128;
+            a.v_out = static_cast<__nv_bfloat16*>(v_new_) + int64_t(r0) * o_.num_kv_heads * 128;
+            a.n_q_heads = o_.num_q_heads;
+            a.n_kv_heads = o_.num_kv_heads;
+            if (asv_linear(&a, compute_) != ASV_OK) throw CudaError(asv_last_error());
+        });
+    }
+    void layer_back(int l, int32_t b) {
+        const LayerW& lw = layers_[static_cast<size_t>(l)];
+        const int32_t rows = (b + 15) / 16 * 16;
+        auto* h = static_cast<__nv_bfloat16*>(h_);
+        row_chunks(b, [&](int32_t r0, int32_t n) {  // h += attn_out . Wo^T
+            asv_linear_args a = lin(lw.o, hidden_, hidden_, static_cast<const __nv_bfloat16*>(out_) + int64_t(r0) * hidden_,
+                                    n, h + int64_t(r0) * hidden_, hidden_, ASV_EPI_RESIDUAL);
+            if (asv_linear(&a, compute_) != ASV_OK) throw CudaError(asv_last_error());
+        });
+        if (asv_rmsnorm(h_, lw.g2, x_, hidden_, b, rows, 1e-5f, o_.pdl, compute_) != ASV_OK)
+            throw CudaError(asv_last_error());
+        auto* act = static_cast<__nv_bfloat16*>(act_);
+        row_chunks(b, [&](int32_t r0, int32_t n) {  // act = silu(x Wg^T) * (x Wu^T)
+            asv_linear_args a = lin(lw.gate_up, 2 * inter_, hidden_,
+                                    static_cast<const __nv_bfloat16*>(x_) + int64_t(r0) * hidden_, n,
+                                    act + int64_t(r0) * inter_, inter_, ASV_EPI_SILU_MUL);
+            if (asv_linear(&a, compute_) != ASV_OK) throw CudaError(asv_last_error());
+        });
+        row_chunks(b, [&](int32_t r0, int32_t n) {  // h += act . Wd^T
+            asv_linear_args a = lin(lw.down, hidden_, inter_, act + int64_t(r0) * inter_, n,
+                                    h + int64_t(r0) * hidden_, hidden_, ASV_EPI_RESIDUAL);
+            if (asv_linear(&a, compute_) != ASV_OK) throw CudaError(asv_last_error());
+        });
+    }
+
     uint64_t* ts_slot(size_t slot) const { return ts_arena_ + slot * static_cast<size_t>(workers_) * 2; }
 
     // retire every executed iteration up to and including `e`, in order
@@ -1135,6 +1282,14 @@ class GpuExecutor : public prefixsim::EngineObserver {
     int32_t workers_ = 0;
     int64_t max_rows_ = 0;
     char* result_host_ = nullptr;           // mapped pinned: per-iteration result read-back (e2e)
+    // full decode step (o_.full_step)
+    struct LayerW {
+        __nv_bfloat16 *qkv = nullptr, *o = nullptr, *gate_up = nullptr, *down = nullptr, *g1 = nullptr, *g2 = nullptr;
+    };
+    std::vector<LayerW> layers_;
+    void *weights_ = nullptr, *h_ = nullptr, *x_ = nullptr, *act_ = nullptr;
+    int32_t hidden_ = 0, inter_ = 0;
+    int64_t max_rows_full_ = 0, weights_bytes_per_layer_ = 0;
     void *q_ = nullptr, *out_ = nullptr, *k_new_ = nullptr, *v_new_ = nullptr, *ws_ = nullptr;
     size_t ws_bytes_ = 0;
     int32_t ws_splits_ = 0;

@@ -78,7 +78,7 @@ def engine_run(config, *, device: int = 0, prefetch_device: int | None = None,
                exec_begin: int = 0, exec_end: int = -1, timed_begin: int = 0, copy_begin: int | None = None,
                host_pool_bytes: int = 8 << 30, shard_index: int = 0, shard_count: int = 1,
                pdl: bool = True, run_ahead: int = 256, policy: str | None = None,
-               pair_mode: bool = False) -> dict:
+               pair_mode: bool = False, full_step: bool = False, intermediate_size: int = 0) -> dict:
     """Run the decode engine on the GPU (asv_engine_run): reference decisions executed for real."""
     text = config if isinstance(config, str) else json.dumps(config)
     o = _lib.EngineOpts()
@@ -93,6 +93,8 @@ def engine_run(config, *, device: int = 0, prefetch_device: int | None = None,
     o.pdl = 1 if pdl else 0
     o.run_ahead = run_ahead
     o.pair_mode = 1 if pair_mode else 0
+    o.full_step = 1 if full_step else 0
+    o.intermediate_size = intermediate_size
     st = _lib.EngineStats()
     _lib.check(_lib.lib().asv_engine_run(text.encode(), policy.encode() if policy else None,
                                           C.byref(o), C.byref(st)))

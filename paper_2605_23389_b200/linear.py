@@ -15,30 +15,15 @@ from . import _lib
 
 STORE, RESIDUAL, SILU_MUL, QKV_ROPE = _lib.EPI_STORE, _lib.EPI_RESIDUAL, _lib.EPI_SILU_MUL, _lib.EPI_QKV_ROPE
 
-_ws: dict = {}
-
-
-def workspace(n_out: int, k: int, max_batch: int, device: torch.device) -> torch.Tensor:
-    """Zero-filled split-K workspace (its tile counters self-reset after every call)."""
-    idx = device.index or 0
-    need = int(_lib.lib().asv_linear_workspace_bytes(n_out, k, max_batch, idx))
-    key = idx
-    cur = _ws.get(key)
-    if cur is None or cur.numel() < need:
-        cur = torch.zeros(max(need, 1 << 20), dtype=torch.uint8, device=device)
-        _ws[key] = cur
-    return cur
-
 
 def linear(x: torch.Tensor, w: torch.Tensor, batch: int, y: torch.Tensor | None = None,
            epilogue: int = STORE, positions: torch.Tensor | None = None, rope_theta: float = 10000.0,
            q: torch.Tensor | None = None, k_out: torch.Tensor | None = None, v_out: torch.Tensor | None = None,
-           n_q_heads: int = 0, n_kv_heads: int = 0, stream=None) -> torch.Tensor | None:
+           n_q_heads: int = 0, n_kv_heads: int = 0, pdl: bool = False, stream=None) -> torch.Tensor | None:
     """y[:batch] = epilogue(x[:batch] @ w.T) on tcgen05 (x has >= batch rounded up to 16 rows)."""
     if x.dtype != torch.bfloat16 or w.dtype != torch.bfloat16:
         raise TypeError("x and w must be bfloat16")
     n_out, k = w.shape
-    ws = workspace(n_out, k, batch, x.device)
     a = _lib.LinearArgs()
     a.w, a.n_out, a.k = w.data_ptr(), n_out, k
     a.x, a.x_rows, a.batch = x.data_ptr(), x.shape[0], batch
@@ -51,15 +36,15 @@ def linear(x: torch.Tensor, w: torch.Tensor, batch: int, y: torch.Tensor | None 
     a.k_out = k_out.data_ptr() if k_out is not None else None
     a.v_out = v_out.data_ptr() if v_out is not None else None
     a.n_q_heads, a.n_kv_heads = n_q_heads, n_kv_heads
-    a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
+    a.pdl = 1 if pdl else 0
     st = (stream or torch.cuda.current_stream(x.device)).cuda_stream
     _lib.check(_lib.lib().asv_linear(C.byref(a), C.c_void_p(st)))
     return y
 
 
 def rmsnorm(h: torch.Tensor, gamma: torch.Tensor, out: torch.Tensor, batch: int, eps: float = 1e-5,
-            stream=None) -> torch.Tensor:
+            pdl: bool = False, stream=None) -> torch.Tensor:
     st = (stream or torch.cuda.current_stream(h.device)).cuda_stream
     _lib.check(_lib.lib().asv_rmsnorm(h.data_ptr(), gamma.data_ptr(), out.data_ptr(), h.shape[-1], batch,
-                                      out.shape[0], C.c_float(eps), C.c_void_p(st)))
+                                      out.shape[0], C.c_float(eps), 1 if pdl else 0, C.c_void_p(st)))
     return out

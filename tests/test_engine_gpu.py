@@ -64,3 +64,19 @@ def test_mismatched_shape_is_rejected():
     with pytest.raises(ValueError, match="kv_bytes_per_token"):
         engine.engine_run(GOLDEN["configs"]["smoke"], device=0, num_q_heads=32, num_kv_heads=8, num_layers=32,
                           execute_transfers=False)
+
+
+def test_full_decode_step_runs_and_is_deterministic():
+    """full_step: every executed iteration runs the whole decoder layer stack (tcgen05 GEMMs +
+    attention); decisions and bytes moved are unchanged, and the run is deterministic."""
+    from paper_2605_23389_b200 import engine
+    cfg = GOLDEN["configs"]["smoke"]
+    kw = dict(device=0, num_q_heads=32, num_kv_heads=32, num_layers=32, execute_transfers=True, exec_begin=0,
+              exec_end=-1, timed_begin=0, copy_begin=0, host_pool_bytes=1 << 30, full_step=True)
+    a = engine.engine_run(cfg, **kw)
+    b = engine.engine_run(cfg, **kw)
+    want = _expect("smoke:aligned")
+    for k, v in want.items():
+        assert a["logical_bytes"][k] == v, k
+    assert a["iterations_timed"] == b["iterations_timed"] == GOLDEN["logs"]["smoke:aligned"]["iterations"]
+    assert a["window_ms"] > 0 and a["kernel_launches_timed"] > b["iterations_timed"] * 32 * 7

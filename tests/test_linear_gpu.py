@@ -135,3 +135,39 @@ def test_bad_arguments_fail_loudly():
     w = _rand((100, 128), 2)  # n_out not a multiple of 128
     with pytest.raises(ValueError, match="multiple of 128"):
         L.linear(x, w, 4, torch.empty(4, 100, dtype=torch.bfloat16, device="cuda"))
+
+
+def test_pdl_chain_matches_torch():
+    """rmsnorm -> o_proj-like residual GEMM -> rmsnorm -> gate/up SiLU GEMM -> down residual GEMM, all
+    launched with programmatic dependent launch back to back (weights prefetched before each wait)."""
+    from paper_2605_23389_b200 import linear as L
+    batch, d, inter = 6, 4096, 11008
+    h0 = _rand((batch, d), 21)
+    g1, g2 = _rand((d,), 22), _rand((d,), 23)
+    wo = _rand((d, d), 24, 1 / math.sqrt(d))
+    wgu = _rand((2 * inter, d), 25, 1 / math.sqrt(d))
+    wd = _rand((d, inter), 26, 1 / math.sqrt(inter))
+    h = h0.clone()
+    x = torch.zeros(16, d, dtype=torch.bfloat16, device="cuda")
+    act = torch.zeros(16, inter, dtype=torch.bfloat16, device="cuda")
+    for _ in range(3):  # repeated: every launch overlaps the previous one's tail
+        h.copy_(h0)
+        L.rmsnorm(h, g1, x, batch, 1e-5, pdl=True)
+        L.linear(x, wo, batch, h, L.RESIDUAL, pdl=True)
+        L.rmsnorm(h, g2, x, batch, 1e-5, pdl=True)
+        L.linear(x, wgu, batch, act, L.SILU_MUL, pdl=True)
+        L.linear(act, wd, batch, h, L.RESIDUAL, pdl=True)
+    torch.cuda.synchronize()
+
+    def rms(t, g):
+        t = t.float()
+        return (t * torch.rsqrt(t.pow(2).mean(-1, keepdim=True) + 1e-5) * g.float()).bfloat16().float()
+
+    r = h0.float()
+    r = (r + rms(r.bfloat16(), g1) @ wo.float().T).bfloat16().float()
+    xg = rms(r.bfloat16(), g2)
+    gu = xg @ wgu.float().T
+    gg, uu = gu.view(batch, -1, 2, 64)[:, :, 0].reshape(batch, -1), gu.view(batch, -1, 2, 64)[:, :, 1].reshape(batch, -1)
+    a = (torch.nn.functional.silu(gg) * uu).bfloat16().float()
+    r = r + a @ wd.float().T
+    _check(h, r, "pdl chain")
