@@ -402,59 +402,16 @@ cudaError_t launch_epi(const CUtensorMap& tw, const CUtensorMap& tx, const Linea
 
 }  // namespace
 
-// CTAs per SM at this batch (shared memory of the ring / accumulator staging)
-int ctas_per_sm(int bn) {
-    const int per = smem_bytes(bn) + 1024;
-    const int n = 232448 / per;
-    return n < 1 ? 1 : n > 2 ? 2 : n;
-}
-
-// Clusters of `splits` CTAs (at batch tile bn) the device holds at once.
-int active_clusters(int bn, int splits) {
-    static std::mutex mu;
-    static int cache[17][kMaxSplits + 1] = {};
-    std::lock_guard<std::mutex> lk(mu);
-    int& c = cache[bn / 16][splits];
-    if (c == 0) {
-        // every epilogue instantiation has the same resources: query one
-        static bool configured = false;
-        if (!configured) {
-            cudaFuncSetAttribute(linear_kernel<ASV_EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 smem_bytes(256));
-            cudaFuncSetAttribute(linear_kernel<ASV_EPI_STORE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
-            configured = true;
-        }
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(splits * 64);
-        cfg.blockDim = dim3(128);
-        cfg.dynamicSmemBytes = smem_bytes(bn);
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = splits;
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        int n = 0;
-        if (cudaOccupancyMaxActiveClusters(&n, linear_kernel<ASV_EPI_STORE>, &cfg) != cudaSuccess || n < 1) {
-            cudaGetLastError();
-            n = 148 * ctas_per_sm(bn) / splits;
-        }
-        c = n;
-    }
-    return c;
-}
-
-// K splits per tile: the most splits (<= kMaxSplits = one portable cluster, each
-// >= 2 K blocks, none empty) whose tiles x clusters still run in ONE wave
-// (measured: a second partial wave of short CTAs costs more than it saves).
-int linear_splits(int n_out, int k, int bn) {
+// K splits per tile: the largest power of two (<= kMaxSplits = one portable
+// cluster, every split >= 2 K blocks, none empty) with tiles x splits <= 2 CTAs
+// per SM.  Measured on B200 at batch 16 (us, splits 1/2/3/4/8): qkv 25/21/30/26/27,
+// o 24/16/14/12/12, gate_up 34/41/36/40/46, down 55/31/24/21/18 — a second
+// partial wave of short CTAs, or odd cluster sizes, cost more than they save.
+int linear_splits(int n_out, int k, int sms) {
     const int tiles = n_out / kBM, kbs = k / kBK;
-    int best = 1;
-    for (int sp = 2; sp <= kMaxSplits && sp <= kbs / 2; ++sp) {
-        if (tiles <= active_clusters(bn, sp)) best = sp;
-    }
-    const int per = (kbs + best - 1) / best;
+    int sp = 1;
+    while (sp * 2 <= kMaxSplits && sp * 2 <= kbs / 2 && tiles * sp * 2 <= 2 * sms) sp *= 2;
+    const int per = (kbs + sp - 1) / sp;
     return (kbs + per - 1) / per;
 }
 
@@ -485,7 +442,7 @@ static int linear_run(const asv_linear_args* a, cudaStream_t st) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int tiles = a->n_out / kBM, kbs = a->k / kBK;
-    int splits = linear_splits(a->n_out, a->k, bn);
+    int splits = linear_splits(a->n_out, a->k, sms);
     if (const char* e = getenv("ASV_LINEAR_SPLITS")) {  // tuning experiments only
         const int kbs_ = a->k / kBK, want = atoi(e);
         if (want >= 1 && want <= kMaxSplits && want <= kbs_) {
@@ -531,8 +488,11 @@ static int linear_run(const asv_linear_args* a, cudaStream_t st) {
 // ------------------------------------------------------------------ RMSNorm
 // out[b][:] = h[b][:] * rsqrt(mean(h^2) + eps) * gamma, rows [batch, rows_out) zeroed
 // (they are the MMA-N padding of the next linear layer's activation tile)
-__global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ h, const __nv_bfloat16* __restrict__ gamma,
-                               __nv_bfloat16* __restrict__ out, int dim, int batch, float eps) {
+__global__ void __launch_bounds__(256) rmsnorm_kernel(const __nv_bfloat16* __restrict__ h,
+                                                      const __nv_bfloat16* __restrict__ gamma,
+                                                      __nv_bfloat16* __restrict__ out, int dim, int batch, float eps) {
+    // one row per CTA, one pass: every thread keeps its <= 4 x 8 values in registers
+    constexpr int kVec = 4;
     grid_dep_wait();  // h is the previous kernel's output (no-op without PDL)
     grid_dep_launch();
     const int b = blockIdx.x;
@@ -542,14 +502,20 @@ __global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ h, const __nv_b
         return;
     }
     const __nv_bfloat16* x = h + static_cast<int64_t>(b) * dim;
+    uint4 u[kVec], g[kVec];
     float ss = 0.f;
-    for (int i = threadIdx.x * 8; i < dim; i += blockDim.x * 8) {
-        const uint4 u = *reinterpret_cast<const uint4*>(x + i);
-        const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&u);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const float f = __bfloat162float(e[j]);
-            ss += f * f;
+    for (int j = 0; j < kVec; ++j) {
+        const int i = (threadIdx.x + j * blockDim.x) * 8;
+        if (i < dim) {
+            u[j] = *reinterpret_cast<const uint4*>(x + i);
+            g[j] = __ldg(reinterpret_cast<const uint4*>(gamma + i));
+            const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&u[j]);
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const float f = __bfloat162float(e[t]);
+                ss += f * f;
+            }
         }
     }
     __shared__ float red[32];
@@ -563,16 +529,18 @@ __global__ void rmsnorm_kernel(const __nv_bfloat16* __restrict__ h, const __nv_b
     }
     __syncthreads();
     const float inv = rsqrtf(red[0] / dim + eps);
-    for (int i = threadIdx.x * 8; i < dim; i += blockDim.x * 8) {
-        const uint4 u = *reinterpret_cast<const uint4*>(x + i);
-        const uint4 g = *reinterpret_cast<const uint4*>(gamma + i);
-        const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&u);
-        const __nv_bfloat16* ge = reinterpret_cast<const __nv_bfloat16*>(&g);
-        uint4 r;
-        __nv_bfloat16* re = reinterpret_cast<__nv_bfloat16*>(&r);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) re[j] = __float2bfloat16(__bfloat162float(e[j]) * inv * __bfloat162float(ge[j]));
-        *reinterpret_cast<uint4*>(o + i) = r;
+    for (int j = 0; j < kVec; ++j) {
+        const int i = (threadIdx.x + j * blockDim.x) * 8;
+        if (i < dim) {
+            const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&u[j]);
+            const __nv_bfloat16* ge = reinterpret_cast<const __nv_bfloat16*>(&g[j]);
+            uint4 r;
+            __nv_bfloat16* re = reinterpret_cast<__nv_bfloat16*>(&r);
+#pragma unroll
+            for (int t = 0; t < 8; ++t) re[t] = __float2bfloat16(__bfloat162float(e[t]) * inv * __bfloat162float(ge[t]));
+            *reinterpret_cast<uint4*>(o + i) = r;
+        }
     }
 }
 
@@ -627,8 +595,8 @@ int asv_linear(const asv_linear_args* args, void* stream) {
 
 int asv_rmsnorm(const void* h, const void* gamma, void* out, int32_t dim, int32_t batch, int32_t rows_out, float eps,
                 int32_t pdl, void* stream) {
-    if (h == nullptr || gamma == nullptr || out == nullptr || dim <= 0 || dim % 8 != 0 || batch < 1 ||
-        rows_out < batch)
+    if (h == nullptr || gamma == nullptr || out == nullptr || dim <= 0 || dim % 8 != 0 || dim > 256 * 8 * 4 ||
+        batch < 1 || rows_out < batch)
         return asv::fail(ASV_ERR_INVALID, "rmsnorm: bad arguments");
     cudaError_t e =
         asv::rmsnorm_launch(h, gamma, out, dim, batch, rows_out, eps, pdl != 0, static_cast<cudaStream_t>(stream));
