@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--e2e", action="store_true")
+    ap.add_argument("--full", action="store_true", help="also run the full decoder-layer step (tcgen05 GEMMs)")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     from paper_2605_23389_b200 import engine as E
@@ -37,12 +38,17 @@ def main():
         cfg = E.load_config(os.path.join(ROOT, "configs", name + ".json"))
         at = cfg["b200"]
         row = {"config": name, "policy": pol or "aligned", "start": start, "pair_mode": pair}
-        for mode in (["value", "e2e"] if a.e2e else ["value"]):
-            st = E.engine_run(cfg, policy=pol, device=0, num_q_heads=at["num_q_heads"],
-                              num_kv_heads=at["num_kv_heads"], num_layers=at["num_layers"],
-                              execute_transfers=(mode == "e2e"), exec_begin=start, timed_begin=start + a.warmup,
-                              exec_end=start + a.warmup + a.steps, copy_begin=max(0, start - 400),
-                              host_pool_bytes=2 << 30, pair_mode=pair)
+        modes = ["value"] + (["e2e"] if a.e2e else []) + (["full_step"] if a.full else [])
+        for mode in modes:
+            try:
+                    st = E.engine_run(cfg, policy=pol, device=0, num_q_heads=at["num_q_heads"],
+                                  num_kv_heads=at["num_kv_heads"], num_layers=at["num_layers"],
+                                  execute_transfers=(mode == "e2e"), exec_begin=start, timed_begin=start + a.warmup,
+                                  exec_end=start + a.warmup + a.steps, copy_begin=max(0, start - 400),
+                                  host_pool_bytes=2 << 30, pair_mode=pair, full_step=(mode == "full_step"))
+            except ValueError as exc:  # e.g. full_step weights next to a pool sized for KV alone
+                row[mode] = {"skipped": str(exc)}
+                continue
             it = max(1, st["iterations_timed"])
             row[mode] = {"tok_s": st["tokens_timed"] / (st["window_ms"] / 1e3) if st["window_ms"] > 0 else 0,
                          "ms_per_step": st["window_ms"] / it, "mean_batch": st["tokens_timed"] / it,
@@ -52,6 +58,10 @@ def main():
                          "virtual_bubble_ms_per_step": st["bubble_ms_timed"] / it,
                          "virtual_tok_s_whole_run": st["virtual_decode_tok_s"],
                          "h2d_gb": st["h2d_bytes_window"] / 1e9, "p2p_gb": st["p2p_bytes_window"] / 1e9}
+            if mode == "full_step":
+                row[mode]["hbm_gbps"] = ((st["attn_bytes"] + st["weight_bytes"]) / (st["window_ms"] * 1e-3) / 1e9
+                                         if st["window_ms"] > 0 else 0)
+                row[mode]["weight_gb_per_step"] = st["weight_bytes"] / it / 1e9
         print(json.dumps(row), flush=True)
         results.append(row)
     if a.out:
