@@ -357,7 +357,11 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, ui
 }
 
 int stages_for(int bn) {
-    const int st = kSmemBudget / (kABytes + bn * 128);
+    static const int budget = [] {  // ASV_LINEAR_SMEM_KB: tuning experiments only
+        const char* e = getenv("ASV_LINEAR_SMEM_KB");
+        return e != nullptr ? atoi(e) * 1024 : kSmemBudget;
+    }();
+    const int st = budget / (kABytes + bn * 128);
     return st < 2 ? 2 : st > kMaxStages ? kMaxStages : st;
 }
 // the epilogue reuses the ring for the [bn][128] fp32 accumulator tile
