@@ -673,6 +673,7 @@ decode_attn_kernel(const Params p) {
             if (have_cur) {
                 issue(slot);
                 ++issued;
+                __syncwarp();  // lane 0 may just have pushed the next item's descriptor into the ring
             }
             if (!qn_ready && citem < pushed) {  // prefetch the next item's q
                 qn.load(p, ring[citem % kRing], lane);

@@ -24,10 +24,16 @@ def run(n_q, n_kv, L, seq_lens, iters=20, warmup=3, num_workers=None, seed=0):
     att = PagedDecodeAttention(n_q, n_kv, L, device=0)
     npages = [(s + 16) // 16 for s in seq_lens]
     P = sum(npages)
-    pool = torch.empty(P * att.page_bytes // 2, dtype=torch.bfloat16, device=dev)
+    # grouped layer-major pool: page ids must stay below asv_pool_usable_pages (include/asv.h)
+    import ctypes as C
+    from paper_2605_23389_b200 import _lib
+    pool_pages = P + 8
+    usable = int(_lib.lib().asv_pool_usable_pages(C.byref(att.shape), pool_pages))
+    assert usable >= P
+    pool = torch.empty(pool_pages * att.page_bytes // 2, dtype=torch.bfloat16, device=dev)
     pool.uniform_(-1, 1)
     rng = np.random.default_rng(seed)
-    perm = rng.permutation(P).astype(np.int32)
+    perm = rng.permutation(usable)[:P].astype(np.int32)
     indptr = np.concatenate([[0], np.cumsum(npages)]).astype(np.int32)
     b = len(seq_lens)
     q = torch.randn(b, n_q, 128, device=dev, dtype=torch.bfloat16)
