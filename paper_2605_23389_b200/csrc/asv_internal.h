@@ -49,6 +49,7 @@ struct AttnLaunch {
     int64_t v_off;
     int32_t group_pages;    // pages per layer-major group (pool_group_pages)
     int32_t group_skip;     // group_pages * (L - 1): pool_slot(p) = p + (p / group_pages) * group_skip
+    int32_t usable_pages;   // page ids must be < this (the kernel traps otherwise)
     const int32_t* gdesc;
     const int32_t* split_base;
     int32_t num_items;

@@ -310,6 +310,7 @@ int asv_decode_attention(const asv_attn_shape* shape, const asv_attn_args* a, vo
     const int64_t gp = pool_group_pages(L.page_bytes, a->pool_pages);
     L.group_pages = static_cast<int32_t>(gp);
     L.group_skip = static_cast<int32_t>(gp * (shape->num_layers - 1));
+    L.usable_pages = static_cast<int32_t>(pool_usable_pages(L.page_bytes, a->pool_pages));
     L.layer_off = static_cast<int64_t>(a->layer) * gp * L.page_bytes;
     L.v_off = static_cast<int64_t>(n_kv) * kBlockBytes;
     L.gdesc = a->plan_dev + pl.off_desc;

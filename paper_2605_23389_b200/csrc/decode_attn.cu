@@ -56,6 +56,7 @@ struct Params {
     int64_t v_off;
     int32_t group_pages;        // layer-major page groups (asv_internal.h pool_slot)
     int32_t group_skip;
+    int32_t usable_pages;       // valid page ids: [0, usable_pages)
     const int32_t* gdesc;       // [G][kDescWords]
     const int32_t* split_base;  // [b+1]
     int32_t num_items;
@@ -223,6 +224,11 @@ __device__ __forceinline__ void load_desc(const Params& p, uint32_t k, int lane,
     const int4 a = __ldg(reinterpret_cast<const int4*>(gd));
     const int4 b = __ldg(reinterpret_cast<const int4*>(gd) + 1);
     phys = __ldg(gd + 8 + lane);
+    // a page id outside the pool would make the fused KV append write outside it: fail loudly
+    if ((lane < a.w - a.z && static_cast<uint32_t>(phys) >= static_cast<uint32_t>(p.usable_pages)) ||
+        b.z >= p.usable_pages) {
+        __trap();
+    }
     phys += (phys / p.group_pages) * p.group_skip;  // page id -> slice index in the grouped pool
     d.r = a.x;
     d.slot = a.y;
@@ -958,6 +964,7 @@ cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st) {
     p.v_off = a.v_off;
     p.group_pages = a.group_pages;
     p.group_skip = a.group_skip;
+    p.usable_pages = a.usable_pages;
     p.gdesc = a.gdesc;
     p.split_base = a.split_base;
     p.num_items = a.num_items;

@@ -187,3 +187,30 @@ def test_pdl_chain_of_layers_matches_oracle(oracle, n_q, n_kv):
         ref, _ = oracle.attention(n_q, n_kv, L, layer, qs[layer], pool, seq, indptr, indices, att.sm_scale)
         got = outs[layer].float().cpu().numpy()
         assert (np.abs(got - ref) <= ATOL + RTOL * np.abs(ref)).all(), f"layer {layer}"
+
+
+def test_page_id_outside_the_pool_fails_loudly():
+    """A page id >= the pool's usable pages traps the kernel (it would otherwise append KV
+    outside the pool); run in a subprocess because a trap poisons the CUDA context."""
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
+from paper_2605_23389_b200 import PagedDecodeAttention
+att = PagedDecodeAttention(32, 32, 1, device=0)
+pool = torch.zeros(8 * att.page_bytes, dtype=torch.uint8, device="cuda")
+seq = [40]
+indptr = np.array([0, 3], np.int32)
+indices = np.array([0, 1, 8], np.int32)   # 8 >= 8 pages in the pool
+q = torch.zeros(1, 32, 128, dtype=torch.bfloat16, device="cuda")
+out = torch.empty_like(q)
+kn = torch.zeros(1, 32, 128, dtype=torch.bfloat16, device="cuda")
+att.run(q, pool, 0, att.plan(seq, indptr, indices), out, k_new=kn, v_new=kn)
+torch.cuda.synchronize()
+print("NO ERROR")
+'''
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code, root], capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0 and "NO ERROR" not in r.stdout, r.stdout + r.stderr
