@@ -33,6 +33,10 @@ extern "C" {
 
 const char* asv_last_error(void);
 int asv_abi_version(void);
+/* sizeof() of a boundary struct by name ("asv_attn_shape", "asv_attn_plan", "asv_attn_args",
+ * "asv_linear_args", "asv_engine_opts", "asv_engine_stats"); -1 for an unknown name.  Lets a
+ * binding (ctypes / cgo / N-API) check its struct mirrors against the compiled library. */
+int64_t asv_struct_size(const char* name);
 
 /* ------------------------------------------------------------------------ */
 /* Paged KV layout.  A page holds 16 tokens (= ClusterConfig::block_size,     */
@@ -264,6 +268,12 @@ typedef struct asv_engine_opts {
                                    residual) with synthetic weights, not attention alone */
     int32_t intermediate_size;  /* MLP width for full_step (0: 11008 for hidden 4096, 13824 for 5120,
                                    else 8/3 hidden rounded up to 128) */
+    int32_t execute_prefill_offload; /* 1 (with execute_transfers): every prefill_offload transfer
+                                   (cluster_sim.hpp:285-299) is a real D2H copy of the request's
+                                   s x kv_bytes_per_token bytes from the prefill GPU (= the prefetch
+                                   device) into its host-pool pages, on its own PCIe stream; a later
+                                   host->GPU fetch of the request waits for it (pool_insert happens
+                                   at transfer completion).  Prefill compute itself stays virtual. */
 } asv_engine_opts;
 
 /* transfer kinds for the per-kind byte counters */
@@ -312,6 +322,9 @@ typedef struct asv_engine_stats {
     int64_t result_d2h_bytes_window; /* e2e: each iteration's attention output [b][n_h][128] bf16 read back
                                         to pinned host memory (SM stores, no copy-engine queue) */
     int64_t weight_bytes;         /* full_step: decoder weight bytes streamed inside the window */
+    int64_t offload_bytes;        /* prefill_offload D2H bytes executed (== logical prefill_offload bytes
+                                     of the executed span) */
+    int64_t offload_bytes_window; /* the same restricted to the timed window */
 } asv_engine_stats;
 
 int asv_engine_run(const char* config_json, const char* policy_override, const asv_engine_opts* opts,

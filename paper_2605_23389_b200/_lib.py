@@ -107,6 +107,7 @@ class EngineOpts(C.Structure):
         ("pair_mode", C.c_int32),
         ("full_step", C.c_int32),
         ("intermediate_size", C.c_int32),
+        ("execute_prefill_offload", C.c_int32),
     ]
 
 
@@ -147,6 +148,8 @@ class EngineStats(C.Structure):
         ("hazard_waits", C.c_int64),
         ("result_d2h_bytes_window", C.c_int64),
         ("weight_bytes", C.c_int64),
+        ("offload_bytes", C.c_int64),
+        ("offload_bytes_window", C.c_int64),
     ]
 
     def as_dict(self):
@@ -163,6 +166,7 @@ class EngineStats(C.Structure):
 SIGNATURES = [
     ("asv_last_error", C.c_char_p, []),
     ("asv_abi_version", C.c_int, []),
+    ("asv_struct_size", C.c_int64, [C.c_char_p]),
     ("asv_free", None, [C.c_void_p]),
     ("asv_page_bytes", C.c_int64, [C.POINTER(AttnShape)]),
     ("asv_page_offset", C.c_int64,

@@ -63,6 +63,18 @@ extern "C" {
 
 const char* asv_last_error(void) { return g_last_error.c_str(); }
 int asv_abi_version(void) { return 1; }
+
+int64_t asv_struct_size(const char* name) {
+    if (name == nullptr) return -1;
+    const std::string n(name);
+    if (n == "asv_attn_shape") return static_cast<int64_t>(sizeof(asv_attn_shape));
+    if (n == "asv_attn_plan") return static_cast<int64_t>(sizeof(asv_attn_plan));
+    if (n == "asv_attn_args") return static_cast<int64_t>(sizeof(asv_attn_args));
+    if (n == "asv_linear_args") return static_cast<int64_t>(sizeof(asv_linear_args));
+    if (n == "asv_engine_opts") return static_cast<int64_t>(sizeof(asv_engine_opts));
+    if (n == "asv_engine_stats") return static_cast<int64_t>(sizeof(asv_engine_stats));
+    return -1;
+}
 void asv_free(void* p) { std::free(p); }
 
 int64_t asv_page_bytes(const asv_attn_shape* s) {

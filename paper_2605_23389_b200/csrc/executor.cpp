@@ -10,6 +10,9 @@
 //   * admit / evict (NVLink, :517, :551) -> P2P copies between the prefetch and
 //     the decode GPU of a pair, or a zero-copy ownership change on one GPU;
 //   * spill / flush (PCIe, :529, :541) -> D2H copies back to the host pool;
+//   * prefill_offload (PCIe, :285-299) -> D2H copy of the prefilled KV from the
+//     prefill GPU into the request's host-pool pages (prefill compute itself is
+//     virtual: the source is a resident prefill-output page ring);
 //   * every iteration (:476-496) -> CSR page table in SchedulerState::running
 //     order, one plan upload, L decode-attention launches (PDL-chained).
 // Bytes moved equal the reference's: a request with s tokens moves
@@ -167,6 +170,8 @@ struct ReqKV {
     std::vector<int32_t> pages;
     int ready_slot = -1;          // lane flag + value of the copy that filled `pages` (-1: none pending)
     uint32_t ready_v = 0;
+    int host_slot = -1;           // lane flag + value of the D2H copy (prefill offload, spill, flush) that
+    uint32_t host_v = 0;          // last wrote its host-pool pages (-1: none pending)
     int64_t prefix = 0;
 };
 
@@ -226,6 +231,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
         if (const char* nb = std::getenv("ASV_BULK_STREAMS")) n_bulk_ = std::max(1, std::min(3, std::atoi(nb)));
         ASV_CUDA(cudaStreamCreateWithFlags(&d2h_, cudaStreamNonBlocking));  // other PCIe direction
         ASV_CUDA(cudaStreamCreateWithFlags(&urgent_, cudaStreamNonBlocking));  // strays / swap-ins
+        ASV_CUDA(cudaStreamCreateWithFlags(&prefill_, cudaStreamNonBlocking));  // prefill offloads (D2H)
         ASV_CUDA(cudaSetDevice(o.decode_device));
         // host pool
         if (o.execute_transfers) {
@@ -233,6 +239,13 @@ class GpuExecutor : public prefixsim::EngineObserver {
             ASV_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&arena_), static_cast<size_t>(arena_pages_ * page_bytes_),
                                    cudaHostAllocPortable));
             std::memset(arena_, 0, static_cast<size_t>(arena_pages_ * page_bytes_));
+            if (o.execute_prefill_offload) {
+                // prefill output ring on the prefill (= prefetch) GPU: <= 512 MiB of pages that the
+                // offload copies read in rotation (the prefill compute is not executed)
+                const int64_t n = std::max<int64_t>(2, std::min<int64_t>(64, (int64_t(512) << 20) / page_bytes_));
+                prefill_out_.init(xfer_device(), n, page_bytes_, slice_, &flags_);
+                ASV_CUDA(cudaSetDevice(o.decode_device));
+            }
         }
         // attention operands
         ASV_CUDA(cudaSetDevice(o.decode_device));
@@ -355,6 +368,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
         cudaStreamDestroy(xfer3_);
         cudaStreamDestroy(d2h_);
         cudaStreamDestroy(urgent_);
+        cudaStreamDestroy(prefill_);
     }
 
     // ---------------------------------------------------------- observer
@@ -433,8 +447,15 @@ class GpuExecutor : public prefixsim::EngineObserver {
                 write_back_to_host(t.request_id);
                 end_xfer_group();
                 break;
+            case ASV_XFER_PREFILL_OFFLOAD:
+                if (o_.execute_prefill_offload) {
+                    begin_xfer_group(kPrefill);
+                    offload_to_host(t.request_id, t.bytes);
+                    end_xfer_group();
+                }
+                break;
             default:
-                break;  // prefill_offload: prefill is off the decode path (its KV lands in the pool)
+                break;
         }
         host_ms_ += ms_since(t0);
         host_copy_ms_ += ms_since(t0);
@@ -608,6 +629,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
         ASV_CUDA(cudaStreamSynchronize(xfer3_));
         ASV_CUDA(cudaStreamSynchronize(d2h_));
         ASV_CUDA(cudaStreamSynchronize(urgent_));
+        ASV_CUDA(cudaStreamSynchronize(prefill_));
         ASV_CUDA(cudaSetDevice(o_.decode_device));
         ASV_CUDA(cudaStreamSynchronize(p2p_));
         retire_through(executed_ - 1);
@@ -739,9 +761,12 @@ class GpuExecutor : public prefixsim::EngineObserver {
     // those streams is posted to the copy worker thread.
     // A batch prefetch is spread over n_bulk_ streams (one request each, round
     // robin): concurrent H2D streams keep more PCIe reads in flight.
-    enum Lane { kIter = 0, kBulk = 1, kUrgent = 2, kD2H = 3, kP2P = 4, kBulk2 = 5, kBulk3 = 6, kLanes = 7 };
+    enum Lane { kIter = 0, kBulk = 1, kUrgent = 2, kD2H = 3, kP2P = 4, kBulk2 = 5, kBulk3 = 6, kPrefill = 7,
+                kLanes = 8 };
+    static_assert(kLanes <= SeqFlags::kSlots, "one sequence flag per lane");
     cudaStream_t lane_stream(int lane) const {
         switch (lane) {
+            case kPrefill: return prefill_;
             case kD2H: return d2h_;
             case kUrgent: return urgent_;
             case kP2P: return p2p_;
@@ -800,7 +825,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
     void timer_begin(int lane, bool p2p) {
         CopyTimer t{};
         t.p2p = p2p;
-        t.lane = lane == kD2H ? 'd' : lane == kUrgent ? 'u' : lane == kP2P ? 'p' : 'b';
+        t.lane = lane == kD2H ? 'd' : lane == kUrgent ? 'u' : lane == kP2P ? 'p' : lane == kPrefill ? 'o' : 'b';
         t.seq = cur_seq_;
         t.bytes = 0;
         open_timer_[lane] = static_cast<int64_t>(copy_timers_.size());
@@ -902,12 +927,46 @@ class GpuExecutor : public prefixsim::EngineObserver {
         if (!copies_active()) return;
         next_copy_lane();
         lane_wait_iteration(lane_, hz);
+        lane_wait_host(lane_, r);
         const int64_t moved = post_copy_kv(r.pages, *pool, id, q.prefix_len, true);
         timer_add(lane_, moved);
         stats_.h2d_bytes += moved;
         if (group_timed_) stats_.h2d_bytes_window += moved;
         r.ready_slot = lane_;  // this request is usable as soon as its own pages land
         r.ready_v = lane_signal(lane_);
+    }
+
+    // prefill_offload: the prefilled KV (s tokens) leaves the prefill GPU for the
+    // request's host-pool pages; reference pool_insert happens at its completion
+    // (cluster_sim.hpp:285-299, 379-394), so a later fetch of the request waits
+    // for this copy (lane_wait_host)
+    void offload_to_host(prefixsim::RequestId id, int64_t bytes) {
+        if (bytes % row_bytes_all_ != 0) throw std::logic_error("prefill_offload bytes not a whole number of tokens");
+        const int64_t tokens = bytes / row_bytes_all_;
+        std::vector<int32_t> src(static_cast<size_t>((tokens + 15) / 16));
+        const int64_t ring = pool_usable_pages(slice_, prefill_out_.size());
+        for (size_t j = 0; j < src.size(); ++j) src[j] = static_cast<int32_t>(static_cast<int64_t>(j) % ring);
+        next_copy_lane();
+        const int64_t moved = post_copy_kv(src, prefill_out_, id, tokens, false);
+        timer_add(lane_, moved);
+        stats_.offload_bytes += moved;
+        if (group_timed_) stats_.offload_bytes_window += moved;
+        ReqKV& r = kv(id);
+        r.host_slot = lane_;
+        r.host_v = lane_signal(lane_);
+    }
+    // the lane's stream waits for the D2H copy that last wrote the request's host pages
+    void lane_wait_host(int lane, ReqKV& r) {
+        const int slot = r.host_slot;
+        const uint32_t v = r.host_v;
+        r.host_slot = -1;
+        if (slot < 0 || flags_.reached(slot, v)) return;
+        const cudaStream_t st = lane_stream(lane);
+        const int dev = lane_device(lane);
+        worker_.post([this, st, dev, slot, v] {
+            ASV_CUDA(cudaSetDevice(dev));
+            flags_.wait(st, slot, v);
+        }, "wait_host");
     }
 
     void write_back_to_host(prefixsim::RequestId id) {
@@ -923,6 +982,8 @@ class GpuExecutor : public prefixsim::EngineObserver {
             if (group_timed_) stats_.d2h_bytes_window += moved;
             group_quarantine_.push_back({pool, std::move(r.pages)});
             r.pages.clear();
+            r.host_slot = lane_;
+            r.host_v = lane_signal(lane_);
         } else {
             pool->release(r.pages, pool == &dec_ ? executed_ - 1 : -1);
             r.pages.clear();
@@ -1033,8 +1094,14 @@ class GpuExecutor : public prefixsim::EngineObserver {
                 ASV_OK) {
             throw CudaError(asv_last_error());
         }
+        if (o_.execute_prefill_offload &&
+            asv_kv_copy_d2h(&shape_, prefill_out_.base(), prefill_out_.size(), a, 17, const_cast<void* const*>(host),
+                            prefill_, &moved) != ASV_OK) {
+            throw CudaError(asv_last_error());
+        }
         ASV_CUDA(cudaStreamSynchronize(xfer_));
         ASV_CUDA(cudaStreamSynchronize(d2h_));
+        ASV_CUDA(cudaStreamSynchronize(prefill_));
         ASV_CUDA(cudaSetDevice(o_.decode_device));
         if (asv_kv_copy_d2d(&shape_, dec_.base(), dec_.size(), dec_.device(), b, dec_.base(), dec_.size(),
                             dec_.device(), a, 17, p2p_, &moved) != ASV_OK) {
@@ -1261,13 +1328,14 @@ class GpuExecutor : public prefixsim::EngineObserver {
     int64_t page_bytes_ = 0, row_bytes_all_ = 0, slice_ = 0;
     bool pair_ = false;
     int64_t dec_pages_ = 0, pre_pages_ = 0;
-    PagePool dec_, pre_;
+    PagePool dec_, pre_, prefill_out_;
     cudaStream_t compute_ = nullptr, p2p_ = nullptr, xfer_ = nullptr, xfer2_ = nullptr, xfer3_ = nullptr,
-                 d2h_ = nullptr, urgent_ = nullptr;
+                 d2h_ = nullptr, urgent_ = nullptr, prefill_ = nullptr;
     int n_bulk_ = 2;                        // bulk H2D streams (ASV_BULK_STREAMS=1..3)
     int64_t bulk_rr_ = 0;
     int group_lane_ = 1;                    // lane the open group was begun on
-    int64_t open_timer_[7] = {-1, -1, -1, -1, -1, -1, -1};  // per lane: timer of the open group
+    int64_t open_timer_[kLanes] = {-1, -1, -1, -1, -1, -1, -1, -1};  // per lane: timer of the open group
+    static_assert(kLanes == 8, "open_timer_ initialiser lists one entry per lane");
     SeqFlags flags_;
     CopyWorker worker_;                     // issues every copy-stream operation
     CopyWorker launcher_;                   // issues every compute-stream operation (iterations)

@@ -78,7 +78,8 @@ def engine_run(config, *, device: int = 0, prefetch_device: int | None = None,
                exec_begin: int = 0, exec_end: int = -1, timed_begin: int = 0, copy_begin: int | None = None,
                host_pool_bytes: int = 8 << 30, shard_index: int = 0, shard_count: int = 1,
                pdl: bool = True, run_ahead: int = 256, policy: str | None = None,
-               pair_mode: bool = False, full_step: bool = False, intermediate_size: int = 0) -> dict:
+               pair_mode: bool = False, full_step: bool = False, intermediate_size: int = 0,
+               prefill_offload: bool | None = None) -> dict:
     """Run the decode engine on the GPU (asv_engine_run): reference decisions executed for real."""
     text = config if isinstance(config, str) else json.dumps(config)
     o = _lib.EngineOpts()
@@ -95,6 +96,13 @@ def engine_run(config, *, device: int = 0, prefetch_device: int | None = None,
     o.pair_mode = 1 if pair_mode else 0
     o.full_step = 1 if full_step else 0
     o.intermediate_size = intermediate_size
+    # prefill offloads (prefill GPU -> host pool, D2H; reference cluster_sim.hpp:285-299) belong to the
+    # prefill instance's link: by default they are executed when a separate prefill/prefetch GPU exists,
+    # and stay virtual when the decode GPU is alone (its PCIe link would carry the prefill instance's
+    # traffic too; prefill_offload=True measures exactly that)
+    if prefill_offload is None:
+        prefill_offload = execute_transfers and o.prefetch_device != o.decode_device
+    o.execute_prefill_offload = 1 if (execute_transfers and prefill_offload) else 0
     st = _lib.EngineStats()
     _lib.check(_lib.lib().asv_engine_run(text.encode(), policy.encode() if policy else None,
                                           C.byref(o), C.byref(st)))

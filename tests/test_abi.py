@@ -30,6 +30,18 @@ def test_library_exports_every_declared_symbol():
     assert set(declared_symbols()) <= bound, set(declared_symbols()) - bound
 
 
+def test_struct_mirrors_match_the_library():
+    """Every ctypes mirror has the size of the C struct the library was compiled with."""
+    import ctypes as C
+    from paper_2605_23389_b200 import _lib
+    h = _lib.lib()
+    for cname, mirror in (("asv_attn_shape", _lib.AttnShape), ("asv_attn_plan", _lib.AttnPlan),
+                          ("asv_attn_args", _lib.AttnArgs), ("asv_linear_args", _lib.LinearArgs),
+                          ("asv_engine_opts", _lib.EngineOpts), ("asv_engine_stats", _lib.EngineStats)):
+        assert h.asv_struct_size(cname.encode()) == C.sizeof(mirror), cname
+    assert h.asv_struct_size(b"nope") == -1
+
+
 def test_library_is_built_for_sm100a():
     import subprocess
     so = os.path.join(ROOT, "paper_2605_23389_b200", "libasv.so")

@@ -17,11 +17,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLDEN = json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))
 
 
-def _run(cfg, policy=None, pair=False, transfers=True):
+def _run(cfg, policy=None, pair=False, transfers=True, prefill_offload=True):
     from paper_2605_23389_b200 import engine
     return engine.engine_run(cfg, policy=policy, device=0, num_q_heads=32, num_kv_heads=32, num_layers=32,
                              execute_transfers=transfers, exec_begin=0, exec_end=-1, timed_begin=0, copy_begin=0,
-                             host_pool_bytes=1 << 30, pair_mode=pair)
+                             host_pool_bytes=1 << 30, pair_mode=pair, prefill_offload=prefill_offload)
 
 
 def _expect(key):
@@ -37,6 +37,7 @@ def test_aligned_bytes_moved_match_reference(pair):
         assert lb[k] == v, k
     assert st["h2d_bytes"] == lb["batch_prefetch"] + lb["stray_prefetch"]
     assert st["d2h_bytes"] == lb["spill"] + lb["flush"]
+    assert st["offload_bytes"] == lb["prefill_offload"] > 0  # prefill GPU -> host pool, executed
     assert st["p2p_bytes"] == ((lb["admit"] + lb["evict"]) if pair else 0)
     assert st["iterations_timed"] == GOLDEN["logs"]["smoke:aligned"]["iterations"]
     assert st["window_ms"] > 0 and st["attn_ms"] > 0
@@ -51,11 +52,19 @@ def test_fcfs_bytes_moved_match_reference(policy):
         assert lb[k] == v, k
     assert st["h2d_bytes"] == lb["admit"]
     assert st["d2h_bytes"] == lb["evict"]
+    assert st["offload_bytes"] == lb["prefill_offload"]
+
+
+def test_prefill_offload_can_be_left_virtual():
+    st = _run(GOLDEN["configs"]["smoke"], prefill_offload=False)
+    lb = st["logical_bytes"]
+    assert st["offload_bytes"] == 0 and lb["prefill_offload"] > 0
+    assert st["h2d_bytes"] == lb["batch_prefetch"] + lb["stray_prefetch"]
 
 
 def test_resident_mode_moves_nothing():
     st = _run(GOLDEN["configs"]["smoke"], transfers=False)
-    assert st["h2d_bytes"] == st["d2h_bytes"] == st["p2p_bytes"] == 0
+    assert st["h2d_bytes"] == st["d2h_bytes"] == st["p2p_bytes"] == st["offload_bytes"] == 0
     assert st["tokens_timed"] > 0 and st["kernel_launches_timed"] >= 32 * st["iterations_timed"]
 
 
