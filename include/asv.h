@@ -329,6 +329,14 @@ typedef struct asv_engine_stats {
 
 int asv_engine_run(const char* config_json, const char* policy_override, const asv_engine_opts* opts,
                    asv_engine_stats* stats);
+/* asv_engine_run plus the run's artefacts, replacing `prefixsim run --config X`
+ * (reference tools/prefixsim_main.cpp:66-111, write_run_artifacts :31-49):
+ *   out_dir (nullable): writes log.jsonl (schema 1, byte-identical to the reference's log of the same
+ *     config/shard: the decisions are the reference's), summary.json, ttft_cdf.csv, sched_cdf.csv
+ *     (io.hpp summary_to_json / cdf_to_csv) and gpu_stats.json (the measured B200 numbers);
+ *   log_out (nullable): the schema-1 JSONL log, malloc'ed (release with asv_free), length in *log_len. */
+int asv_engine_run_ex(const char* config_json, const char* policy_override, const asv_engine_opts* opts,
+                      asv_engine_stats* stats, const char* out_dir, char** log_out, int64_t* log_len);
 
 /* Density-first search on a pool snapshot (batch_gen.hpp:126-210).
  * residents: n x {id, prefix_len, kv_blocks} in insertion order (all inserted at t=0).

@@ -199,6 +199,9 @@ SIGNATURES = [
      [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
     ("asv_engine_run", C.c_int,
      [C.c_char_p, C.c_char_p, C.POINTER(EngineOpts), C.POINTER(EngineStats)]),
+    ("asv_engine_run_ex", C.c_int,
+     [C.c_char_p, C.c_char_p, C.POINTER(EngineOpts), C.POINTER(EngineStats), C.c_char_p, C.POINTER(C.c_void_p),
+      C.POINTER(C.c_int64)]),
     ("asv_run_config_jsonl_shard", C.c_int,
      [C.c_char_p, C.c_char_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
     ("asv_dfs_batch", C.c_int,

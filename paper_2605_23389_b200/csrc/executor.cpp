@@ -1395,8 +1395,10 @@ class GpuExecutor : public prefixsim::EngineObserver {
 
 }  // namespace
 
+// `log_out` (optional) receives the run's decision log (the reference's MetricsLog,
+// virtual clock): it is byte-identical to the reference's for the same config
 int engine_run(const char* config_json, const char* policy_override, const asv_engine_opts* opts,
-               asv_engine_stats* stats) {
+               asv_engine_stats* stats, prefixsim::MetricsLog* log_out) {
     try {
         if (config_json == nullptr || opts == nullptr || stats == nullptr) {
             return fail(ASV_ERR_INVALID, "null config/opts/stats");
@@ -1418,6 +1420,7 @@ int engine_run(const char* config_json, const char* policy_override, const asv_e
         prefixsim::MetricsLog log = sim.run();
         (void)t0;
         ex.finish(log, stats);
+        if (log_out != nullptr) *log_out = std::move(log);
         return ASV_OK;
     } catch (const CudaError& e) {
         return fail(ASV_ERR_CUDA, e.what());
@@ -1434,5 +1437,75 @@ int engine_run(const char* config_json, const char* policy_override, const asv_e
 
 extern "C" int asv_engine_run(const char* config_json, const char* policy_override, const asv_engine_opts* opts,
                               asv_engine_stats* stats) {
-    return asv::engine_run(config_json, policy_override, opts, stats);
+    return asv::engine_run(config_json, policy_override, opts, stats, nullptr);
+}
+
+namespace {
+
+std::string stats_to_json(const asv_engine_stats& s) {
+    static const char* kinds[ASV_XFER_KINDS] = {"prefill_offload", "batch_prefetch", "stray_prefetch", "admit",
+                                                "evict", "spill", "flush"};
+    prefixsim::json lb, lc;
+    for (int k = 0; k < ASV_XFER_KINDS; ++k) {
+        lb[kinds[k]] = s.logical_bytes[k];
+        lc[kinds[k]] = s.logical_count[k];
+    }
+    const double tok_s = s.window_ms > 0 ? static_cast<double>(s.tokens_timed) / (s.window_ms * 1e-3) : 0.0;
+    prefixsim::json j = {
+        {"decode_tokens_per_s_measured", tok_s},
+        {"iterations_total", s.iterations_total},
+        {"iterations_timed", s.iterations_timed},
+        {"tokens_timed", s.tokens_timed},
+        {"window_ms", s.window_ms},
+        {"attn_ms", s.attn_ms},
+        {"attn_bytes", s.attn_bytes},
+        {"attn_hbm_gbps", s.attn_ms > 0 ? static_cast<double>(s.attn_bytes) / (s.attn_ms * 1e-3) / 1e9 : 0.0},
+        {"h2d_bytes", s.h2d_bytes},
+        {"d2h_bytes", s.d2h_bytes},
+        {"p2p_bytes", s.p2p_bytes},
+        {"offload_bytes", s.offload_bytes},
+        {"pcie_union_ms", s.pcie_union_ms},
+        {"logical_bytes", lb},
+        {"logical_count", lc},
+        {"virtual_decode_tok_s", s.virtual_decode_tok_s},
+        {"max_batch", s.max_batch},
+        {"kernel_launches_timed", s.kernel_launches_timed},
+        {"measured_idle_frac", s.measured_idle_frac},
+        {"host_decide_ms", s.host_decide_ms},
+    };
+    return j.dump(2) + "\n";
+}
+
+}  // namespace
+
+extern "C" int asv_engine_run_ex(const char* config_json, const char* policy_override, const asv_engine_opts* opts,
+                                 asv_engine_stats* stats, const char* out_dir, char** log_out, int64_t* log_len) {
+    prefixsim::MetricsLog log;
+    const int rc = asv::engine_run(config_json, policy_override, opts, stats, &log);
+    if (rc != ASV_OK) return rc;
+    try {
+        std::string jsonl;
+        if (log_out != nullptr || out_dir != nullptr) jsonl = prefixsim::log_to_jsonl(log);
+        if (out_dir != nullptr) {
+            // the reference's run artefacts (prefixsim_main.cpp write_run_artifacts; SVG charts omitted)
+            const std::string d(out_dir);
+            const prefixsim::Summary sum = prefixsim::summarize(log);
+            prefixsim::write_file(d + "/log.jsonl", jsonl);
+            prefixsim::write_file(d + "/summary.json", prefixsim::summary_to_json(sum).dump(2) + "\n");
+            prefixsim::write_file(d + "/ttft_cdf.csv", prefixsim::cdf_to_csv(sum.ttft_cdf, "ttft_ms"));
+            prefixsim::write_file(d + "/sched_cdf.csv", prefixsim::cdf_to_csv(sum.sched_time_cdf, "schedule_ms"));
+            prefixsim::write_file(d + "/gpu_stats.json", stats_to_json(*stats));
+        }
+        if (log_out != nullptr) {
+            char* buf = static_cast<char*>(std::malloc(jsonl.size() + 1));
+            if (buf == nullptr) throw std::runtime_error("out of host memory");
+            std::memcpy(buf, jsonl.data(), jsonl.size());
+            buf[jsonl.size()] = 0;
+            *log_out = buf;
+            if (log_len != nullptr) *log_len = static_cast<int64_t>(jsonl.size());
+        }
+        return ASV_OK;
+    } catch (const std::exception& e) {
+        return asv::fail(ASV_ERR_RUNTIME, e.what());
+    }
 }

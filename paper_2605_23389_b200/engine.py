@@ -79,8 +79,11 @@ def engine_run(config, *, device: int = 0, prefetch_device: int | None = None,
                host_pool_bytes: int = 8 << 30, shard_index: int = 0, shard_count: int = 1,
                pdl: bool = True, run_ahead: int = 256, policy: str | None = None,
                pair_mode: bool = False, full_step: bool = False, intermediate_size: int = 0,
-               prefill_offload: bool | None = None) -> dict:
-    """Run the decode engine on the GPU (asv_engine_run): reference decisions executed for real."""
+               prefill_offload: bool | None = None, out_dir: str | None = None, return_log: bool = False):
+    """Run the decode engine on the GPU (asv_engine_run_ex): reference decisions executed for real.
+
+    Returns the stats dict; with return_log=True, (stats, schema-1 JSONL log).  out_dir: also write
+    the reference's run artefacts there (log.jsonl, summary.json, CDF CSVs) plus gpu_stats.json."""
     text = config if isinstance(config, str) else json.dumps(config)
     o = _lib.EngineOpts()
     o.decode_device = device
@@ -104,6 +107,17 @@ def engine_run(config, *, device: int = 0, prefetch_device: int | None = None,
         prefill_offload = execute_transfers and o.prefetch_device != o.decode_device
     o.execute_prefill_offload = 1 if (execute_transfers and prefill_offload) else 0
     st = _lib.EngineStats()
-    _lib.check(_lib.lib().asv_engine_run(text.encode(), policy.encode() if policy else None,
-                                          C.byref(o), C.byref(st)))
-    return st.as_dict()
+    h = _lib.lib()
+    if out_dir is None and not return_log:
+        _lib.check(h.asv_engine_run(text.encode(), policy.encode() if policy else None, C.byref(o), C.byref(st)))
+        return st.as_dict()
+    buf, n = C.c_void_p(), C.c_int64(0)
+    _lib.check(h.asv_engine_run_ex(text.encode(), policy.encode() if policy else None, C.byref(o), C.byref(st),
+                                   out_dir.encode() if out_dir else None,
+                                   C.byref(buf) if return_log else None, C.byref(n) if return_log else None))
+    if not return_log:
+        return st.as_dict()
+    try:
+        return st.as_dict(), C.string_at(buf.value, n.value).decode()
+    finally:
+        h.asv_free(buf)
