@@ -64,6 +64,12 @@ def group_pages(n_kv: int, pool_pages: int) -> int:
     return pool_pages // ((pool_pages + gmax - 1) // gmax)
 
 
+def usable_pages(n_kv: int, pool_pages_: int) -> int:
+    """page ids the kernels accept: whole layer-major groups (asv_pool_usable_pages)."""
+    g = group_pages(n_kv, pool_pages_)
+    return (pool_pages_ // g) * g
+
+
 def block_view(pool: np.ndarray, n_kv: int, num_layers: int) -> np.ndarray:
     """uint8 LAYER-MAJOR device pool of ONE page group -> [layers][pages][2][n_kv][4096] byte view."""
     assert group_pages(n_kv, pool_pages(pool, n_kv, num_layers)) == pool_pages(pool, n_kv, num_layers), \

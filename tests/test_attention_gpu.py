@@ -34,8 +34,8 @@ def _run_case(oracle, n_q, n_kv, L, layer, seq_lens, seed=1, num_workers=None, a
     need = sum((s + 16) // 16 for s in seq_lens)
     pool_pages = need + 7
     pool = U.random_bf16(seed, pool_pages * pb // 2).view(np.uint8).copy()
-    indptr, indices = U.make_batch(seq_lens, pool_pages, seed + 1, append=True)
-    blocks = U.block_view(pool, n_kv, L)
+    indptr, indices = U.make_batch(seq_lens, U.usable_pages(n_kv, pool_pages), seed + 1, append=True)
+    blocks = U.block_view(pool, n_kv, L) if (const_v is not None or poison_tail) else None
     if const_v is not None:
         # every element of every V block equal: the swizzle is irrelevant
         cv = U.f32_to_bf16_bits(np.array([const_v], np.float32))[0]
@@ -84,13 +84,17 @@ def _run_case(oracle, n_q, n_kv, L, layer, seq_lens, seed=1, num_workers=None, a
     if append:
         # fused KV append (K3): token row seq_len of (layer, kv head) holds k_new / v_new
         pool_after = pool_d.cpu().numpy()
-        ba = U.block_view(pool_after, n_kv, L)
+        npages = U.pool_pages(pool_after, n_kv, L)
+
+        def blk(page, kv, h):  # works for multi-group pools (>= 2 GiB layer pitch) too
+            off = U.pool_block_offset(n_kv, L, npages, int(page), layer, kv, h)
+            return pool_after[off:off + 4096]
         for r, s in enumerate(seq_lens):
             page = indices[indptr[r] + s // 16]
             t = s % 16
             for h in range(n_kv):
-                krow = U.unswizzle_block(ba[layer, page, 0, h])[t]
-                vrow = U.unswizzle_block(ba[layer, page, 1, h])[t]
+                krow = U.unswizzle_block(blk(page, 0, h))[t]
+                vrow = U.unswizzle_block(blk(page, 1, h))[t]
                 assert (krow == kn_bits[r, h]).all()
                 assert (vrow == vn_bits[r, h]).all()
     return got, ref_out, plan
@@ -214,3 +218,19 @@ print("NO ERROR")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code, root], capture_output=True, text=True, timeout=300)
     assert r.returncode != 0 and "NO ERROR" not in r.stdout, r.stdout + r.stderr
+
+
+# ---- BASELINE.json full sizes (C2: 1K-16K, C5: up to 128K tokens) against the oracle ----
+
+def test_config2_lengths_full_size(oracle):
+    """C2 shape: 7B MHA, batch 8 of KV lengths drawn from 1K-16K (the headline workload's range)."""
+    rng = np.random.default_rng(1024)
+    seq = rng.integers(1024, 16385, size=8).tolist()
+    _run_case(oracle, 32, 32, 1, 0, seq, seed=111)
+
+
+@pytest.mark.parametrize("n_q,n_kv", [(32, 32), (40, 8)])
+def test_config5_max_context_128k(oracle, n_q, n_kv):
+    """C5's longest request: 131072 KV tokens (8192 pages, ~250 splits merged) beside two short ones,
+    MHA and 13B GQA-8, against the fp32 oracle; plus the fused append at row 131072."""
+    _run_case(oracle, n_q, n_kv, 1, 0, [131072, 17, 1000], seed=121)
