@@ -22,7 +22,11 @@ a steady-state point of the trace (earlier iterations run decisions only).
 
 N > 1 (torchrun): requests are sharded data-parallel (request i -> rank i % N),
 every rank runs its shard's engine on its GPU, no data-path collective; the
-window is the max over ranks.  `--impl reference` times the reference's CPU
+window is the max over ranks.  `--topology pairs`: ranks 2p (decode) and 2p+1
+(prefetch) form a pair; the decode rank's engine drives both GPUs (candidate
+buffers, host->GPU prefetches and prefill offloads on the prefetch GPU, admits /
+evicts as NVLink peer copies), requests are sharded over the N/2 pairs, and the
+prefetch rank only joins the barriers and reductions.  `--impl reference` times the reference's CPU
 path (the compiled reference decision engine + the fp32 CPU attention oracle)
 on the host cores instead.
 """
@@ -62,6 +66,10 @@ def parse():
     ap.add_argument("--no-full-step", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=12.0)
+    ap.add_argument("--topology", default="dp", choices=["dp", "pairs"],
+                    help="dp: every GPU decodes its own shard over its own PCIe link (default); pairs: "
+                         "GPUs 2p / 2p+1 form a (decode, prefetch) pair, the prefetch GPU pulls KV from host "
+                         "memory and pushes it to its decode partner over NVLink (SURVEY §8(e))")
     return ap.parse_args()
 
 
@@ -262,9 +270,28 @@ def main():
         return
 
     dev = d.local
+    pairs = args.topology == "pairs" and d.world > 1
+    if pairs and d.world % 2:
+        raise SystemExit("--topology pairs needs an even number of GPUs")
     run_kw = dict(device=dev, num_q_heads=attn["num_q_heads"], num_kv_heads=attn["num_kv_heads"],
                   num_layers=attn["num_layers"], exec_begin=S, timed_begin=S + W, exec_end=S + W + K,
                   shard_index=d.rank, shard_count=d.world, host_pool_bytes=HOST_POOL_BYTES)
+    idle = False  # a pair's prefetch rank: its GPU is driven by the decode rank's engine
+    if pairs:
+        run_kw.update(shard_index=d.rank // 2, shard_count=d.world // 2)
+        if os.environ.get("ASV_BENCH_DEVICE"):  # testing: the pair on one device (separate pools)
+            run_kw.update(pair_mode=True)
+        else:
+            run_kw.update(prefetch_device=dev + 1)
+        idle = d.rank % 2 == 1
+    real_run = E.engine_run
+
+    def engine_run(cfg_, **kw):
+        if idle:
+            from paper_2605_23389_b200 import _lib
+            return _lib.EngineStats().as_dict()
+        return real_run(cfg_, **kw)
+    E = argparse.Namespace(engine_run=engine_run)
     d.barrier()
     with ClockSampler(dev) as clk:
         res = E.engine_run(cfg, execute_transfers=False, **run_kw)
@@ -294,9 +321,11 @@ def main():
             d.barrier()
         # the same window with the prefill instance colocated on this GPU: every prefill_offload
         # (prefill GPU -> host pool) is a real D2H copy sharing this GPU's PCIe link with the prefetches
-        e2e_colo = E.engine_run(cfg, execute_transfers=True, copy_begin=max(0, S - COPY_LEAD), prefill_offload=True,
-                                **kw)
-        d.barrier()
+        e2e_colo = None
+        if not pairs:  # a pair already runs its prefill offloads on the prefetch GPU's link
+            e2e_colo = E.engine_run(cfg, execute_transfers=True, copy_begin=max(0, S - COPY_LEAD),
+                                    prefill_offload=True, **kw)
+            d.barrier()
 
     win, tok = d.reduce([res["window_ms"], float(res["tokens_timed"])], "MAX")[0], \
         d.reduce([float(res["tokens_timed"])], "SUM")[0]
@@ -331,7 +360,7 @@ def main():
                                              if link > 0 else None),
                 "what": "same window and KV moves, every step runs the full decoder layer stack (see full_decode_step)"}
 
-    if e2e is not None:
+    if e2e is not None and e2e_colo is not None:
         cw = d.reduce([e2e_colo["window_ms"]], "MAX")[0]
         c_steps = max(1, e2e_colo["iterations_timed"])
         c_link = e2e_colo["pcie_union_ms"]
@@ -415,7 +444,7 @@ def main():
             "data": (f"synthetic: deterministic splitmix64 trace {cfg.get('workload', {}).get('path', '?')}, "
                      "random bf16 KV/q"),
             "config": {"workload": WORKLOAD_NAME, "global_batch": tok / max(1, res["iterations_timed"]),
-                       "seq_len": "1K-16K (+ up to 68 generated)", "parallelism": f"dp{d.world}",
+                       "seq_len": "1K-16K (+ up to 68 generated)", "parallelism": f"pairs{d.world // 2}" if pairs else f"dp{d.world}",
                        "steady_start_iteration": S,
                        "l2": "inputs larger than L2: every step reads ~10-60 GB of KV (L2 is 126 MB)"},
             "e2e": e2e_obj, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,

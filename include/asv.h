@@ -316,7 +316,8 @@ typedef struct asv_engine_stats {
                                      timed iteration, from per-warp %globaltimer */
     double measured_bubble_ms;    /* sum over timed iterations of the mean idle time per warp x layers */
     double pcie_union_ms;         /* union of the PCIe copy-group intervals (both directions) inside the
-                                     window: time the host link had work (single device only, else 0) */
+                                     window: time the host link had work (with a separate prefetch GPU: the union
+                                     of its timed PCIe copy groups, from the first one) */
     double host_wait_ms;          /* host time blocked on the GPU (run-ahead ring, page reclaim) */
     int64_t hazard_waits;         /* copy-stream waits on a page's last iteration (page reuse) */
     int64_t result_d2h_bytes_window; /* e2e: each iteration's attention output [b][n_h][128] bf16 read back

@@ -639,15 +639,29 @@ class GpuExecutor : public prefixsim::EngineObserver {
             stats_.window_ms = ms;
         }
         std::vector<std::pair<float, float>> pcie;  // PCIe copy groups relative to the window start
+        // a pair's PCIe copies run on the prefetch GPU, whose events cannot be timed against the
+        // decode GPU's window events: their union is taken relative to the first timed PCIe group
+        const bool cross = xfer_device() != o_.decode_device;
+        cudaEvent_t anchor = win_beg_;
+        if (cross) {
+            anchor = nullptr;
+            for (const auto& pr : copy_timers_) {
+                if (!pr.p2p) {
+                    anchor = pr.a;
+                    break;
+                }
+            }
+        }
+        const float clip = cross ? 1e30f : static_cast<float>(stats_.window_ms);
         for (auto& pr : copy_timers_) {
             float ms = 0.f;
             if (cudaEventElapsedTime(&ms, pr.a, pr.b) == cudaSuccess) {
                 (pr.p2p ? stats_.p2p_busy_ms : stats_.h2d_busy_ms) += ms;
             }
             float a = 0.f, b = 0.f;
-            if (!pr.p2p && window_open_ && cudaEventElapsedTime(&a, win_beg_, pr.a) == cudaSuccess &&
-                cudaEventElapsedTime(&b, win_beg_, pr.b) == cudaSuccess) {
-                pcie.emplace_back(std::max(0.f, a), std::min(b, static_cast<float>(stats_.window_ms)));
+            if (!pr.p2p && window_open_ && anchor != nullptr && cudaEventElapsedTime(&a, anchor, pr.a) == cudaSuccess &&
+                cudaEventElapsedTime(&b, anchor, pr.b) == cudaSuccess) {
+                pcie.emplace_back(std::max(0.f, a), std::min(b, clip));
                 if (tracing_) {
                     trace_.push_back(std::string("{\"copy\":\"") + pr.lane + "\",\"seq\":" + std::to_string(pr.seq) +
                                      ",\"bytes\":" + std::to_string(pr.bytes) + ",\"t0\":" + std::to_string(a) +
