@@ -131,7 +131,7 @@ size_t asv_attn_workspace_bytes(const asv_attn_shape* shape, int32_t max_batch,
 int asv_attn_workspace_init(void* workspace, size_t bytes, void* stream);
 
 typedef struct asv_attn_args {
-    const void* q;          /* [b][n_h][128] bf16, this layer */
+    const void* q;          /* [b][n_h][128] bf16 (fp16 with kv_dtype = ASV_KV_F16), this layer */
     void* kv_pool;          /* device page pool base (layer-major layout above) */
     int64_t pool_pages;     /* pages in the pool: the layer stride of the layer-major pool */
     int32_t layer;          /* layer slice of every page to attend over */
@@ -149,7 +149,12 @@ typedef struct asv_attn_args {
     uint64_t* warp_timestamps; /* optional [workers][2] device-accessible buffer (device or mapped host):
                                   %globaltimer at each persistent warp's start and end — the measured
                                   intra-iteration bubble */
+    int32_t kv_dtype;       /* ASV_KV_BF16 (0, default) or ASV_KV_F16: the element type of the KV pool,
+                               q, k_new / v_new and out (the layout is the same 16-bit one) */
 } asv_attn_args;
+
+#define ASV_KV_BF16 0
+#define ASV_KV_F16 1
 
 /* K1+K2+K3: paged split-KV decode attention with fused KV append (K1+K3), then the
  * log-sum-exp merge of split requests (K2), chained with programmatic dependent

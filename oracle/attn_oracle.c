@@ -15,7 +15,7 @@
  * attention vectors exist there); pinned instead by known-answer tests
  * (tests/test_oracle.py) and an independent numpy restatement.
  *
- * Numerics: bf16 inputs widened to fp32 exactly; dot products in fp32, the
+ * Numerics: bf16 (or IEEE fp16, kv_dtype 1) inputs widened to fp32 exactly; dot products in fp32, the
  * softmax normaliser and the weighted V sum accumulated in double.
  * Layout and swizzle: include/asv.h (device pool LAYER-MAJOR in page groups of
  * G pages, each group [L][G][2][n_kv][16][128], G the largest equal split with
@@ -34,6 +34,32 @@ static inline float bf16_to_f32(uint16_t h) {
     return f;
 }
 
+/* IEEE binary16 -> fp32, exact (subnormals, inf, nan) */
+static inline float f16_to_f32(uint16_t h) {
+    const uint32_t sign = (uint32_t)(h & 0x8000u) << 16;
+    const int exp = (h >> 10) & 0x1f;
+    uint32_t mant = h & 0x3ffu, u;
+    if (exp == 0x1f) {
+        u = sign | 0x7f800000u | (mant << 13);
+    } else if (exp != 0) {
+        u = sign | ((uint32_t)(exp - 15 + 127) << 23) | (mant << 13);
+    } else if (mant == 0) {
+        u = sign;
+    } else {  /* subnormal: normalise */
+        int e = -14;
+        while (!(mant & 0x400u)) {
+            mant <<= 1;
+            --e;
+        }
+        u = sign | ((uint32_t)(e + 127) << 23) | ((mant & 0x3ffu) << 13);
+    }
+    float f;
+    memcpy(&f, &u, 4);
+    return f;
+}
+
+static inline float kv_to_f32(uint16_t h, int f16) { return f16 ? f16_to_f32(h) : bf16_to_f32(h); }
+
 /* byte offset of (token t, dim d) inside one 4 KiB (page, layer, K|V, head) block */
 static inline int64_t swz_off(int t, int d) {
     int c = d / 8;
@@ -49,6 +75,7 @@ typedef struct {
     const int32_t* indptr;
     const int32_t* indices;
     float sm_scale;
+    int f16;             /* element type: 0 bf16, 1 fp16 */
     float* out;
     float* lse;
     int next;            /* work counter (guarded by mu) */
@@ -62,7 +89,7 @@ static void one_row(const job_t* j, int r, int h) {
     const int s = j->seq_lens[r];
     const uint16_t* qv = j->q + ((int64_t)r * j->n_q + h) * D;
     float qf[128];
-    for (int d = 0; d < D; ++d) qf[d] = bf16_to_f32(qv[d]);
+    for (int d = 0; d < D; ++d) qf[d] = kv_to_f32(qv[d], j->f16);
     float* scores = (float*)malloc(sizeof(float) * (size_t)(s > 0 ? s : 1));
     /* block (page, layer, kv, head) of the grouped layer-major pool */
     const int64_t slice = (int64_t)2 * j->n_kv * 4096;
@@ -78,7 +105,7 @@ static void one_row(const job_t* j, int r, int h) {
         for (int d = 0; d < D; ++d) {
             uint16_t kb;
             memcpy(&kb, base + swz_off(t % 16, d), 2);
-            acc += qf[d] * bf16_to_f32(kb);
+            acc += qf[d] * kv_to_f32(kb, j->f16);
         }
         scores[t] = acc * j->sm_scale;
         if (scores[t] > mx) mx = scores[t];
@@ -94,7 +121,7 @@ static void one_row(const job_t* j, int r, int h) {
         for (int d = 0; d < D; ++d) {
             uint16_t vb;
             memcpy(&vb, base + swz_off(t % 16, d), 2);
-            o[d] += p * (double)bf16_to_f32(vb);
+            o[d] += p * (double)kv_to_f32(vb, j->f16);
         }
     }
     float* dst = j->out + ((int64_t)r * j->n_q + h) * D;
@@ -118,12 +145,12 @@ static void* worker(void* arg) {
 }
 
 /* out: [batch][n_q][128] fp32; lse: [batch][n_q] natural log (nullable).
- * Returns 0 on success. */
-int asv_oracle_decode_attention(int n_q, int n_kv, int num_layers, int layer, const uint16_t* q,
-                                const uint8_t* pool, int64_t pool_pages, const int32_t* seq_lens,
-                                const int32_t* indptr, const int32_t* indices, int batch,
-                                float sm_scale, float* out, float* lse, int threads) {
-    if (n_kv <= 0 || n_q % n_kv != 0 || batch < 1) return 1;
+ * kv_dtype: 0 bf16, 1 fp16 (q and the pool).  Returns 0 on success. */
+int asv_oracle_decode_attention_dt(int n_q, int n_kv, int num_layers, int layer, const uint16_t* q,
+                                   const uint8_t* pool, int64_t pool_pages, const int32_t* seq_lens,
+                                   const int32_t* indptr, const int32_t* indices, int batch,
+                                   float sm_scale, float* out, float* lse, int threads, int kv_dtype) {
+    if (n_kv <= 0 || n_q % n_kv != 0 || batch < 1 || (kv_dtype != 0 && kv_dtype != 1)) return 1;
     job_t j;
     j.n_q = n_q;
     j.n_kv = n_kv;
@@ -137,6 +164,7 @@ int asv_oracle_decode_attention(int n_q, int n_kv, int num_layers, int layer, co
     j.indptr = indptr;
     j.indices = indices;
     j.sm_scale = sm_scale;
+    j.f16 = kv_dtype;
     j.out = out;
     j.lse = lse;
     j.next = 0;
@@ -148,6 +176,14 @@ int asv_oracle_decode_attention(int n_q, int n_kv, int num_layers, int layer, co
     for (int i = 0; i < threads; ++i) pthread_join(tids[i], NULL);
     pthread_mutex_destroy(&j.mu);
     return 0;
+}
+
+int asv_oracle_decode_attention(int n_q, int n_kv, int num_layers, int layer, const uint16_t* q,
+                                const uint8_t* pool, int64_t pool_pages, const int32_t* seq_lens,
+                                const int32_t* indptr, const int32_t* indices, int batch,
+                                float sm_scale, float* out, float* lse, int threads) {
+    return asv_oracle_decode_attention_dt(n_q, n_kv, num_layers, layer, q, pool, pool_pages, seq_lens, indptr,
+                                          indices, batch, sm_scale, out, lse, threads, 0);
 }
 
 /* Write (token t of layer/kv/head) row into a page buffer using the swizzle —

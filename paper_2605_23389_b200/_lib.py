@@ -59,6 +59,7 @@ class AttnArgs(C.Structure):
         ("launch_index", C.c_uint32),
         ("pdl", C.c_int32),
         ("warp_timestamps", C.c_void_p),
+        ("kv_dtype", C.c_int32),
     ]
 
 

@@ -62,13 +62,17 @@ class PagedDecodeAttention:
     """
 
     def __init__(self, num_q_heads: int, num_kv_heads: int, num_layers: int,
-                 device: int | torch.device = 0, sm_scale: float | None = None):
+                 device: int | torch.device = 0, sm_scale: float | None = None,
+                 dtype: torch.dtype = torch.bfloat16):
         self.lib = _lib.lib()
         self.device = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
         self.shape = _lib.AttnShape(num_q_heads, num_kv_heads, HEAD_DIM, PAGE_SIZE, num_layers)
         self.num_q_heads = num_q_heads
         self.num_kv_heads = num_kv_heads
         self.num_layers = num_layers
+        if dtype not in (torch.bfloat16, torch.float16):
+            raise TypeError("KV dtype must be bfloat16 or float16")
+        self.dtype = dtype  # element type of the KV pool, q, k_new / v_new and out
         self.sm_scale = float(sm_scale) if sm_scale is not None else 1.0 / math.sqrt(HEAD_DIM)
         w = C.c_int32(0)
         _lib.check(self.lib.asv_attn_num_workers(C.byref(self.shape), self.device.index or 0, C.byref(w)))
@@ -120,10 +124,12 @@ class PagedDecodeAttention:
     def run(self, q: torch.Tensor, kv_pool: torch.Tensor, layer: int, plan: Plan,
             out: torch.Tensor, lse: torch.Tensor | None = None, k_new: torch.Tensor | None = None,
             v_new: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-        """out[b][n_h][128] (bf16) = softmax(q K^T * sm_scale) V for every request of the plan."""
+        """out[b][n_h][128] (self.dtype) = softmax(q K^T * sm_scale) V for every request of the plan."""
         b = plan.batch
-        if q.dtype != torch.bfloat16 or out.dtype != torch.bfloat16:
-            raise TypeError("q and out must be bfloat16")
+        if q.dtype != self.dtype or out.dtype != self.dtype:
+            raise TypeError(f"q and out must be {self.dtype}")
+        if k_new is not None and (k_new.dtype != self.dtype or v_new is None or v_new.dtype != self.dtype):
+            raise TypeError(f"k_new and v_new must be {self.dtype}")
         if q.shape[0] < b or out.shape[0] < b:
             raise ValueError("q/out batch smaller than the plan")
         args = _lib.AttnArgs()
@@ -142,6 +148,7 @@ class PagedDecodeAttention:
         args.sm_scale = self.sm_scale
         args.launch_index = self._launches & 0xFFFFFFFF
         args.pdl = 1 if self.pdl else 0
+        args.kv_dtype = 1 if self.dtype == torch.float16 else 0
         self._launches += 1
         with torch.cuda.device(self.device):
             _lib.check(self.lib.asv_decode_attention(C.byref(self.shape), C.byref(args),

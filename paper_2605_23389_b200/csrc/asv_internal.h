@@ -42,6 +42,7 @@ struct AttnLaunch {
     int group;              // n_q / n_kv
     int grid;               // persistent CTAs
     bool pdl;               // programmatic dependent launch
+    bool f16;               // KV / q / out element type: fp16 (else bf16)
     const void* q;
     void* pool;
     int64_t page_bytes;     // one layer slice of one page (pool_slot unit)
@@ -70,7 +71,7 @@ struct AttnLaunch {
     unsigned long long* warp_ts;  // optional per-warp %globaltimer (start, end)
 };
 
-int attn_warps_per_cta(int group);
+int attn_warps_per_cta(int group, bool f16 = false);
 cudaError_t attn_occupancy(int group, int* blocks_per_sm);
 cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st);
 // n_int32 rounded up to a multiple of 4 (16-byte units); both pointers 16-byte aligned

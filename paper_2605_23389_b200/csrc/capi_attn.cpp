@@ -299,7 +299,10 @@ int asv_decode_attention(const asv_attn_shape* shape, const asv_attn_args* a, vo
     const int64_t need = kHeadBytes + static_cast<int64_t>(pl.total_splits) * n_q * (128 * 4 + 8);
     if (a->workspace == nullptr || static_cast<int64_t>(a->workspace_bytes) < need)
         return fail(ASV_ERR_INVALID, "workspace too small for plan: need " + std::to_string(need));
-    const int nw = attn_warps_per_cta(n_q / n_kv);
+    if (a->kv_dtype != ASV_KV_BF16 && a->kv_dtype != ASV_KV_F16)
+        return fail(ASV_ERR_INVALID, "kv_dtype must be ASV_KV_BF16 or ASV_KV_F16");
+    const bool f16 = a->kv_dtype == ASV_KV_F16;
+    const int nw = attn_warps_per_cta(n_q / n_kv, f16);
     if (pl.num_workers < nw || pl.num_workers % nw != 0)
         return fail(ASV_ERR_INVALID, "plan num_workers must be a multiple of the CTA warp count");
 
@@ -328,6 +331,7 @@ int asv_decode_attention(const asv_attn_shape* shape, const asv_attn_args* a, vo
     L.gdesc = a->plan_dev + pl.off_desc;
     L.split_base = a->plan_dev + pl.off_split_base;
     L.pdl = a->pdl != 0;
+    L.f16 = f16;
     L.merge_reqs = a->plan_dev + pl.off_merge;
     L.n_merge = pl.n_merge;
     {

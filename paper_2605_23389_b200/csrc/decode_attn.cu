@@ -26,8 +26,12 @@
 //  * the owner of a request's last split appends the step's K/V row at position
 //    seq_len (prefix_len += 1, cluster_sim.hpp:443-447);
 //  * programmatic dependent launch: the KV prefetch of layer l+1 overlaps layer
-//    l's tail; q, outputs and the append wait on griddepcontrol.wait.
+//    l's tail; q, outputs and the append wait on griddepcontrol.wait;
+//  * KV element type bf16 (default) or fp16 (template flag F16): q, KV, the
+//    appended row and the output share it; the same FHFMA / HMMA instructions
+//    exist in both types, P is rounded to the KV type before P.V.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -48,7 +52,7 @@ constexpr int kWarpExtra = 768;                 // per warp: mbarriers | descrip
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct Params {
-    const __nv_bfloat16* q;
+    const uint16_t* q;          // bf16 or fp16 bits (F16)
     const char* pool;
     char* pool_w;
     int64_t page_bytes;
@@ -63,9 +67,9 @@ struct Params {
     int32_t n_kv;
     int32_t n_q;
     int32_t total_warps;
-    const __nv_bfloat16* k_new;
-    const __nv_bfloat16* v_new;
-    __nv_bfloat16* out;
+    const uint16_t* k_new;
+    const uint16_t* v_new;
+    uint16_t* out;
     float* lse;
     float* part_o;    // [slots * n_q][128]
     float2* part_ml;  // [slots * n_q]
@@ -135,21 +139,45 @@ __device__ __forceinline__ uint2 lds64(uint32_t a) {
     asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
     return v;
 }
-// d = a.{lo|hi} * b.{lo|hi} + c   (bf16 x bf16 -> fp32, sm_100 FHFMA)
-template <int AH, int BH>
-__device__ __forceinline__ float fma_bf(uint32_t a, uint32_t b, float c) {
-    asm("{\n .reg .b16 a0, a1, b0, b1;\n mov.b32 {a0, a1}, %1;\n mov.b32 {b0, b1}, %2;\n"
-        " fma.rn.f32.bf16 %0, a%3, b%4, %0;\n}\n"
-        : "+f"(c)
-        : "r"(a), "r"(b), "n"(AH), "n"(BH));
+// d = a.{lo|hi} * b.{lo|hi} + c   (bf16 x bf16 or fp16 x fp16 -> fp32, sm_100 FHFMA)
+template <bool F16, int AH, int BH>
+__device__ __forceinline__ float fma_kv(uint32_t a, uint32_t b, float c) {
+    if constexpr (F16) {
+        asm("{\n .reg .b16 a0, a1, b0, b1;\n mov.b32 {a0, a1}, %1;\n mov.b32 {b0, b1}, %2;\n"
+            " fma.rn.f32.f16 %0, a%3, b%4, %0;\n}\n"
+            : "+f"(c)
+            : "r"(a), "r"(b), "n"(AH), "n"(BH));
+    } else {
+        asm("{\n .reg .b16 a0, a1, b0, b1;\n mov.b32 {a0, a1}, %1;\n mov.b32 {b0, b1}, %2;\n"
+            " fma.rn.f32.bf16 %0, a%3, b%4, %0;\n}\n"
+            : "+f"(c)
+            : "r"(a), "r"(b), "n"(AH), "n"(BH));
+    }
     return c;
 }
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-    return *reinterpret_cast<uint32_t*>(&v);
+template <bool F16>
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+    if constexpr (F16) {
+        __half2 v = __floats2half2_rn(lo, hi);
+        return *reinterpret_cast<uint32_t*>(&v);
+    } else {
+        __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+        return *reinterpret_cast<uint32_t*>(&v);
+    }
 }
-__device__ __forceinline__ float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
-__device__ __forceinline__ float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
+// x rounded to the KV type: its bits, and (in *f) its value
+template <bool F16>
+__device__ __forceinline__ uint16_t round_kv(float x, float* f) {
+    if constexpr (F16) {
+        const __half h = __float2half_rn(x);
+        *f = __half2float(h);
+        return __half_as_ushort(h);
+    } else {
+        const __nv_bfloat16 h = __float2bfloat16_rn(x);
+        *f = __bfloat162float(h);
+        return __bfloat16_as_ushort(h);
+    }
+}
 
 __device__ __forceinline__ void ldsm_x4(uint32_t a, uint32_t& r0, uint32_t& r1, uint32_t& r2,
                                         uint32_t& r3) {
@@ -163,24 +191,25 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t a, uint32_t& r0, uint32_t& r1
                  : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
                  : "r"(a));
 }
-__device__ __forceinline__ void mma_bf16(float* c, uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
-    // rows 8..15 of A (a1, a3) are the zero padding of the <= 8-head query group
-    asm volatile(
-        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7},"
-        " {%8,%9}, {%0,%1,%2,%3};"
-        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-        : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
-}
-// m16n8k16 with a full A fragment (a0..a3) and B fragment (b0, b1)
+// m16n8k16 with a full A fragment (a0..a3) and B fragment (b0, b1), fp32 accumulate
+template <bool F16>
 __device__ __forceinline__ void mma_m16(float* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
                                         uint32_t b1) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7},"
-        " {%8,%9}, {%0,%1,%2,%3};"
-        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+    if constexpr (F16) {
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7},"
+            " {%8,%9}, {%0,%1,%2,%3};"
+            : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+    } else {
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7},"
+            " {%8,%9}, {%0,%1,%2,%3};"
+            : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+    }
 }
-// zero the bf16 halves of a packed pair {token k (lo), token k+1 (hi)} past `valid`
+// zero the 16-bit halves of a packed pair {token k (lo), token k+1 (hi)} past `valid`
 __device__ __forceinline__ uint32_t mask_tokens(uint32_t b, int k, int valid) {
     if (k >= valid) return 0u;
     if (k + 1 >= valid) return b & 0x0000ffffu;
@@ -240,12 +269,13 @@ __device__ __forceinline__ void load_desc(const Params& p, uint32_t k, int lane,
 }
 
 // ------------------------------------------------------------- epilogues
+template <bool F16>
 __device__ __forceinline__ void write_final_row(const Params& p, int r, int qh, int lane, const float* o,
                                                 float m, float l) {
     const float inv = l > 0.f ? 1.f / l : 0.f;
     uint2 w;
-    w.x = pack_bf16(o[0] * inv, o[1] * inv);
-    w.y = pack_bf16(o[2] * inv, o[3] * inv);
+    w.x = pack2<F16>(o[0] * inv, o[1] * inv);
+    w.y = pack2<F16>(o[2] * inv, o[3] * inv);
     *reinterpret_cast<uint2*>(p.out + (static_cast<int64_t>(r) * p.n_q + qh) * kD + lane * 4) = w;
     if (p.lse != nullptr && lane == 0) {
         p.lse[static_cast<int64_t>(r) * p.n_q + qh] = l > 0.f ? (m + __log2f(l)) / kLog2e : -INFINITY;
@@ -258,8 +288,7 @@ __device__ __forceinline__ void append_row(const Params& p, const Desc& d, int l
     const int t = d.seq % kPage;
     const int c = lane & 15;
     const bool is_v = lane >= 16;
-    const __nv_bfloat16* src =
-        (is_v ? p.v_new : p.k_new) + (static_cast<int64_t>(d.r) * p.n_kv + d.head) * kD + c * 8;
+    const uint16_t* src = (is_v ? p.v_new : p.k_new) + (static_cast<int64_t>(d.r) * p.n_kv + d.head) * kD + c * 8;
     char* dst = p.pool_w + static_cast<int64_t>(d.append_phys) * p.page_bytes + p.layer_off +
                 (is_v ? p.v_off : 0) + static_cast<int64_t>(d.head) * kBlockBytes + swz(t, c);
     *reinterpret_cast<uint4*>(dst) = __ldg(reinterpret_cast<const uint4*>(src));
@@ -295,8 +324,7 @@ struct QRegs {
     __device__ __forceinline__ void load(const Params& p, const Desc& d, int lane) {
         const int head = lane >> 2, kc = (lane & 3) * 2;
         const bool hv = head < GROUP;
-        const __nv_bfloat16* src =
-            p.q + (static_cast<int64_t>(d.r) * p.n_q + d.head * GROUP + (hv ? head : 0)) * kD;
+        const uint16_t* src = p.q + (static_cast<int64_t>(d.r) * p.n_q + d.head * GROUP + (hv ? head : 0)) * kD;
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
             v[2 * ks] = hv ? __ldg(reinterpret_cast<const uint32_t*>(src + ks * 16 + kc)) : 0u;
@@ -306,11 +334,11 @@ struct QRegs {
 };
 
 // ------------------------------------------------------- per-item state
-template <int GROUP>
+template <int GROUP, bool F16>
 struct Acc;
 
-template <>
-struct Acc<1> {
+template <bool F16>
+struct Acc<1, F16> {
     float m, l, o[4];
     __device__ __forceinline__ void reset() {
         m = -INFINITY;
@@ -319,21 +347,21 @@ struct Acc<1> {
     }
     // one 16-token page: scores, online softmax, P.V
     __device__ __forceinline__ void page(const QRegs<1>& q, uint32_t ks, uint32_t vs, uint32_t sp,
-                                         __nv_bfloat16* scratch, int valid, float scale, int lane) {
+                                         uint16_t* scratch, int valid, float scale, int lane) {
         const int t = lane & 15;
         const int half = lane >> 4;
         float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             const uint4 kv = lds128(ks + swz(t, half * 8 + j));
-            a0 = fma_bf<0, 0>(kv.x, q.v[4 * j + 0], a0);
-            a1 = fma_bf<1, 1>(kv.x, q.v[4 * j + 0], a1);
-            a2 = fma_bf<0, 0>(kv.y, q.v[4 * j + 1], a2);
-            a3 = fma_bf<1, 1>(kv.y, q.v[4 * j + 1], a3);
-            a0 = fma_bf<0, 0>(kv.z, q.v[4 * j + 2], a0);
-            a1 = fma_bf<1, 1>(kv.z, q.v[4 * j + 2], a1);
-            a2 = fma_bf<0, 0>(kv.w, q.v[4 * j + 3], a2);
-            a3 = fma_bf<1, 1>(kv.w, q.v[4 * j + 3], a3);
+            a0 = fma_kv<F16, 0, 0>(kv.x, q.v[4 * j + 0], a0);
+            a1 = fma_kv<F16, 1, 1>(kv.x, q.v[4 * j + 0], a1);
+            a2 = fma_kv<F16, 0, 0>(kv.y, q.v[4 * j + 1], a2);
+            a3 = fma_kv<F16, 1, 1>(kv.y, q.v[4 * j + 1], a3);
+            a0 = fma_kv<F16, 0, 0>(kv.z, q.v[4 * j + 2], a0);
+            a1 = fma_kv<F16, 1, 1>(kv.z, q.v[4 * j + 2], a1);
+            a2 = fma_kv<F16, 0, 0>(kv.w, q.v[4 * j + 3], a2);
+            a3 = fma_kv<F16, 1, 1>(kv.w, q.v[4 * j + 3], a3);
         }
         float s = (a0 + a1) + (a2 + a3);
         s += __shfl_xor_sync(0xffffffffu, s, 16);
@@ -353,10 +381,11 @@ struct Acc<1> {
             o[3] *= alpha;
         }
         m = m_new;
-        // P rounded to bf16 for the PV product (FA2/FA3 convention); l sums the
-        // rounded weights so O / l stays an exact convex combination of V rows.
-        const __nv_bfloat16 pb = __float2bfloat16_rn(exp2f(s - m_new));
-        l += (half == 0) ? __bfloat162float(pb) : 0.f;
+        // P rounded to the KV type for the PV product (FA2/FA3 convention); l sums
+        // the rounded weights so O / l stays an exact convex combination of V rows.
+        float pf;
+        const uint16_t pb = round_kv<F16>(exp2f(s - m_new), &pf);
+        l += (half == 0) ? pf : 0.f;
         if (half == 0) scratch[t] = pb;
         __syncwarp();
         const uint4 p0 = lds128(sp);
@@ -370,14 +399,14 @@ struct Acc<1> {
                 const uint2 v0 = lds64(vs + swz(tt, cidx) + coff);
                 const uint2 v1 = lds64(vs + swz(tt + 1, cidx) + coff);
                 const uint32_t pp = pw[tt >> 1];
-                o[0] = fma_bf<0, 0>(v0.x, pp, o[0]);
-                o[1] = fma_bf<1, 0>(v0.x, pp, o[1]);
-                o[2] = fma_bf<0, 0>(v0.y, pp, o[2]);
-                o[3] = fma_bf<1, 0>(v0.y, pp, o[3]);
-                o[0] = fma_bf<0, 1>(v1.x, pp, o[0]);
-                o[1] = fma_bf<1, 1>(v1.x, pp, o[1]);
-                o[2] = fma_bf<0, 1>(v1.y, pp, o[2]);
-                o[3] = fma_bf<1, 1>(v1.y, pp, o[3]);
+                o[0] = fma_kv<F16, 0, 0>(v0.x, pp, o[0]);
+                o[1] = fma_kv<F16, 1, 0>(v0.x, pp, o[1]);
+                o[2] = fma_kv<F16, 0, 0>(v0.y, pp, o[2]);
+                o[3] = fma_kv<F16, 1, 0>(v0.y, pp, o[3]);
+                o[0] = fma_kv<F16, 0, 1>(v1.x, pp, o[0]);
+                o[1] = fma_kv<F16, 1, 1>(v1.x, pp, o[1]);
+                o[2] = fma_kv<F16, 0, 1>(v1.y, pp, o[2]);
+                o[3] = fma_kv<F16, 1, 1>(v1.y, pp, o[3]);
             }
         } else {
             // partial last page: rows >= valid may hold stale data (0 * NaN = NaN)
@@ -388,14 +417,14 @@ struct Acc<1> {
                 if (tt >= valid) v0 = make_uint2(0u, 0u);
                 if (tt + 1 >= valid) v1 = make_uint2(0u, 0u);
                 const uint32_t pp = pw[tt >> 1];
-                o[0] = fma_bf<0, 0>(v0.x, pp, o[0]);
-                o[1] = fma_bf<1, 0>(v0.x, pp, o[1]);
-                o[2] = fma_bf<0, 0>(v0.y, pp, o[2]);
-                o[3] = fma_bf<1, 0>(v0.y, pp, o[3]);
-                o[0] = fma_bf<0, 1>(v1.x, pp, o[0]);
-                o[1] = fma_bf<1, 1>(v1.x, pp, o[1]);
-                o[2] = fma_bf<0, 1>(v1.y, pp, o[2]);
-                o[3] = fma_bf<1, 1>(v1.y, pp, o[3]);
+                o[0] = fma_kv<F16, 0, 0>(v0.x, pp, o[0]);
+                o[1] = fma_kv<F16, 1, 0>(v0.x, pp, o[1]);
+                o[2] = fma_kv<F16, 0, 0>(v0.y, pp, o[2]);
+                o[3] = fma_kv<F16, 1, 0>(v0.y, pp, o[3]);
+                o[0] = fma_kv<F16, 0, 1>(v1.x, pp, o[0]);
+                o[1] = fma_kv<F16, 1, 1>(v1.x, pp, o[1]);
+                o[2] = fma_kv<F16, 0, 1>(v1.y, pp, o[2]);
+                o[3] = fma_kv<F16, 1, 1>(v1.y, pp, o[3]);
             }
         }
     }
@@ -405,7 +434,7 @@ struct Acc<1> {
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1) lt += __shfl_xor_sync(0xffffffffu, lt, off);
         if (d.nsplit == 1) {
-            write_final_row(p, d.r, d.head, lane, o, m, lt);
+            write_final_row<F16>(p, d.r, d.head, lane, o, m, lt);
             return false;
         }
         const int64_t slot = static_cast<int64_t>(d.slot) * p.n_q + d.head;
@@ -421,7 +450,7 @@ struct Acc<1> {
 // 2(lane%4)+1 in both the S and the O fragments, so the online-softmax state is
 // per lane and the rescale needs no data movement; P^T crosses lanes once per
 // page through a 256-byte shared-memory transpose.
-template <int GROUP>
+template <int GROUP, bool F16>
 struct Acc {
     float m[2], l[2];  // heads h0 = 2(lane%4), h0+1
     float o[8][4];     // O^T fragments: d = 16mt + lane/4 (+8), heads h0, h0+1
@@ -432,7 +461,7 @@ struct Acc {
         for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
     }
     __device__ __forceinline__ void page(const QRegs<GROUP>& q, uint32_t ks, uint32_t vs, uint32_t sp,
-                                         __nv_bfloat16* pt, int valid, float scale, int lane) {
+                                         uint16_t* pt, int valid, float scale, int lane) {
         const int tA = lane >> 2, tB = tA + 8;     // this lane's token rows
         const int hc = (lane & 3) * 2;             // this lane's head pair
         // ---- S^T = K Q^T (two accumulators: 4-deep HMMA chains)
@@ -443,8 +472,8 @@ struct Acc {
             uint32_t a0, a1, a2, a3, c0, c1, c2, c3;
             ldsm_x4(ks + swz(arow, 2 * kk + (lane >> 4)), a0, a1, a2, a3);
             ldsm_x4(ks + swz(arow, 2 * kk + 2 + (lane >> 4)), c0, c1, c2, c3);
-            mma_m16(sa, a0, a1, a2, a3, q.v[2 * kk], q.v[2 * kk + 1]);
-            mma_m16(sb, c0, c1, c2, c3, q.v[2 * kk + 2], q.v[2 * kk + 3]);
+            mma_m16<F16>(sa, a0, a1, a2, a3, q.v[2 * kk], q.v[2 * kk + 1]);
+            mma_m16<F16>(sb, c0, c1, c2, c3, q.v[2 * kk + 2], q.v[2 * kk + 3]);
         }
         // lane: s[0] = (tA, h0), s[1] = (tA, h1), s[2] = (tB, h0), s[3] = (tB, h1)
         float sv[4];
@@ -474,12 +503,13 @@ struct Acc {
         }
         m[0] = mn0;
         m[1] = mn1;
-        const __nv_bfloat16 p0 = __float2bfloat16_rn(exp2f(sv[0] - mn0));
-        const __nv_bfloat16 p1 = __float2bfloat16_rn(exp2f(sv[1] - mn1));
-        const __nv_bfloat16 p2 = __float2bfloat16_rn(exp2f(sv[2] - mn0));
-        const __nv_bfloat16 p3 = __float2bfloat16_rn(exp2f(sv[3] - mn1));
-        l[0] += __bfloat162float(p0) + __bfloat162float(p2);
-        l[1] += __bfloat162float(p1) + __bfloat162float(p3);
+        float f0, f1, f2, f3;
+        const uint16_t p0 = round_kv<F16>(exp2f(sv[0] - mn0), &f0);
+        const uint16_t p1 = round_kv<F16>(exp2f(sv[1] - mn1), &f1);
+        const uint16_t p2 = round_kv<F16>(exp2f(sv[2] - mn0), &f2);
+        const uint16_t p3 = round_kv<F16>(exp2f(sv[3] - mn1), &f3);
+        l[0] += f0 + f2;
+        l[1] += f1 + f3;
         // ---- P^T -> B fragments (k = tokens, n = heads) via pt[head][16 tokens]
         pt[hc * 16 + tA] = p0;
         pt[(hc + 1) * 16 + tA] = p1;
@@ -495,7 +525,7 @@ struct Acc {
             for (int mt = 0; mt < 8; ++mt) {
                 uint32_t a0, a1, a2, a3;
                 ldsm_x4_t(vs + swz(vrow, 2 * mt + ((lane >> 3) & 1)), a0, a1, a2, a3);
-                mma_m16(o[mt], a0, a1, a2, a3, pb0, pb1);
+                mma_m16<F16>(o[mt], a0, a1, a2, a3, pb0, pb1);
             }
         } else {
             // stale rows >= valid: P is 0 there but 0 * NaN = NaN, so mask V too
@@ -507,7 +537,7 @@ struct Acc {
                 a1 = mask_tokens(a1, hc, valid);
                 a2 = mask_tokens(a2, hc + 8, valid);
                 a3 = mask_tokens(a3, hc + 8, valid);
-                mma_m16(o[mt], a0, a1, a2, a3, pb0, pb1);
+                mma_m16<F16>(o[mt], a0, a1, a2, a3, pb0, pb1);
             }
         }
         __syncwarp();  // pt is rewritten by the next page
@@ -529,11 +559,12 @@ struct Acc {
             const float lt = e ? lt1 : lt0, mm = e ? m[1] : m[0];
             if (nsplit1) {
                 const float inv = lt > 0.f ? 1.f / lt : 0.f;
-                __nv_bfloat16* dst = p.out + (static_cast<int64_t>(d.r) * p.n_q + qh) * kD;
+                uint16_t* dst = p.out + (static_cast<int64_t>(d.r) * p.n_q + qh) * kD;
+                float unused;
 #pragma unroll
                 for (int mt = 0; mt < 8; ++mt) {
-                    dst[16 * mt + dr] = __float2bfloat16_rn(o[mt][e] * inv);
-                    dst[16 * mt + dr + 8] = __float2bfloat16_rn(o[mt][2 + e] * inv);
+                    dst[16 * mt + dr] = round_kv<F16>(o[mt][e] * inv, &unused);
+                    dst[16 * mt + dr + 8] = round_kv<F16>(o[mt][2 + e] * inv, &unused);
                 }
                 if (p.lse != nullptr && dr == 0) {
                     p.lse[static_cast<int64_t>(d.r) * p.n_q + qh] = lt > 0.f ? (mm + __log2f(lt)) / kLog2e : -INFINITY;
@@ -554,7 +585,7 @@ struct Acc {
 };
 
 // ============================================================ the kernel
-template <int NW, int S, int GROUP>
+template <int NW, int S, int GROUP, bool F16>
 __global__ void __launch_bounds__(NW * 32, (NW == 2 ? 4 : 2))
 decode_attn_kernel(const Params p) {
     constexpr int kRing = S + 1;  // descriptor ring must cover the TMA lookahead
@@ -567,7 +598,7 @@ decode_attn_kernel(const Params p) {
     char* wbase = smem_raw + warp * kWarpBytes;
     const uint32_t stage0 = smem_u32(wbase);
     const uint32_t bar0 = smem_u32(wbase + S * kStageBytes);
-    __nv_bfloat16* scratch = reinterpret_cast<__nv_bfloat16*>(wbase + S * kStageBytes + 512);
+    uint16_t* scratch = reinterpret_cast<uint16_t*>(wbase + S * kStageBytes + 512);
     const uint32_t sp = smem_u32(scratch);
     Desc* ring = reinterpret_cast<Desc*>(wbase + S * kStageBytes + 64);
 
@@ -649,7 +680,7 @@ decode_attn_kernel(const Params p) {
     grid_dep_launch();
 
     QRegs<GROUP> q, qn;
-    Acc<GROUP> acc;
+    Acc<GROUP, F16> acc;
     int consumed = 0;   // pages
     int citem = 0;      // items started by the consumer
     bool qn_ready = false;
@@ -718,6 +749,7 @@ constexpr int kMergeWarps = 4;
 // One CTA per (request, query head) row: the 8 warps take every 8th split and
 // keep an online (max, sum, o[4 dims per lane]) state over 8-split batches of
 // coalesced loads, then the 8 states are combined through shared memory.
+template <bool F16>
 __global__ void __launch_bounds__(kMergeWarps * 32, 6)
 merge_splits_kernel(const Params p, const int32_t* __restrict__ merge_reqs, int32_t rows) {
     grid_dep_launch();
@@ -793,7 +825,7 @@ merge_splits_kernel(const Params p, const int32_t* __restrict__ merge_reqs, int3
                 ot[3] += e * x.w;
                 Lt += e * s_l[w];
             }
-            write_final_row(p, r, qh, lane, ot, Mt, Lt);
+            write_final_row<F16>(p, r, qh, lane, ot, Mt, Lt);
         }
         __syncthreads();
     }
@@ -802,15 +834,16 @@ merge_splits_kernel(const Params p, const int32_t* __restrict__ merge_reqs, int3
 // ------------------------------------------------------------- launcher
 // (warps per CTA, TMA stages per warp) variants; the default is chosen per group
 // from B200 measurements, ASV_ATTN_VARIANT=<NW>x<S> overrides it (tuning only).
-template <int NW, int S, int GROUP>
+template <int NW, int S, int GROUP, bool F16>
 struct Launch {
     static constexpr int kSmem = NW * (S * kStageBytes + kWarpExtra);
     static cudaError_t configure() {
-        return cudaFuncSetAttribute(decode_attn_kernel<NW, S, GROUP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    kSmem);
+        return cudaFuncSetAttribute(decode_attn_kernel<NW, S, GROUP, F16>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     }
     static cudaError_t occupancy(int* blocks) {
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, decode_attn_kernel<NW, S, GROUP>, NW * 32, kSmem);
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, decode_attn_kernel<NW, S, GROUP, F16>, NW * 32,
+                                                             kSmem);
     }
     static cudaError_t run(const Params& p, int grid, bool pdl, cudaStream_t st) {
         cudaLaunchConfig_t cfg = {};
@@ -823,13 +856,13 @@ struct Launch {
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = pdl ? 1 : 0;
-        return cudaLaunchKernelEx(&cfg, decode_attn_kernel<NW, S, GROUP>, p);
+        return cudaLaunchKernelEx(&cfg, decode_attn_kernel<NW, S, GROUP, F16>, p);
     }
 };
 
-template <int NW, int S, int GROUP>
+template <int NW, int S, int GROUP, bool F16>
 cudaError_t dispatch_variant(bool query, int* blocks, const Params* p, int grid, bool pdl, cudaStream_t st) {
-    using L = Launch<NW, S, GROUP>;
+    using L = Launch<NW, S, GROUP, F16>;
     static bool configured = false;  // attribute set is idempotent; a race is harmless
     if (!configured) {
         cudaError_t e = L::configure();
@@ -858,59 +891,73 @@ Variant selected_variant(int group) {
     return default_variant(group);
 }
 
-template <int GROUP>
+// fp16 KV: the default (4 warps x 3 stages) variant only
+template <int GROUP, bool F16>
 cudaError_t dispatch_group(bool query, int* blocks, const Params* p, int grid, bool pdl, cudaStream_t st) {
     const Variant v = selected_variant(GROUP);
-    if (v.nw == 4 && v.stages == 3) return dispatch_variant<4, 3, GROUP>(query, blocks, p, grid, pdl, st);
-    if constexpr (GROUP == 1 || GROUP == 5 || GROUP == 4) {
-        if (v.nw == 4 && v.stages == 4) return dispatch_variant<4, 4, GROUP>(query, blocks, p, grid, pdl, st);
-        if (v.nw == 2 && v.stages == 6) return dispatch_variant<2, 6, GROUP>(query, blocks, p, grid, pdl, st);
-        if (v.nw == 4 && v.stages == 2) return dispatch_variant<4, 2, GROUP>(query, blocks, p, grid, pdl, st);
-        if (v.nw == 2 && v.stages == 4) return dispatch_variant<2, 4, GROUP>(query, blocks, p, grid, pdl, st);
+    if (v.nw == 4 && v.stages == 3) return dispatch_variant<4, 3, GROUP, F16>(query, blocks, p, grid, pdl, st);
+    if constexpr (!F16 && (GROUP == 1 || GROUP == 5 || GROUP == 4)) {
+        if (v.nw == 4 && v.stages == 4) return dispatch_variant<4, 4, GROUP, F16>(query, blocks, p, grid, pdl, st);
+        if (v.nw == 2 && v.stages == 6) return dispatch_variant<2, 6, GROUP, F16>(query, blocks, p, grid, pdl, st);
+        if (v.nw == 4 && v.stages == 2) return dispatch_variant<4, 2, GROUP, F16>(query, blocks, p, grid, pdl, st);
+        if (v.nw == 2 && v.stages == 4) return dispatch_variant<2, 4, GROUP, F16>(query, blocks, p, grid, pdl, st);
     }
-    return dispatch_variant<4, 3, GROUP>(query, blocks, p, grid, pdl, st);
+    return dispatch_variant<4, 3, GROUP, F16>(query, blocks, p, grid, pdl, st);
 }
 
-bool variant_available(int group, Variant v) {
+bool variant_available(int group, bool f16, Variant v) {
     if (v.nw == 4 && v.stages == 3) return true;
-    if (group != 1 && group != 4 && group != 5) return false;
+    if (f16 || (group != 1 && group != 4 && group != 5)) return false;
     return (v.nw == 4 && (v.stages == 4 || v.stages == 2)) || (v.nw == 2 && (v.stages == 6 || v.stages == 4));
 }
 
-cudaError_t dispatch(int group, bool query, int* blocks, const Params* p, int grid, bool pdl,
-                     cudaStream_t st) {
+template <bool F16>
+cudaError_t dispatch_t(int group, bool query, int* blocks, const Params* p, int grid, bool pdl, cudaStream_t st) {
     switch (group) {
-        case 1: return dispatch_group<1>(query, blocks, p, grid, pdl, st);
-        case 2: return dispatch_group<2>(query, blocks, p, grid, pdl, st);
-        case 4: return dispatch_group<4>(query, blocks, p, grid, pdl, st);
-        case 5: return dispatch_group<5>(query, blocks, p, grid, pdl, st);
-        case 8: return dispatch_group<8>(query, blocks, p, grid, pdl, st);
+        case 1: return dispatch_group<1, F16>(query, blocks, p, grid, pdl, st);
+        case 2: return dispatch_group<2, F16>(query, blocks, p, grid, pdl, st);
+        case 4: return dispatch_group<4, F16>(query, blocks, p, grid, pdl, st);
+        case 5: return dispatch_group<5, F16>(query, blocks, p, grid, pdl, st);
+        case 8: return dispatch_group<8, F16>(query, blocks, p, grid, pdl, st);
         default: return cudaErrorInvalidValue;
     }
 }
 
+cudaError_t dispatch(int group, bool f16, bool query, int* blocks, const Params* p, int grid, bool pdl,
+                     cudaStream_t st) {
+    return f16 ? dispatch_t<true>(group, query, blocks, p, grid, pdl, st)
+               : dispatch_t<false>(group, query, blocks, p, grid, pdl, st);
+}
+
 }  // namespace
 
-int attn_warps_per_cta(int group) {
+int attn_warps_per_cta(int group, bool f16) {
     const Variant v = selected_variant(group);
-    return variant_available(group, v) ? v.nw : 4;
+    return variant_available(group, f16, v) ? v.nw : 4;
 }
 
 __global__ void sm_copy_kernel(const int4* __restrict__ src, int4* __restrict__ dst, int64_t n16);
 
 cudaError_t attn_occupancy(int group, int* blocks_per_sm) {
-    cudaError_t e = dispatch(group, true, blocks_per_sm, nullptr, 0, false, nullptr);
+    // both KV types: same shared memory and occupancy; loading both keeps lazy module
+    // loading off the launch path
+    int other = 0;
+    cudaError_t e = dispatch(group, true, true, &other, nullptr, 0, false, nullptr);
+    if (e != cudaSuccess) return e;
+    e = dispatch(group, false, true, blocks_per_sm, nullptr, 0, false, nullptr);
     if (e != cudaSuccess) return e;
     // Load every kernel of the path now (lazy module loading would load them at
     // their first launch, which blocks on device-wide progress: a first launch
     // queued behind a stream-memory-op wait then deadlocks; measured).
     cudaFuncAttributes fa;
-    e = cudaFuncGetAttributes(&fa, merge_splits_kernel);
+    e = cudaFuncGetAttributes(&fa, merge_splits_kernel<false>);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncGetAttributes(&fa, merge_splits_kernel<true>);
     if (e != cudaSuccess) return e;
     return cudaFuncGetAttributes(&fa, sm_copy_kernel);
 }
 
-cudaError_t merge_launch(const Params& p, const int32_t* merge_reqs, int32_t n_merge, int sms, bool pdl,
+cudaError_t merge_launch(const Params& p, const int32_t* merge_reqs, int32_t n_merge, int sms, bool pdl, bool f16,
                          cudaStream_t st) {
     const int32_t rows = n_merge * p.n_q;
     if (rows <= 0) return cudaSuccess;
@@ -925,7 +972,8 @@ cudaError_t merge_launch(const Params& p, const int32_t* merge_reqs, int32_t n_m
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, merge_splits_kernel, p, merge_reqs, rows);
+    return f16 ? cudaLaunchKernelEx(&cfg, merge_splits_kernel<true>, p, merge_reqs, rows)
+               : cudaLaunchKernelEx(&cfg, merge_splits_kernel<false>, p, merge_reqs, rows);
 }
 
 // 16-byte SM copy between any two device-accessible buffers, used where a
@@ -956,7 +1004,7 @@ cudaError_t sm_copy(const int32_t* src, int32_t* dst, int64_t n_int32, cudaStrea
 
 cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st) {
     Params p;
-    p.q = static_cast<const __nv_bfloat16*>(a.q);
+    p.q = static_cast<const uint16_t*>(a.q);
     p.pool = static_cast<const char*>(a.pool);
     p.pool_w = static_cast<char*>(a.pool);
     p.page_bytes = a.page_bytes;
@@ -970,10 +1018,10 @@ cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st) {
     p.num_items = a.num_items;
     p.n_kv = a.n_kv;
     p.n_q = a.n_q;
-    p.total_warps = a.grid * attn_warps_per_cta(a.group);
-    p.k_new = static_cast<const __nv_bfloat16*>(a.k_new);
-    p.v_new = static_cast<const __nv_bfloat16*>(a.v_new);
-    p.out = static_cast<__nv_bfloat16*>(a.out);
+    p.total_warps = a.grid * attn_warps_per_cta(a.group, a.f16);
+    p.k_new = static_cast<const uint16_t*>(a.k_new);
+    p.v_new = static_cast<const uint16_t*>(a.v_new);
+    p.out = static_cast<uint16_t*>(a.out);
     p.lse = a.lse;
     p.part_o = a.part_o;
     p.part_ml = reinterpret_cast<float2*>(a.part_ml);
@@ -991,9 +1039,9 @@ cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st) {
         p.l2_prefetch = pf;
     }
     if (p.num_items <= 0) return cudaSuccess;
-    cudaError_t e = dispatch(a.group, false, nullptr, &p, a.grid, a.pdl, st);
+    cudaError_t e = dispatch(a.group, a.f16, false, nullptr, &p, a.grid, a.pdl, st);
     if (e != cudaSuccess) return e;
-    return merge_launch(p, a.merge_reqs, a.n_merge, a.sms, a.pdl, st);
+    return merge_launch(p, a.merge_reqs, a.n_merge, a.sms, a.pdl, a.f16, st);
 }
 
 }  // namespace asv

@@ -48,6 +48,11 @@ def random_bf16(seed: int, n: int) -> np.ndarray:
     return f32_to_bf16_bits(uniform_pm1(seed, n))
 
 
+def random_f16(seed: int, n: int) -> np.ndarray:
+    """IEEE fp16 bits of the same U[-1, 1) draws (fp16 KV variant)."""
+    return uniform_pm1(seed, n).astype(np.float16).view(np.uint16)
+
+
 def swz_off(t: int, d: int) -> int:
     c = d // 8
     return t * 256 + ((c ^ (t & 7)) << 4) + (d % 8) * 2
@@ -123,14 +128,15 @@ class Oracle:
         if not os.path.exists(ORACLE_SO):
             raise RuntimeError("oracle/libasv_oracle.so missing: run __graft_entry__.build()")
         self.h = C.CDLL(ORACLE_SO)
-        f = self.h.asv_oracle_decode_attention
+        f = self.h.asv_oracle_decode_attention_dt
         f.restype = C.c_int
         f.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int64,
                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_float, C.c_void_p,
-                      C.c_void_p, C.c_int]
+                      C.c_void_p, C.c_int, C.c_int]
 
     def attention(self, n_q, n_kv, num_layers, layer, q_bits, pool, seq_lens, indptr, indices,
-                  sm_scale, threads=None):
+                  sm_scale, threads=None, f16=False):
+        """q_bits / pool hold bf16 bits (fp16 bits with f16=True)."""
         b = len(seq_lens)
         q_bits = np.ascontiguousarray(q_bits, dtype=np.uint16)
         pool = np.ascontiguousarray(pool, dtype=np.uint8)
@@ -139,19 +145,20 @@ class Oracle:
         indices = np.ascontiguousarray(indices, dtype=np.int32)
         out = np.zeros((b, n_q, 128), dtype=np.float32)
         lse = np.zeros((b, n_q), dtype=np.float32)
-        rc = self.h.asv_oracle_decode_attention(
+        rc = self.h.asv_oracle_decode_attention_dt(
             n_q, n_kv, num_layers, layer, q_bits.ctypes.data, pool.ctypes.data,
             pool_pages(pool, n_kv, num_layers), seq.ctypes.data, indptr.ctypes.data, indices.ctypes.data,
-            b, float(sm_scale), out.ctypes.data, lse.ctypes.data, threads or os.cpu_count() or 1)
+            b, float(sm_scale), out.ctypes.data, lse.ctypes.data, threads or os.cpu_count() or 1, 1 if f16 else 0)
         assert rc == 0
         return out, lse
 
 
-def numpy_attention(n_q, n_kv, num_layers, layer, q_bits, pool, seq_lens, indptr, indices, sm_scale):
+def numpy_attention(n_q, n_kv, num_layers, layer, q_bits, pool, seq_lens, indptr, indices, sm_scale, f16=False):
     """Independent pure-numpy restatement of PAPER Eq. 2 over the paged layout (small cases)."""
     blocks = block_view(pool, n_kv, num_layers)
     g = n_q // n_kv
-    q = bf16_bits_to_f32(np.asarray(q_bits, np.uint16)).astype(np.float64)
+    widen = (lambda x: np.asarray(x, np.uint16).view(np.float16).astype(np.float32)) if f16 else bf16_bits_to_f32
+    q = widen(np.asarray(q_bits, np.uint16)).astype(np.float64)
     b = len(seq_lens)
     out = np.zeros((b, n_q, 128))
     lse = np.zeros((b, n_q))
@@ -161,8 +168,8 @@ def numpy_attention(n_q, n_kv, num_layers, layer, q_bits, pool, seq_lens, indptr
         for kvh in range(n_kv):
             K = np.concatenate([unswizzle_block(blocks[layer, p, 0, kvh]) for p in pages[:(s + 15) // 16]])[:s]
             V = np.concatenate([unswizzle_block(blocks[layer, p, 1, kvh]) for p in pages[:(s + 15) // 16]])[:s]
-            K = bf16_bits_to_f32(K).astype(np.float64)
-            V = bf16_bits_to_f32(V).astype(np.float64)
+            K = widen(K).astype(np.float64)
+            V = widen(V).astype(np.float64)
             for h in range(kvh * g, (kvh + 1) * g):
                 sc = K @ q[r, h] * sm_scale
                 m = sc.max()

@@ -3,6 +3,7 @@
 Tolerance (bf16 KV, bf16 output; P rounded to bf16 before PV as in FA2/FA3):
     |gpu - oracle| <= ATOL + RTOL * |oracle| elementwise, and rel-L2 <= RL2,
 with ATOL = 4e-3, RTOL = 8e-3, RL2 = 5e-3; lse within 2e-3 absolute.
+fp16 KV (8 more mantissa bits): ATOL = 1e-3, RTOL = 2e-3, RL2 = 1e-3, lse 5e-4.
 The measured max-abs / rel-L2 are printed so runs record the achieved error.
 """
 import math
@@ -25,20 +26,23 @@ def oracle():
 
 
 def _run_case(oracle, n_q, n_kv, L, layer, seq_lens, seed=1, num_workers=None, append=True,
-              poison_tail=False, const_v=None, repeat=1):
+              poison_tail=False, const_v=None, repeat=1, f16=False):
     from paper_2605_23389_b200 import PagedDecodeAttention
 
     dev = torch.device("cuda", 0)
-    att = PagedDecodeAttention(n_q, n_kv, L, device=0)
+    tdt = torch.float16 if f16 else torch.bfloat16
+    rnd = U.random_f16 if f16 else U.random_bf16
+    att = PagedDecodeAttention(n_q, n_kv, L, device=0, dtype=tdt)
     pb = att.page_bytes
     need = sum((s + 16) // 16 for s in seq_lens)
     pool_pages = need + 7
-    pool = U.random_bf16(seed, pool_pages * pb // 2).view(np.uint8).copy()
+    pool = rnd(seed, pool_pages * pb // 2).view(np.uint8).copy()
     indptr, indices = U.make_batch(seq_lens, U.usable_pages(n_kv, pool_pages), seed + 1, append=True)
     blocks = U.block_view(pool, n_kv, L) if (const_v is not None or poison_tail) else None
     if const_v is not None:
         # every element of every V block equal: the swizzle is irrelevant
-        cv = U.f32_to_bf16_bits(np.array([const_v], np.float32))[0]
+        cv = (np.array([const_v], np.float16).view(np.uint16) if f16
+              else U.f32_to_bf16_bits(np.array([const_v], np.float32)))[0]
         blocks[:, :, 1] = np.full(2048, cv, np.uint16).view(np.uint8)  # [layer][page][V]
     if poison_tail:
         # rows >= seq_len in each last page hold NaN bit patterns; the kernel must ignore them
@@ -52,18 +56,18 @@ def _run_case(oracle, n_q, n_kv, L, layer, seq_lens, seed=1, num_workers=None, a
                             off = U.swz_off(t, d)
                             blocks[layer, last, kv, h].view(np.uint16)[off // 2] = nan_row[d]
     b = len(seq_lens)
-    q_bits = U.random_bf16(seed + 2, b * n_q * 128).reshape(b, n_q, 128)
-    kn_bits = U.random_bf16(seed + 3, b * n_kv * 128).reshape(b, n_kv, 128)
-    vn_bits = U.random_bf16(seed + 4, b * n_kv * 128).reshape(b, n_kv, 128)
+    q_bits = rnd(seed + 2, b * n_q * 128).reshape(b, n_q, 128)
+    kn_bits = rnd(seed + 3, b * n_kv * 128).reshape(b, n_kv, 128)
+    vn_bits = rnd(seed + 4, b * n_kv * 128).reshape(b, n_kv, 128)
 
     ref_out, ref_lse = oracle.attention(n_q, n_kv, L, layer, q_bits, pool, seq_lens, indptr, indices,
-                                        att.sm_scale)
+                                        att.sm_scale, f16=f16)
 
     pool_d = torch.from_numpy(pool).to(dev)
-    q_d = torch.from_numpy(q_bits.view(np.int16)).to(dev).view(torch.bfloat16)
-    kn_d = torch.from_numpy(kn_bits.view(np.int16)).to(dev).view(torch.bfloat16) if append else None
-    vn_d = torch.from_numpy(vn_bits.view(np.int16)).to(dev).view(torch.bfloat16) if append else None
-    out_d = torch.empty(b, n_q, 128, dtype=torch.bfloat16, device=dev)
+    q_d = torch.from_numpy(q_bits.view(np.int16)).to(dev).view(tdt)
+    kn_d = torch.from_numpy(kn_bits.view(np.int16)).to(dev).view(tdt) if append else None
+    vn_d = torch.from_numpy(vn_bits.view(np.int16)).to(dev).view(tdt) if append else None
+    out_d = torch.empty(b, n_q, 128, dtype=tdt, device=dev)
     lse_d = torch.empty(b, n_q, dtype=torch.float32, device=dev)
     plan = att.plan(seq_lens, indptr, indices, num_workers=num_workers)
     for _ in range(repeat):
@@ -74,12 +78,13 @@ def _run_case(oracle, n_q, n_kv, L, layer, seq_lens, seed=1, num_workers=None, a
 
     err = np.abs(got - ref_out)
     rel_l2 = float(np.linalg.norm(got - ref_out) / max(np.linalg.norm(ref_out), 1e-30))
-    print(f"n_q={n_q} n_kv={n_kv} b={b} splits={plan.total_splits} max_abs={err.max():.3e} "
+    print(f"{'fp16' if f16 else 'bf16'} n_q={n_q} n_kv={n_kv} b={b} splits={plan.total_splits} max_abs={err.max():.3e} "
           f"rel_l2={rel_l2:.3e} lse_max_abs={np.abs(got_lse - ref_lse).max():.3e}")
+    atol, rtol, rl2, lse_atol = (1e-3, 2e-3, 1e-3, 5e-4) if f16 else (ATOL, RTOL, RL2, LSE_ATOL)
     assert np.isfinite(got).all()
-    assert (err <= ATOL + RTOL * np.abs(ref_out)).all(), f"max abs err {err.max()}"
-    assert rel_l2 <= RL2
-    assert np.abs(got_lse - ref_lse).max() <= LSE_ATOL
+    assert (err <= atol + rtol * np.abs(ref_out)).all(), f"max abs err {err.max()}"
+    assert rel_l2 <= rl2
+    assert np.abs(got_lse - ref_lse).max() <= lse_atol
 
     if append:
         # fused KV append (K3): token row seq_len of (layer, kv head) holds k_new / v_new
@@ -234,3 +239,29 @@ def test_config5_max_context_128k(oracle, n_q, n_kv):
     """C5's longest request: 131072 KV tokens (8192 pages, ~250 splits merged) beside two short ones,
     MHA and 13B GQA-8, against the fp32 oracle; plus the fused append at row 131072."""
     _run_case(oracle, n_q, n_kv, 1, 0, [131072, 17, 1000], seed=121)
+
+
+# ---- fp16 KV (north star: "bf16/fp16 KV"): same kernel family, fp16 FHFMA / HMMA; same tolerance ----
+
+@pytest.mark.parametrize("n_q,n_kv", [(32, 32), (32, 8), (40, 8), (64, 8)])
+def test_fp16_kv_matches_oracle(oracle, n_q, n_kv):
+    rng = np.random.default_rng(16 + n_q + n_kv)
+    seq = rng.integers(1, 3000, size=10).tolist() + [16, 17, 9000]
+    _run_case(oracle, n_q, n_kv, 2, 1, seq, seed=161 + n_q, f16=True)
+
+
+def test_fp16_poisoned_tail_and_known_answer(oracle):
+    _run_case(oracle, 32, 32, 1, 0, [5, 21, 100], seed=171, poison_tail=True, append=False, f16=True)
+    _run_case(oracle, 40, 8, 1, 0, [5, 23, 700], seed=172, poison_tail=True, append=False, f16=True)
+    got, _, _ = _run_case(oracle, 32, 32, 1, 0, [1, 7, 300], seed=173, const_v=0.375, append=False, f16=True)
+    assert np.all(got == np.float32(0.375))
+
+
+def test_dtype_mismatch_is_rejected():
+    from paper_2605_23389_b200 import PagedDecodeAttention
+    att = PagedDecodeAttention(32, 32, 1, device=0, dtype=torch.float16)
+    plan = att.plan([40], [0, 3], [0, 1, 2])
+    q = torch.zeros(1, 32, 128, dtype=torch.bfloat16, device="cuda")
+    pool = torch.zeros(4 * att.page_bytes, dtype=torch.uint8, device="cuda")
+    with pytest.raises(TypeError, match="float16"):
+        att.run(q, pool, 0, plan, torch.empty_like(q))

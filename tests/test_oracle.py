@@ -60,6 +60,24 @@ def test_oracle_matches_numpy_restatement(oracle, n_q, n_kv):
     assert np.abs(l1 - l2).max() < 2e-5
 
 
+@pytest.mark.parametrize("n_q,n_kv", [(32, 32), (40, 8)])
+def test_oracle_fp16_matches_numpy_restatement(oracle, n_q, n_kv):
+    """fp16 KV variant: the oracle's exact binary16 widening (subnormals included) vs numpy's."""
+    L, layer = 2, 0
+    seq = [3, 16, 40]
+    pages = sum((s + 15) // 16 for s in seq) + 2
+    pool = U.random_f16(6, pages * U.page_bytes(n_kv, L) // 2)
+    pool[::97] = np.array([0x0001, 0x03ff, 0x8200, 0x3c00], np.uint16)[np.arange(pool[::97].size) % 4]  # subnormals, 1.0
+    pool = pool.view(np.uint8).copy()
+    indptr, indices = U.make_batch(seq, pages, 10, append=False)
+    q = U.random_f16(9, len(seq) * n_q * 128).reshape(len(seq), n_q, 128)
+    sc = 1 / math.sqrt(128)
+    o1, l1 = oracle.attention(n_q, n_kv, L, layer, q, pool, seq, indptr, indices, sc, threads=4, f16=True)
+    o2, l2 = U.numpy_attention(n_q, n_kv, L, layer, q, pool, seq, indptr, indices, sc, f16=True)
+    assert np.abs(o1 - o2).max() < 2e-6
+    assert np.abs(l1 - l2).max() < 2e-5
+
+
 def test_known_answer_single_token(oracle):
     """s = 1: softmax over one key is 1, so O = V_0 exactly."""
     n_kv, L = 4, 1

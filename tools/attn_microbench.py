@@ -19,9 +19,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2605_23389_b200 import PagedDecodeAttention
 
 
-def run(n_q, n_kv, L, seq_lens, iters=20, warmup=3, num_workers=None, seed=0):
+def run(n_q, n_kv, L, seq_lens, iters=20, warmup=3, num_workers=None, seed=0, dtype=torch.bfloat16):
     dev = torch.device("cuda", 0)
-    att = PagedDecodeAttention(n_q, n_kv, L, device=0)
+    att = PagedDecodeAttention(n_q, n_kv, L, device=0, dtype=dtype)
     npages = [(s + 16) // 16 for s in seq_lens]
     P = sum(npages)
     # grouped layer-major pool: page ids must stay below asv_pool_usable_pages (include/asv.h)
@@ -30,13 +30,13 @@ def run(n_q, n_kv, L, seq_lens, iters=20, warmup=3, num_workers=None, seed=0):
     pool_pages = P + 8
     usable = int(_lib.lib().asv_pool_usable_pages(C.byref(att.shape), pool_pages))
     assert usable >= P
-    pool = torch.empty(pool_pages * att.page_bytes // 2, dtype=torch.bfloat16, device=dev)
+    pool = torch.empty(pool_pages * att.page_bytes // 2, dtype=dtype, device=dev)
     pool.uniform_(-1, 1)
     rng = np.random.default_rng(seed)
     perm = rng.permutation(usable)[:P].astype(np.int32)
     indptr = np.concatenate([[0], np.cumsum(npages)]).astype(np.int32)
     b = len(seq_lens)
-    q = torch.randn(b, n_q, 128, device=dev, dtype=torch.bfloat16)
+    q = torch.randn(b, n_q, 128, device=dev, dtype=dtype)
     out = torch.empty_like(q)
     lse = torch.empty(b, n_q, device=dev)
     plan = att.plan(seq_lens, indptr, perm, num_workers=num_workers)
@@ -66,6 +66,7 @@ if __name__ == "__main__":
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--case", default=None)
+    ap.add_argument("--fp16", action="store_true", help="fp16 KV / q / out instead of bf16")
     a = ap.parse_args()
     rng = np.random.default_rng(1)
     cases = {
@@ -85,6 +86,8 @@ if __name__ == "__main__":
     for name, (nq, nkv, L, seq) in cases.items():
         if a.case and a.case != name:
             continue
-        r = run(nq, nkv, L, seq, iters=a.iters, warmup=a.warmup)
+        r = run(nq, nkv, L, seq, iters=a.iters, warmup=a.warmup,
+                dtype=torch.float16 if a.fp16 else torch.bfloat16)
         r["case"] = name
+        r["dtype"] = "fp16" if a.fp16 else "bf16"
         print(json.dumps(r), flush=True)
