@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -169,7 +170,12 @@ int asv_attn_plan_build(const asv_attn_shape* shape, int32_t batch, const int32_
     std::vector<int32_t> best_ns(static_cast<size_t>(batch), 1), ns(static_cast<size_t>(batch));
     double best = -1.0;
     static const int kChunks[] = {2, 3, 4, 6, 8, 10, 12, 16, 20, 24, 28, 32};
+    static const int forced_chunk = [] {  // ASV_PLAN_CHUNK=<pages>: tuning experiments only
+        const char* e = getenv("ASV_PLAN_CHUNK");
+        return e != nullptr ? atoi(e) : 0;
+    }();
     for (const int c : kChunks) {
+        if (forced_chunk > 0 && c != forced_chunk) continue;
         double total = 0.0;
         int max_item = 0;
         for (int r = 0; r < batch; ++r) {

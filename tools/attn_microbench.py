@@ -76,6 +76,7 @@ if __name__ == "__main__":
         "C4_13b_gqa8_b32": (40, 8, 40, rng.integers(1024, 8192, 32).tolist()),
         "gqa_7b_b64": (32, 8, 32, rng.integers(1024, 4096, 64).tolist()),
         "mha_b1_128k": (32, 32, 4, [131072]),
+        "C2_step_b4_1k-16k": (32, 32, 32, rng.integers(1024, 16385, 4).tolist()),
         # same launches with one layer per page: page stride 64 KiB / 256 KiB instead of
         # 2.5 MiB / 8 MiB (probes address-stride / TLB effects of the all-layers page)
         "C4_13b_gqa8_b32_L1": (40, 8, 1, None),
