@@ -284,46 +284,52 @@ def main():
         else:
             run_kw.update(prefetch_device=dev + 1)
         idle = d.rank % 2 == 1
-    real_run = E.engine_run
 
-    def engine_run(cfg_, **kw):
+    def run_engine(cfg_, **kw):
+        """asv_engine_run on this rank's GPU(s); a pair's prefetch rank runs nothing (zero stats)."""
         if idle:
             from paper_2605_23389_b200 import _lib
             return _lib.EngineStats().as_dict()
-        return real_run(cfg_, **kw)
-    E = argparse.Namespace(engine_run=engine_run)
+        return E.engine_run(cfg_, **kw)
     d.barrier()
     with ClockSampler(dev) as clk:
-        res = E.engine_run(cfg, execute_transfers=False, **run_kw)
+        res = run_engine(cfg, execute_transfers=False, **run_kw)
     clocks = clk.summary()
     d.barrier()
     # the whole decoder layer stack per step (RMSNorm, QKV+RoPE / O / gate-up / down GEMMs on
     # tcgen05 with synthetic weights, attention), KV resident: SURVEY §8(f) rank 1
     full = None
     if not args.no_full_step:
-        full = E.engine_run(cfg, execute_transfers=False, full_step=True, **run_kw)
+        full = run_engine(cfg, execute_transfers=False, full_step=True, **run_kw)
         d.barrier()
     e2e = None
     if not args.no_e2e:
         ek = max(K, E2E_MIN_STEPS)
         kw = dict(run_kw, exec_end=S + W + ek)
-        e2e = E.engine_run(cfg, execute_transfers=True, copy_begin=max(0, S - COPY_LEAD), **kw)
+        e2e = run_engine(cfg, execute_transfers=True, copy_begin=max(0, S - COPY_LEAD), **kw)
         d.barrier()
         # the same (longer) window with the KV resident: what the e2e run would reach without the link
-        e2e_res = E.engine_run(cfg, execute_transfers=False, **kw)
+        e2e_res = run_engine(cfg, execute_transfers=False, **kw)
         d.barrier()
         # end to end with the whole decoder layer stack per step: decode work long enough to hide the
         # KV prefetch behind it
         e2e_full = None
         if not args.no_full_step:
-            e2e_full = E.engine_run(cfg, execute_transfers=True, copy_begin=max(0, S - COPY_LEAD), full_step=True,
+            e2e_full = run_engine(cfg, execute_transfers=True, copy_begin=max(0, S - COPY_LEAD), full_step=True,
                                     **kw)
             d.barrier()
         # the same window with the prefill instance colocated on this GPU: every prefill_offload
         # (prefill GPU -> host pool) is a real D2H copy sharing this GPU's PCIe link with the prefetches
+        # the pair data path on this one device: candidate buffers in their own pool, every admit /
+        # evict a real device copy on the pair's P2P lane (the NVLink push of a 2-GPU pair)
+        e2e_pair1 = None
+        if not pairs and d.world == 1:
+            e2e_pair1 = run_engine(cfg, execute_transfers=True, copy_begin=max(0, S - COPY_LEAD), pair_mode=True,
+                                   **kw)
+            d.barrier()
         e2e_colo = None
         if not pairs:  # a pair already runs its prefill offloads on the prefetch GPU's link
-            e2e_colo = E.engine_run(cfg, execute_transfers=True, copy_begin=max(0, S - COPY_LEAD),
+            e2e_colo = run_engine(cfg, execute_transfers=True, copy_begin=max(0, S - COPY_LEAD),
                                     prefill_offload=True, **kw)
             d.barrier()
 
@@ -377,6 +383,18 @@ def main():
                     "copy into the host pool over this GPU's own PCIe link (prefill instance colocated); the "
                     "headline e2e leaves it to the prefill instance's link, as the reference's disaggregated "
                     "model does"}
+
+    if e2e is not None and e2e_pair1 is not None:
+        pw = e2e_pair1["window_ms"]
+        ps = max(1, e2e_pair1["iterations_timed"])
+        e2e_obj["pair_path_one_device"] = {
+            "value": e2e_pair1["tokens_timed"] / (pw / 1e3) if pw > 0 else 0.0, "unit": "tokens/s",
+            "p2p_bytes_per_step": int(e2e_pair1["p2p_bytes_window"] / ps),
+            "p2p_copy_gbps": (e2e_pair1["p2p_bytes_window"] / (e2e_pair1["p2p_busy_ms"] * 1e-3) / 1e9
+                              if e2e_pair1["p2p_busy_ms"] > 0 else None),
+            "what": "same window with the (prefetch, decode) pair's data path on this one GPU: admits / evicts "
+                    "are device copies between the candidate-buffer pool and the decode pool on the P2P lane "
+                    "(HBM to HBM here; NVLink peer copies with two GPUs, roofline 770 GB/s)"}
 
     peak, peak_src = measured_peaks()
     achieved = res["attn_bytes"] / (res["attn_ms"] * 1e-3) / 1e9 if res["attn_ms"] > 0 else 0.0

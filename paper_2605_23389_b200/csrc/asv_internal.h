@@ -77,6 +77,13 @@ cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st);
 // n_int32 rounded up to a multiple of 4 (16-byte units); both pointers 16-byte aligned
 cudaError_t sm_copy(const int32_t* src, int32_t* dst, int64_t n_int32, cudaStream_t st);
 
+// device-to-device KV page moves on the SMs (kv_move.cu): pages per launch (kernel parameter arrays)
+constexpr int kMoveChunk = 1024;
+cudaError_t kv_move_launch(const void* src_pool, int64_t src_gp, void* dst_pool, int64_t dst_gp, int64_t slice,
+                           int32_t layers, const int32_t* src_pages, const int32_t* dst_pages, int64_t tokens,
+                           cudaStream_t st);
+cudaError_t kv_move_preload();
+
 // decode-step linear layers (decode_gemm.cu)
 cudaError_t linear_preload();
 cudaError_t rmsnorm_launch(const void* h, const void* gamma, void* out, int dim, int batch, int rows_out, float eps,

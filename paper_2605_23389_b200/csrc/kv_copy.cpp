@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/asv.h"
@@ -141,6 +142,21 @@ int asv_kv_copy_d2d(const asv_attn_shape* shape, void* dst_pool, int64_t dst_poo
     if (int rc = check_pages(dst_pages, npg, dst_pool_pages, g)) return rc;
     if (int rc = check_pages(src_pages, npg, src_pool_pages, g)) return rc;
     const PoolView dv(dst_pool, dst_pool_pages, g), sv(src_pool, src_pool_pages, g);
+    // SM gather/scatter kernel (kv_move.cu): one launch per request; across a pair it pulls over
+    // NVLink through peer pointers.  ASV_D2D_COPY_ENGINE=1 selects per-page copy-engine copies.
+    static const bool copy_engine = [] {
+        const char* e = getenv("ASV_D2D_COPY_ENGINE");
+        return e != nullptr && atoi(e) != 0;
+    }();
+    if (!copy_engine) {
+        if (tokens > 0) {
+            cudaError_t e = kv_move_launch(src_pool, sv.group_pages, dst_pool, dv.group_pages, g.slice,
+                                           static_cast<int32_t>(g.layers), src_pages, dst_pages, tokens, st);
+            if (e != cudaSuccess) return cuda_fail(e, "kv page move");
+        }
+        if (bytes_out) *bytes_out = tokens * g.bps * 256 * g.layers;
+        return ASV_OK;
+    }
     const size_t dp = dv.pitch(), sp = sv.pitch();
     int64_t moved = 0;
     for (int64_t j = 0; j < full; ++j) {

@@ -73,6 +73,33 @@ def main():
         end.synchronize()
         return npages * pb / (beg.elapsed_time(end) * 1e-3) / 1e9
 
+    def d2d(lens):
+        """device -> device request moves between two pools (the pair's admit path, one device)"""
+        pool2 = torch.empty(pool_pages * pb, dtype=torch.uint8, device=dev)
+        total = 0
+        beg, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        beg.record(st)
+        for s in lens:
+            npg = (s + 15) // 16
+            sp = rng.permutation(pool_pages)[:npg].astype(np.int32)
+            dp = rng.permutation(pool_pages)[:npg].astype(np.int32)
+            moved = C.c_int64(0)
+            _lib.check(h.asv_kv_copy_d2d(C.byref(shape), pool2.data_ptr(), pool_pages, 0,
+                                         dp.ctypes.data_as(C.POINTER(C.c_int32)), pool.data_ptr(), pool_pages, 0,
+                                         sp.ctypes.data_as(C.POINTER(C.c_int32)), s, st.cuda_stream, C.byref(moved)))
+            total += moved.value
+        end.record(st)
+        end.synchronize()
+        del pool2
+        return round(total / (beg.elapsed_time(end) * 1e-3) / 1e9, 1)
+
+    if os.environ.get("D2D"):
+        d2d([16 * 8] * 4)
+        res["d2d_full_pages_16x256tok"] = d2d([16 * 16] * 16)
+        res["d2d_mixed_1k_8k"] = d2d(rng.integers(1024, 8192, 16).tolist())
+        res["d2d_partial_rows"] = d2d([7] * 64)
+        print(json.dumps(res))
+        return
     plain(8)
     res["plain_1d_8MiB_pages_h2d"] = round(plain(256), 2)
     if os.environ.get("QUICK"):
