@@ -57,7 +57,9 @@ def main():
                          "measured_bubble_ms_per_step": st["measured_bubble_ms"] / it,
                          "virtual_bubble_ms_per_step": st["bubble_ms_timed"] / it,
                          "virtual_tok_s_whole_run": st["virtual_decode_tok_s"],
-                         "h2d_gb": st["h2d_bytes_window"] / 1e9, "p2p_gb": st["p2p_bytes_window"] / 1e9}
+                         "h2d_gb": st["h2d_bytes_window"] / 1e9, "p2p_gb": st["p2p_bytes_window"] / 1e9,
+                         "p2p_gbps": (st["p2p_bytes_window"] / (st["p2p_busy_ms"] * 1e-3) / 1e9
+                                      if st["p2p_busy_ms"] > 0 else None)}
             if mode == "full_step":
                 row[mode]["hbm_gbps"] = ((st["attn_bytes"] + st["weight_bytes"]) / (st["window_ms"] * 1e-3) / 1e9
                                          if st["window_ms"] > 0 else 0)
