@@ -56,11 +56,23 @@ def test_splits_cover_every_page_exactly_once(seq):
     assert plan.num_items == plan.total_splits * 32
 
 
-def test_aligned_batch_gets_equal_items():
-    plan, buf, _, _ = build([4096 + i for i in range(16)])
-    sizes = {int(buf[plan.off_desc + g * DESC + 3] - buf[plan.off_desc + g * DESC + 2])
-             for g in range(plan.total_splits)}
-    assert max(sizes) - min(sizes) <= 1
+def test_aligned_batch_gets_two_item_sizes_longest_first():
+    """Length-aligned batch: near-equal head items, then the last quarter of every request in
+    quarter-size tail items; descriptors are ordered longest first (the dynamic LPT schedule)
+    and each request's splits tile its pages exactly."""
+    seq = [4096 + i for i in range(16)]
+    plan, buf, _, _ = build(seq)
+    d = [buf[plan.off_desc + g * DESC: plan.off_desc + g * DESC + 8] for g in range(plan.total_splits)]
+    sizes = [int(x[3] - x[2]) for x in d]
+    assert sizes == sorted(sizes, reverse=True)
+    big = [z for z in sizes if z > sizes[0] // 2]
+    small = [z for z in sizes if z <= sizes[0] // 2]
+    assert max(big) - min(big) <= 1 and small and max(small) - min(small) <= 1
+    assert 3 <= sizes[0] / small[0] <= 5
+    for r, s in enumerate(seq):
+        spans = sorted((int(x[2]), int(x[3])) for x in d if x[0] == r)
+        assert spans[0][0] == 0 and spans[-1][1] == (s + 15) // 16
+        assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
 
 
 def test_gqa_plan_items_per_kv_head():
