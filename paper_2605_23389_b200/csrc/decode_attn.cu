@@ -209,6 +209,12 @@ __device__ __forceinline__ void mma_m16(float* c, uint32_t a0, uint32_t a1, uint
             : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
     }
 }
+// transpose of an 8x8 16-bit matrix held one b32 (two elements) per lane
+__device__ __forceinline__ uint32_t movmatrix_t(uint32_t x) {
+    uint32_t y;
+    asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+    return y;
+}
 // zero the 16-bit halves of a packed pair {token k (lo), token k+1 (hi)} past `valid`
 __device__ __forceinline__ uint32_t mask_tokens(uint32_t b, int k, int valid) {
     if (k >= valid) return 0u;
@@ -510,14 +516,12 @@ struct Acc {
         const uint16_t p3 = round_kv<F16>(exp2f(sv[3] - mn1), &f3);
         l[0] += f0 + f2;
         l[1] += f1 + f3;
-        // ---- P^T -> B fragments (k = tokens, n = heads) via pt[head][16 tokens]
-        pt[hc * 16 + tA] = p0;
-        pt[(hc + 1) * 16 + tA] = p1;
-        pt[hc * 16 + tB] = p2;
-        pt[(hc + 1) * 16 + tB] = p3;
-        __syncwarp();
-        const uint32_t pb0 = *reinterpret_cast<const uint32_t*>(pt + (lane >> 2) * 16 + hc);
-        const uint32_t pb1 = *reinterpret_cast<const uint32_t*>(pt + (lane >> 2) * 16 + 8 + hc);
+        // ---- P^T -> B fragments (k = tokens, n = heads): the S^T accumulator fragment of
+        // tokens 0-7 / 8-15 (row = token lane/4, cols = heads 2(lane%4)..+1) transposed in
+        // registers (movmatrix) is exactly the m16n8k16 B fragment (k = tokens 2(lane%4)..+1,
+        // n = head lane/4) — no shared-memory round trip, no warp barrier
+        const uint32_t pb0 = movmatrix_t(static_cast<uint32_t>(p0) | (static_cast<uint32_t>(p1) << 16));
+        const uint32_t pb1 = movmatrix_t(static_cast<uint32_t>(p2) | (static_cast<uint32_t>(p3) << 16));
         // ---- O^T += V^T P^T over 8 d-tiles of 16
         const int vrow = (lane & 7) + (lane >> 4) * 8;
         if (valid == kPage) {
@@ -540,7 +544,6 @@ struct Acc {
                 mma_m16<F16>(o[mt], a0, a1, a2, a3, pb0, pb1);
             }
         }
-        __syncwarp();  // pt is rewritten by the next page
     }
     __device__ __forceinline__ bool finish(const Params& p, const Desc& d, int lane) {
         float lt0 = l[0], lt1 = l[1];

@@ -83,6 +83,9 @@ if __name__ == "__main__":
         "C2_aligned_b13_8k_L1": (32, 32, 1, None),
     }
     cases["C4_13b_gqa8_b32_L1"] = (40, 8, 1, cases["C4_13b_gqa8_b32"][3])
+    # same KV bytes and work items as C4 with one query head per kv head (FHFMA path):
+    # isolates the GQA tensor-core path's cost from the memory system's
+    cases["C4_shape_mha8_b32"] = (8, 8, 40, cases["C4_13b_gqa8_b32"][3])
     cases["C2_aligned_b13_8k_L1"] = (32, 32, 1, cases["C2_aligned_b13_8k"][3])
     for name, (nq, nkv, L, seq) in cases.items():
         if a.case and a.case != name:
