@@ -175,6 +175,17 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def read_ceiling():
+    """Streaming-read ceiling of the decode kernel's own access pattern (per-warp rings of 4 KiB
+    bulk loads, no compute), measured by tools/hbm_read_probe.py on a B200 (committed profile)."""
+    p = os.path.join(ROOT, "profiles", "hbm_read_probe_r01f.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    v = [x for k, x in d.items() if k.startswith("bulk4k_")]
+    return max(v) if v else None
+
+
 def ncu_traffic():
     """dram bytes per launch of the decode kernel from the committed ncu capture."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -405,6 +416,11 @@ def main():
                 "alg_bytes_per_launch": res["attn_bytes"] / launches,
                 "avg_launch_us": res["attn_ms"] * 1e3 / launches,
                 "frac_of_8TBps": achieved / 8000.0}
+    rc = read_ceiling()
+    if rc:
+        roofline.update({"read_ceiling_gbps": rc, "frac_of_read_ceiling": achieved / rc,
+                         "read_ceiling_source": "profiles/hbm_read_probe_r01f.json (4 KiB bulk-load rings, "
+                                                "no compute; MEASURED_PEAKS is a read+write copy)"})
     prefetch = None
     if e2e is not None:
         # PCIe link: union of the copy intervals of all PCIe lanes inside the window
