@@ -20,7 +20,15 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _bench(topology, port):
+def _free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _bench(topology, port=None):
+    port = port or _free_port()
     env = dict(os.environ, ASV_BENCH_DEVICE="0", ASV_BENCH_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "bench.py"), "--gpus", "2",
@@ -34,14 +42,14 @@ def _bench(topology, port):
 
 
 def test_dp_two_ranks():
-    line = _bench("dp", 29611)
+    line = _bench("dp")
     assert line["n_gpus"] == 2 and line["config"]["parallelism"] == "dp2"
     assert line["value"] > 0 and line["e2e"]["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] > 0
 
 
 def test_pairs_two_ranks():
-    line = _bench("pairs", 29612)
+    line = _bench("pairs")
     assert line["config"]["parallelism"] == "pairs1"
     assert line["value"] > 0 and line["e2e"]["value"] > 0
     assert line["e2e"]["p2p_bytes_per_step"] > 0            # admits moved buffer -> decode pool
