@@ -71,3 +71,17 @@ def test_cli_run_policy_and_nvlink_flags(tmp_path):
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr
     assert json.loads((out2 / "config_used.json").read_text())["cluster"]["nvlink_available"] is False
+
+
+def test_cli_whole_c1_trace_on_the_gpu(tmp_path):
+    """BASELINE C1 end to end: all 2 146 iterations (32-layer attention each) and every KV move
+    (0.62 TB host -> GPU) executed on the B200; the decision log equals the reference's byte for byte."""
+    out = tmp_path / "c1"
+    r = subprocess.run([CLI, "run", "--config", os.path.join(ROOT, "configs", "c1_7b_b16.json"), "--out", str(out),
+                        "--host-pool-mib", "2048"], capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr
+    assert _sha((out / "log.jsonl").read_text()) == GOLDEN["logs"]["c1_7b_b16:aligned"]["sha256"]
+    gs = json.loads((out / "gpu_stats.json").read_text())
+    assert gs["iterations_timed"] == GOLDEN["logs"]["c1_7b_b16:aligned"]["iterations"]
+    lb = gs["logical_bytes"]
+    assert gs["h2d_bytes"] == lb["batch_prefetch"] + lb["stray_prefetch"] > 0
