@@ -57,3 +57,19 @@ def test_error_mapping_matches_reference_exceptions():
         engine.run_config_jsonl({"policy": "aligned"})
     with pytest.raises(RuntimeError, match="unknown policy"):
         engine.run_config_jsonl({"workload": {"count": 1}, "policy": "nope"})
+
+
+def test_header_is_c_and_links(tmp_path):
+    """include/asv.h is a C header: a C translation unit compiles against it, links against
+    libasv.so and runs the GPU-free entry points (what a cgo / JNI / N-API shim does)."""
+    import shutil
+    import subprocess
+    cc = shutil.which("gcc") or "/opt/gcc/bin/gcc"
+    exe = tmp_path / "abi_smoke"
+    pkg = os.path.join(ROOT, "paper_2605_23389_b200")
+    r = subprocess.run([cc, "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "c", "abi_smoke.c"), "-L", pkg, "-lasv",
+                        f"-Wl,-rpath,{pkg}", "-o", str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0 and r.stdout.startswith("ok 8388608"), (r.returncode, r.stdout, r.stderr)
