@@ -173,10 +173,16 @@ int cmd_run(const Args& a) {
               << summary.value("rejected_requests", int64_t(0)) << " rejected, decode throughput "
               << summary.value("decode_throughput_tok_s", 0.0) << " tok/s, TPOT p99 "
               << summary.value("tpot_p99_ms", 0.0) << " ms\n";
-    std::cout << "B200: " << st.iterations_timed << " iterations executed, decode " << measured
-              << " tok/s measured, attention "
-              << (st.attn_ms > 0 ? static_cast<double>(st.attn_bytes) / (st.attn_ms * 1e-3) / 1e9 : 0.0)
-              << " GB/s, KV moved h2d " << st.h2d_bytes << " B, d2h " << st.d2h_bytes + st.offload_bytes << " B, p2p "
+    std::cout << "B200: " << st.iterations_timed << " iterations executed, decode " << measured << " tok/s measured, ";
+    if (o.full_step) {  // the whole decoder layer stack: weights + KV streamed per window time
+        std::cout << "decoder step HBM "
+                  << (st.window_ms > 0 ? static_cast<double>(st.attn_bytes + st.weight_bytes) / (st.window_ms * 1e-3) / 1e9
+                                       : 0.0);
+    } else {
+        std::cout << "attention "
+                  << (st.attn_ms > 0 ? static_cast<double>(st.attn_bytes) / (st.attn_ms * 1e-3) / 1e9 : 0.0);
+    }
+    std::cout << " GB/s, KV moved h2d " << st.h2d_bytes << " B, d2h " << st.d2h_bytes + st.offload_bytes << " B, p2p "
               << st.p2p_bytes << " B\n";
     std::cout << "artifacts in " << dir << "\n";
     return 0;
