@@ -1473,7 +1473,12 @@ std::string stats_to_json(const asv_engine_stats& s) {
         {"window_ms", s.window_ms},
         {"attn_ms", s.attn_ms},
         {"attn_bytes", s.attn_bytes},
-        {"attn_hbm_gbps", s.attn_ms > 0 ? static_cast<double>(s.attn_bytes) / (s.attn_ms * 1e-3) / 1e9 : 0.0},
+        {"attn_hbm_gbps", s.weight_bytes == 0 && s.attn_ms > 0
+                              ? static_cast<double>(s.attn_bytes) / (s.attn_ms * 1e-3) / 1e9 : 0.0},
+        {"weight_bytes", s.weight_bytes},
+        {"decoder_step_hbm_gbps", s.weight_bytes > 0 && s.window_ms > 0
+                                      ? static_cast<double>(s.attn_bytes + s.weight_bytes) / (s.window_ms * 1e-3) / 1e9
+                                      : 0.0},
         {"h2d_bytes", s.h2d_bytes},
         {"d2h_bytes", s.d2h_bytes},
         {"p2p_bytes", s.p2p_bytes},
