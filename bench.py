@@ -454,7 +454,9 @@ def main():
                     "ms_per_step": fwin / f_steps,
                     "what": "per step and layer: RMSNorm, QKV GEMM + RoPE, paged attention + KV append, O GEMM + "
                             "residual, RMSNorm, gate/up GEMM + SiLU, down GEMM + residual (bf16, fp32 accumulate; "
-                            "GEMMs on tcgen05, synthetic Llama-2-7B-shape weights)",
+                            "GEMMs on tcgen05, synthetic Llama-2-7B-shape weights; after layer 0 each RMSNorm is "
+                            "fused into the next GEMM: norm weight folded into its weights, 1/rms per row from the "
+                            "residual GEMM's row sums of squares)",
                     "weight_gb_per_step": full["weight_bytes"] / f_steps / 1e9,
                     "kv_gb_per_step": full["attn_bytes"] / f_steps / 1e9,
                     "hbm_gbps": f_bytes / (full["window_ms"] * 1e-3) / 1e9 if full["window_ms"] > 0 else None,

@@ -233,6 +233,16 @@ typedef struct asv_linear_args {
     int32_t n_q_heads, n_kv_heads;
     int32_t pdl;             /* 1: programmatic dependent launch — W streams into the ring while the
                                 previous kernel on the stream finishes; X, y wait for it */
+    /* Fused RMSNorm (optional; both sides zero/null = off).  A RESIDUAL linear with ss_out writes,
+     * per 128-row tile and half tile, the sum of squares of each updated (bf16) y row:
+     * ss_out[(tile * 2 + half) * ss_ld + b].  The next linear takes x = that raw residual stream
+     * (the norm weight gamma folded into its w columns) with ss_in = those ss_parts partial sums and
+     * scales output column b by rsqrt(sum(ss_in[.][b]) / ss_dim + ss_eps) — RMSNorm(h) W^T without a
+     * norm kernel; fixed summation order (deterministic). */
+    float* ss_out;
+    const float* ss_in;
+    int32_t ss_parts, ss_ld, ss_dim;
+    float ss_eps;
 } asv_linear_args;
 
 /* One launch: one CTA per (128-row tile, K split); the K splits of a tile are one

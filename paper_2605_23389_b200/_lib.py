@@ -82,6 +82,12 @@ class LinearArgs(C.Structure):
         ("n_q_heads", C.c_int32),
         ("n_kv_heads", C.c_int32),
         ("pdl", C.c_int32),
+        ("ss_out", C.c_void_p),
+        ("ss_in", C.c_void_p),
+        ("ss_parts", C.c_int32),
+        ("ss_ld", C.c_int32),
+        ("ss_dim", C.c_int32),
+        ("ss_eps", C.c_float),
     ]
 
 

@@ -51,6 +51,11 @@ struct LinearParams {
     float rope_log2_theta;           // log2(theta)
     __nv_bfloat16 *q, *kk, *v;       // [batch][heads][128]
     int32_t n_q_heads, n_kv_heads;
+    // fused RMSNorm (asv.h): producer writes ss_out, consumer scales by rsqrt(sum(ss_in) / dim + eps)
+    float* ss_out;
+    const float* ss_in;
+    int32_t ss_parts, ss_ld;
+    float ss_inv_dim, ss_eps;
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -155,6 +160,7 @@ __global__ void __launch_bounds__(128, 2)
     const int ring = nst * stage_bytes > p.bn * 512 ? nst * stage_bytes : p.bn * 512;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kMaxStages + 1);
+    float* rs = reinterpret_cast<float*>(tmem_slot + 4);  // fused RMSNorm: 1/rms per batch column of this CTA
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tile = blockIdx.x / p.splits, split = blockIdx.x % p.splits;
@@ -237,6 +243,24 @@ __global__ void __launch_bounds__(128, 2)
             }
         }
         umma_commit(done);  // accumulator complete
+    } else if (warp >= 2 && p.ss_in != nullptr) {
+        // fused RMSNorm: the two idle warps turn the producer's partial sums of squares into
+        // 1/rms for this CTA's batch columns while the main loop runs (8 independent partial
+        // sums per column, combined in a fixed order: deterministic)
+        grid_dep_wait();
+        const int per_c = (p.batch + p.splits - 1) / p.splits;
+        const int c0 = split * per_c, c1 = min(c0 + per_c, p.batch);
+        for (int c = c0 + static_cast<int>(threadIdx.x) - 64; c < c1; c += 64) {
+            float acc8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            int i = 0;
+            for (; i + 8 <= p.ss_parts; i += 8) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc8[j] += p.ss_in[static_cast<int64_t>(i + j) * p.ss_ld + c];
+            }
+            for (; i < p.ss_parts; ++i) acc8[0] += p.ss_in[static_cast<int64_t>(i) * p.ss_ld + c];
+            const float ssum = ((acc8[0] + acc8[1]) + (acc8[2] + acc8[3])) + ((acc8[4] + acc8[5]) + (acc8[6] + acc8[7]));
+            rs[c - c0] = rsqrtf(ssum * p.ss_inv_dim + p.ss_eps);
+        }
     }
     __syncwarp();
 
@@ -253,7 +277,7 @@ __global__ void __launch_bounds__(128, 2)
         for (int i = 0; i < 16; ++i) part[(c0 + i) * kBM + threadIdx.x] = v[i];
     }
     tc_fence_before();
-    __syncthreads();
+    __syncthreads();  // (also publishes the fused-RMSNorm scales rs[] to every thread)
     if (warp == 1) {
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols) : "memory");
     }
@@ -287,14 +311,27 @@ __global__ void __launch_bounds__(128, 2)
             hi += x1;
         }
         const int b = c;
+        if (p.ss_in != nullptr) {
+            lo *= rs[c - cb];
+            hi *= rs[c - cb];
+        }
         if constexpr (EPI == ASV_EPI_STORE || EPI == ASV_EPI_RESIDUAL) {
             __nv_bfloat16* dst = p.y + static_cast<int64_t>(b) * p.y_ld + tile * kBM + r;
             if constexpr (EPI == ASV_EPI_RESIDUAL) {
                 lo += __bfloat162float(dst[0]);
                 hi += __bfloat162float(dst[64]);
             }
-            dst[0] = __float2bfloat16(lo);
-            dst[64] = __float2bfloat16(hi);
+            const __nv_bfloat16 blo = __float2bfloat16(lo), bhi = __float2bfloat16(hi);
+            dst[0] = blo;
+            dst[64] = bhi;
+            if (p.ss_out != nullptr) {  // the next linear's fused RMSNorm: sum of squares of the stored row
+                const float fl = __bfloat162float(blo), fh = __bfloat162float(bhi);
+                float sq = fl * fl + fh * fh;
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+                if ((threadIdx.x & 31) == 0)
+                    p.ss_out[static_cast<int64_t>(tile * 2 + ((threadIdx.x >> 5) & 1)) * p.ss_ld + b] = sq;
+            }
         } else if constexpr (EPI == ASV_EPI_SILU_MUL) {
             // tile rows [0,64) gate, [64,128) the matching up rows of outputs 64*tile + r
             p.y[static_cast<int64_t>(b) * p.y_ld + tile * 64 + r] = __float2bfloat16(silu(lo) * hi);
@@ -367,7 +404,7 @@ int stages_for(int bn) {
 // the epilogue reuses the ring for the [bn][128] fp32 accumulator tile
 int smem_bytes(int bn) {
     const int ring = stages_for(bn) * (kABytes + bn * 128);
-    return (ring > bn * 512 ? ring : bn * 512) + 1024 + (2 * kMaxStages + 1) * 8 + 16;
+    return (ring > bn * 512 ? ring : bn * 512) + 1024 + (2 * kMaxStages + 1) * 8 + 16 + 256 * 4;
 }
 
 template <int EPI>
@@ -442,6 +479,10 @@ static int linear_run(const asv_linear_args* a, cudaStream_t st) {
     } else if (a->y == nullptr) {
         return fail(ASV_ERR_INVALID, "linear: null y");
     }
+    if (a->ss_out != nullptr && (a->epilogue != ASV_EPI_RESIDUAL || a->ss_ld < a->batch))
+        return fail(ASV_ERR_INVALID, "linear: ss_out needs the RESIDUAL epilogue and ss_ld >= batch");
+    if (a->ss_in != nullptr && (a->ss_parts < 1 || a->ss_ld < a->batch || a->ss_dim < 1))
+        return fail(ASV_ERR_INVALID, "linear: bad fused-RMSNorm arguments (ss_parts, ss_ld, ss_dim)");
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -476,6 +517,12 @@ static int linear_run(const asv_linear_args* a, cudaStream_t st) {
     p.v = static_cast<__nv_bfloat16*>(a->v_out);
     p.n_q_heads = a->n_q_heads;
     p.n_kv_heads = a->n_kv_heads;
+    p.ss_out = a->ss_out;
+    p.ss_in = a->ss_in;
+    p.ss_parts = a->ss_parts;
+    p.ss_ld = a->ss_ld;
+    p.ss_inv_dim = a->ss_dim > 0 ? 1.f / static_cast<float>(a->ss_dim) : 0.f;
+    p.ss_eps = a->ss_eps;
     const int grid = tiles * splits;
     cudaError_t e;
     switch (a->epilogue) {

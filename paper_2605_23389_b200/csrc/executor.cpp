@@ -357,6 +357,8 @@ class GpuExecutor : public prefixsim::EngineObserver {
         if (h_) cudaFree(h_);
         if (x_) cudaFree(x_);
         if (act_) cudaFree(act_);
+        if (ss_a_) cudaFree(ss_a_);
+        if (ss_b_) cudaFree(ss_b_);
         cudaFree(k_new_);
         cudaFree(v_new_);
         cudaFree(ws_);
@@ -589,7 +591,9 @@ class GpuExecutor : public prefixsim::EngineObserver {
             stats_.kernel_launches_timed += o_.num_layers * (plan.n_merge > 0 ? 2 : 1) + 1 + (result_bytes > 0 ? 1 : 0);
             if (o_.full_step) {  // per layer: 2 RMSNorm + 4 linear launches per 256-row chunk
                 const int64_t chunks = (static_cast<int64_t>(running.size()) + 255) / 256;
-                stats_.kernel_launches_timed += o_.num_layers * (2 + 4 * chunks);
+                // RMSNorm launches: 2 per layer unfused; fused, only layer 0's first one remains
+                const int64_t norms = fuse_norm_ ? 1 : 2 * o_.num_layers;
+                stats_.kernel_launches_timed += norms + o_.num_layers * 4 * chunks;
                 stats_.weight_bytes += o_.num_layers * weights_bytes_per_layer_;
             }
             if (first_timed_start_ < 0) first_timed_start_ = rec.start_ms;
@@ -1184,6 +1188,14 @@ class GpuExecutor : public prefixsim::EngineObserver {
             layers_.push_back(lw);
         }
         ASV_CUDA(fill_random_bf16(h_, rows_pad * hidden_, 7, 1.f, 0.f, compute_));
+        // fused RMSNorm (asv.h ss_*): the norm weights are folded into the synthetic QKV / gate-up
+        // weights and each residual GEMM leaves per-tile row sums of squares for the next GEMM;
+        // layer 0 keeps the standalone norm (its input is the step's embedding, not a GEMM output)
+        fuse_norm_ = std::getenv("ASV_UNFUSED_NORM") == nullptr;
+        ss_parts_ = 2 * (hidden_ / 128);
+        ss_ld_ = static_cast<int32_t>(rows_pad);
+        ASV_CUDA(cudaMalloc(&ss_a_, static_cast<size_t>(ss_parts_) * rows_pad * 4));
+        ASV_CUDA(cudaMalloc(&ss_b_, static_cast<size_t>(ss_parts_) * rows_pad * 4));
         ASV_CUDA(cudaStreamSynchronize(compute_));
         if (linear_preload() != cudaSuccess || rmsnorm_preload() != cudaSuccess)
             throw CudaError("full_step: kernel preload failed");
@@ -1209,15 +1221,25 @@ class GpuExecutor : public prefixsim::EngineObserver {
     static void row_chunks(int32_t b, F&& f) {
         for (int32_t r0 = 0; r0 < b; r0 += 256) f(r0, std::min<int32_t>(256, b - r0));
     }
+    // the next linear takes the raw residual stream h and applies RMSNorm in its epilogue
+    void fuse_in(asv_linear_args& a, const float* ss, int32_t r0) const {
+        a.ss_in = ss + r0;
+        a.ss_parts = ss_parts_;
+        a.ss_ld = ss_ld_;
+        a.ss_dim = hidden_;
+        a.ss_eps = 1e-5f;
+    }
     void layer_front(int l, int32_t b, const int32_t* positions) {
         const LayerW& lw = layers_[static_cast<size_t>(l)];
         const int32_t rows = (b + 15) / 16 * 16;
-        if (asv_rmsnorm(h_, lw.g1, x_, hidden_, b, rows, 1e-5f, o_.pdl, compute_) != ASV_OK)
+        const bool fused = fuse_norm_ && l > 0;  // ss_a_ holds the previous layer's down-proj sums
+        if (!fused && asv_rmsnorm(h_, lw.g1, x_, hidden_, b, rows, 1e-5f, o_.pdl, compute_) != ASV_OK)
             throw CudaError(asv_last_error());
+        const auto* xin = static_cast<const __nv_bfloat16*>(fused ? h_ : x_);
         row_chunks(b, [&](int32_t r0, int32_t n) {
             asv_linear_args a = lin(lw.qkv, 128 * (o_.num_q_heads + 2 * o_.num_kv_heads), hidden_,
-                                    static_cast<const __nv_bfloat16*>(x_) + int64_t(r0) * hidden_, n, nullptr, 0,
-                                    ASV_EPI_QKV_ROPE);
+                                    xin + int64_t(r0) * hidden_, n, nullptr, 0, ASV_EPI_QKV_ROPE);
+            if (fused) fuse_in(a, ss_a_, r0);
             a.positions = positions + r0;
             a.rope_theta = 10000.f;
             a.q = static_cast<__nv_bfloat16*>(q_) + int64_t(r0) * o_.num_q_heads * 128;
@@ -1235,20 +1257,29 @@ class GpuExecutor : public prefixsim::EngineObserver {
         row_chunks(b, [&](int32_t r0, int32_t n) {  // h += attn_out . Wo^T
             asv_linear_args a = lin(lw.o, hidden_, hidden_, static_cast<const __nv_bfloat16*>(out_) + int64_t(r0) * hidden_,
                                     n, h + int64_t(r0) * hidden_, hidden_, ASV_EPI_RESIDUAL);
+            if (fuse_norm_) {
+                a.ss_out = ss_b_ + r0;
+                a.ss_ld = ss_ld_;
+            }
             if (asv_linear(&a, compute_) != ASV_OK) throw CudaError(asv_last_error());
         });
-        if (asv_rmsnorm(h_, lw.g2, x_, hidden_, b, rows, 1e-5f, o_.pdl, compute_) != ASV_OK)
+        if (!fuse_norm_ && asv_rmsnorm(h_, lw.g2, x_, hidden_, b, rows, 1e-5f, o_.pdl, compute_) != ASV_OK)
             throw CudaError(asv_last_error());
         auto* act = static_cast<__nv_bfloat16*>(act_);
+        const auto* xin = static_cast<const __nv_bfloat16*>(fuse_norm_ ? h_ : x_);
         row_chunks(b, [&](int32_t r0, int32_t n) {  // act = silu(x Wg^T) * (x Wu^T)
-            asv_linear_args a = lin(lw.gate_up, 2 * inter_, hidden_,
-                                    static_cast<const __nv_bfloat16*>(x_) + int64_t(r0) * hidden_, n,
+            asv_linear_args a = lin(lw.gate_up, 2 * inter_, hidden_, xin + int64_t(r0) * hidden_, n,
                                     act + int64_t(r0) * inter_, inter_, ASV_EPI_SILU_MUL);
+            if (fuse_norm_) fuse_in(a, ss_b_, r0);
             if (asv_linear(&a, compute_) != ASV_OK) throw CudaError(asv_last_error());
         });
         row_chunks(b, [&](int32_t r0, int32_t n) {  // h += act . Wd^T
             asv_linear_args a = lin(lw.down, hidden_, inter_, act + int64_t(r0) * inter_, n,
                                     h + int64_t(r0) * hidden_, hidden_, ASV_EPI_RESIDUAL);
+            if (fuse_norm_) {  // for the next layer's QKV
+                a.ss_out = ss_a_ + r0;
+                a.ss_ld = ss_ld_;
+            }
             if (asv_linear(&a, compute_) != ASV_OK) throw CudaError(asv_last_error());
         });
     }
@@ -1370,6 +1401,9 @@ class GpuExecutor : public prefixsim::EngineObserver {
     };
     std::vector<LayerW> layers_;
     void *weights_ = nullptr, *h_ = nullptr, *x_ = nullptr, *act_ = nullptr;
+    float *ss_a_ = nullptr, *ss_b_ = nullptr;  // fused RMSNorm: per-tile row sums of squares of h
+    int32_t ss_parts_ = 0, ss_ld_ = 0;
+    bool fuse_norm_ = false;
     int32_t hidden_ = 0, inter_ = 0;
     int64_t max_rows_full_ = 0, weights_bytes_per_layer_ = 0;
     void *q_ = nullptr, *out_ = nullptr, *k_new_ = nullptr, *v_new_ = nullptr, *ws_ = nullptr;

@@ -19,8 +19,14 @@ STORE, RESIDUAL, SILU_MUL, QKV_ROPE = _lib.EPI_STORE, _lib.EPI_RESIDUAL, _lib.EP
 def linear(x: torch.Tensor, w: torch.Tensor, batch: int, y: torch.Tensor | None = None,
            epilogue: int = STORE, positions: torch.Tensor | None = None, rope_theta: float = 10000.0,
            q: torch.Tensor | None = None, k_out: torch.Tensor | None = None, v_out: torch.Tensor | None = None,
-           n_q_heads: int = 0, n_kv_heads: int = 0, pdl: bool = False, stream=None) -> torch.Tensor | None:
-    """y[:batch] = epilogue(x[:batch] @ w.T) on tcgen05 (x has >= batch rounded up to 16 rows)."""
+           n_q_heads: int = 0, n_kv_heads: int = 0, pdl: bool = False, stream=None,
+           ss_out: torch.Tensor | None = None, ss_in: torch.Tensor | None = None, ss_eps: float = 1e-5
+           ) -> torch.Tensor | None:
+    """y[:batch] = epilogue(x[:batch] @ w.T) on tcgen05 (x has >= batch rounded up to 16 rows).
+
+    Fused RMSNorm: ss_out ([2 * n_out/128][ld] fp32, RESIDUAL only) receives the per-tile sums of
+    squares of the updated y rows; a following call with ss_in = that tensor treats x as the raw
+    residual stream and scales each output row by rsqrt(mean(x^2) + ss_eps)."""
     if x.dtype != torch.bfloat16 or w.dtype != torch.bfloat16:
         raise TypeError("x and w must be bfloat16")
     n_out, k = w.shape
@@ -37,6 +43,10 @@ def linear(x: torch.Tensor, w: torch.Tensor, batch: int, y: torch.Tensor | None 
     a.v_out = v_out.data_ptr() if v_out is not None else None
     a.n_q_heads, a.n_kv_heads = n_q_heads, n_kv_heads
     a.pdl = 1 if pdl else 0
+    if ss_out is not None:
+        a.ss_out, a.ss_ld = ss_out.data_ptr(), ss_out.shape[-1]
+    if ss_in is not None:
+        a.ss_in, a.ss_parts, a.ss_ld, a.ss_dim, a.ss_eps = ss_in.data_ptr(), ss_in.shape[0], ss_in.shape[-1], k, ss_eps
     st = (stream or torch.cuda.current_stream(x.device)).cuda_stream
     _lib.check(_lib.lib().asv_linear(C.byref(a), C.c_void_p(st)))
     return y

@@ -171,3 +171,36 @@ def test_pdl_chain_matches_torch():
     a = (torch.nn.functional.silu(gg) * uu).bfloat16().float()
     r = r + a @ wd.float().T
     _check(h, r, "pdl chain")
+
+
+@pytest.mark.parametrize("batch", [5, 37])
+def test_fused_rmsnorm_between_linears(batch):
+    """Fused RMSNorm (asv.h ss_*): a RESIDUAL linear leaves per-tile row sums of squares of the
+    updated residual stream; the next linear reads that stream raw and scales each output row by
+    rsqrt(mean(h^2) + eps) — equal to RMSNorm(h) @ W^T with the norm weight folded into W.
+    Checked for the STORE and SILU_MUL consumers against torch fp32."""
+    from paper_2605_23389_b200 import linear as L
+    d, n2, inter = 4096, 1024, 11008
+    rows = (batch + 15) // 16 * 16
+    h0 = _rand((rows, d), 71)
+    x = _x(batch, d, 72)
+    wo, w2 = _rand((d, d), 73, 1 / math.sqrt(d)), _rand((n2, d), 74, 1 / math.sqrt(d))
+    wgu = _rand((2 * inter, d), 75, 1 / math.sqrt(d))
+    ss = torch.full((2 * d // 128, rows), float("nan"), dtype=torch.float32, device="cuda")
+    h = h0.clone()
+    L.linear(x, wo, batch, h, L.RESIDUAL, ss_out=ss)
+    y = torch.zeros(batch, n2, dtype=torch.bfloat16, device="cuda")
+    L.linear(h, w2, batch, y, L.STORE, ss_in=ss)
+    act = torch.zeros(batch, inter, dtype=torch.bfloat16, device="cuda")
+    L.linear(h, wgu, batch, act, L.SILU_MUL, ss_in=ss)
+    torch.cuda.synchronize()
+    h1 = (h0[:batch].float() + x[:batch].float() @ wo.float().T).bfloat16()
+    _check(h[:batch], h1, "residual")
+    # the partial sums are those of the stored bf16 rows, one slot per (tile, half tile, row)
+    assert torch.isfinite(ss[:, :batch]).all()
+    assert torch.allclose(ss[:, :batch].sum(0), h1.float().pow(2).sum(-1), rtol=1e-4)
+    xn = h1.float() * torch.rsqrt(h1.float().pow(2).mean(-1, keepdim=True) + 1e-5)
+    _check(y, (xn @ w2.float().T).bfloat16(), "fused rmsnorm -> store")
+    gu = (xn @ wgu.float().T).view(batch, -1, 2, 64)
+    ref = torch.nn.functional.silu(gu[:, :, 0].reshape(batch, -1)) * gu[:, :, 1].reshape(batch, -1)
+    _check(act, ref.bfloat16(), "fused rmsnorm -> silu")
