@@ -200,11 +200,15 @@ int asv_attn_plan_build(const asv_attn_shape* shape, int32_t batch, const int32_
     // together (B200, C2 bench step: warp idle 10.1% -> 4.2% of the launch, +2.3%
     // tokens/s; profiles/ab_r01f_plan_tail.txt).  ASV_PLAN_TAIL=<percent> overrides
     // (tuning only; 0 = equal spans).
+    // MHA only: on GQA the extra splits cost more in the merge (one row per query head) than the
+    // tail saves (C4 13B GQA-8 engine step: 11 240 -> 10 972 tokens/s with the tail; C1 MHA:
+    // 10 600 -> 11 020).
     constexpr int kTailPct = 25;
-    static const int tail_pct = [] {
+    static const int tail_env = [] {
         const char* e = getenv("ASV_PLAN_TAIL");
-        return e != nullptr ? atoi(e) : kTailPct;
+        return e != nullptr ? atoi(e) : -1;
     }();
+    const int tail_pct = tail_env >= 0 ? tail_env : (shape->num_q_heads == shape->num_kv_heads ? kTailPct : 0);
     std::vector<std::vector<int32_t>> bounds(static_cast<size_t>(batch));
     for (int r = 0; r < batch; ++r) {
         const int n = npages[static_cast<size_t>(r)], k = best_ns[static_cast<size_t>(r)];

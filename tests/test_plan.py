@@ -75,6 +75,14 @@ def test_aligned_batch_gets_two_item_sizes_longest_first():
         assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
 
 
+def test_gqa_plan_keeps_equal_items():
+    """GQA: no small-item tail (its merge has one row per query head; measured slower on C4)."""
+    plan, buf, _, _ = build([4096 + i for i in range(16)], n_q=40, n_kv=8)
+    sizes = {int(buf[plan.off_desc + g * DESC + 3] - buf[plan.off_desc + g * DESC + 2])
+             for g in range(plan.total_splits)}
+    assert max(sizes) - min(sizes) <= 1
+
+
 def test_gqa_plan_items_per_kv_head():
     plan, _, _, _ = build([1000, 2000], n_q=40, n_kv=8)
     assert plan.num_items == plan.total_splits * 8
