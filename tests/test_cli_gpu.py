@@ -85,3 +85,17 @@ def test_cli_whole_c1_trace_on_the_gpu(tmp_path):
     assert gs["iterations_timed"] == GOLDEN["logs"]["c1_7b_b16:aligned"]["iterations"]
     lb = gs["logical_bytes"]
     assert gs["h2d_bytes"] == lb["batch_prefetch"] + lb["stray_prefetch"] > 0
+
+
+def test_cli_compare_with_gpu_measurements(tmp_path):
+    """`compare --gpu`: the reference's policy sweep (virtual clock) plus each policy executed on the B200."""
+    cfg = tmp_path / "smoke.json"
+    cfg.write_text(json.dumps(GOLDEN["configs"]["smoke"]))
+    out = tmp_path / "cmp"
+    r = subprocess.run([CLI, "compare", "--config", str(cfg), "--seeds", "1", "--policies", "aligned,fcfs", "--gpu",
+                        "--resident", "--out", str(out)], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr
+    m = json.loads((out / "gpu_measured.json").read_text())
+    assert set(m) == {"aligned", "fcfs_continuous"}
+    assert all(v["decode_tokens_per_s_measured"] > 0 for v in m.values())
+    assert (out / "compare.csv").exists() and (out / "ratios.json").exists()
