@@ -265,3 +265,9 @@ def test_dtype_mismatch_is_rejected():
     pool = torch.zeros(4 * att.page_bytes, dtype=torch.uint8, device="cuda")
     with pytest.raises(TypeError, match="float16"):
         att.run(q, pool, 0, plan, torch.empty_like(q))
+
+
+def test_mha_13b_shape_last_layer(oracle):
+    """Llama-2-13B MHA shape (40 heads, 40 layers per page: 12.5 MiB pages), the last layer's slice
+    (a small batch: the test pool is built in host memory at 12.5 MiB per page)."""
+    _run_case(oracle, 40, 40, 40, 39, [1, 200, 513, 700], seed=131)
