@@ -90,3 +90,18 @@ def test_full_decode_step_runs_and_is_deterministic():
     assert a["iterations_timed"] == b["iterations_timed"] == GOLDEN["logs"]["smoke:aligned"]["iterations"]
     # per layer >= attention + 4 GEMM launches (the RMSNorms are fused into the GEMMs after layer 0)
     assert a["window_ms"] > 0 and a["kernel_launches_timed"] > b["iterations_timed"] * 32 * 5
+
+
+def test_gqa_13b_config_executes():
+    """BASELINE C4 shape (13B GQA-8: 40 q heads, 8 kv heads, 40 layers; extended ModelSpec with
+    num_kv_heads): the engine executes its decisions, KV moves included, on the GQA kernel path."""
+    import os
+    from paper_2605_23389_b200 import engine
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cfg = engine.load_config(os.path.join(root, "configs", "c4_13b_gqa8.json"))
+    st = engine.engine_run(cfg, device=0, num_q_heads=40, num_kv_heads=8, num_layers=40, execute_transfers=True,
+                           exec_begin=150, timed_begin=155, exec_end=175, copy_begin=0, host_pool_bytes=1 << 30)
+    assert st["iterations_timed"] == 20 and st["tokens_timed"] > 0 and st["window_ms"] > 0
+    assert st["h2d_bytes"] > 0 and st["h2d_bytes"] % (40 * 2 * 8 * 256) == 0  # whole tokens of 160 KiB
+    gbps = st["attn_bytes"] / (st["attn_ms"] * 1e-3) / 1e9
+    assert gbps > 3000, gbps
