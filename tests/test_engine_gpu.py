@@ -99,6 +99,9 @@ def test_gqa_13b_config_executes():
     from paper_2605_23389_b200 import engine
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     cfg = engine.load_config(os.path.join(root, "configs", "c4_13b_gqa8.json"))
+    # a 16K-block pool (~65 GB) instead of the config's 40K (its 172 GB pool plus candidate buffers
+    # needs a whole B200 to itself; earlier tests in the same process hold cached device memory)
+    cfg["cluster"]["decode_hbm_blocks"] = cfg["cluster"]["prefill_hbm_blocks"] = 16384
     st = engine.engine_run(cfg, device=0, num_q_heads=40, num_kv_heads=8, num_layers=40, execute_transfers=True,
                            exec_begin=150, timed_begin=155, exec_end=175, copy_begin=0, host_pool_bytes=1 << 30)
     assert st["iterations_timed"] == 20 and st["tokens_timed"] > 0 and st["window_ms"] > 0
