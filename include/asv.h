@@ -98,6 +98,9 @@ typedef struct asv_attn_plan {
     int32_t n_merge;        /* their count (rows of the merge kernel = n_merge * n_h) */
     int32_t total_int32;    /* size of the plan buffer in int32 */
     int32_t max_item_pages; /* largest work item, pages (<= 32) */
+    int32_t append_missing; /* requests whose page list does not cover position seq_len: a launch
+                               with k_new / v_new set is rejected (ASV_ERR_INVALID) instead of
+                               silently dropping their appended row */
 } asv_attn_plan;
 
 /* Persistent warp count of the decode-attention kernel on `device` (SMs x resident warps). */
@@ -125,7 +128,7 @@ int asv_attn_plan_build(const asv_attn_shape* shape, int32_t batch, const int32_
  * be launched with programmatic dependent launch. */
 int asv_plan_upload(const int32_t* host_plan, int32_t* plan_dev, int64_t n_int32, void* stream);
 
-/* Workspace: split partials + per-(request, kv head) semaphores. */
+/* Workspace: the dynamic-schedule counters + split partials. */
 size_t asv_attn_workspace_bytes(const asv_attn_shape* shape, int32_t max_batch,
                                 int32_t max_total_splits);
 int asv_attn_workspace_init(void* workspace, size_t bytes, void* stream);

@@ -60,6 +60,31 @@ int ref_run_config_jsonl(const char* config_json, const char* policy, char** out
     });
 }
 
+// Same log, but *seconds times the decision engine alone (Simulation::run over the
+// trace, cluster_sim.hpp:773-777): the cost-model calibration and the trace ingest
+// happen before the clock starts.
+int ref_run_config_timed(const char* config_json, const char* policy, char** out, long long* out_len,
+                         double* seconds, long long* iterations) {
+    return guard([&] {
+        auto cfg = prefixsim::experiment_from_json(prefixsim::json::parse(config_json));
+        if (policy) cfg.sim.policy = prefixsim::policy_from_string(policy);
+        const prefixsim::CalibratedCostModel model =
+            cfg.has_calibration ? cfg.calibration
+                                : prefixsim::calibrate(prefixsim::reference_mixed_batch_anchors(), cfg.model).model;
+        std::vector<prefixsim::Request> reqs =
+            cfg.workload.kind == prefixsim::WorkloadSpec::Kind::kTrace
+                ? prefixsim::ingest_trace(cfg.workload.trace_path, cfg.workload.trace_format).requests
+                : prefixsim::generate_synthetic(cfg.workload);
+        const auto t0 = std::chrono::steady_clock::now();
+        const prefixsim::MetricsLog log = prefixsim::run(cfg.sim, std::move(reqs), model);
+        const auto t1 = std::chrono::steady_clock::now();
+        if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+        if (iterations) *iterations = static_cast<long long>(log.iterations.size());
+        *out = dup(prefixsim::log_to_jsonl(log), out_len);
+        return 0;
+    });
+}
+
 // density_first_search on a pool snapshot (all inserted at t = 0, no starvation)
 int ref_dfs_batch(const long long* res, long long n, long long b_max, long long k_min, long long* ids,
                   long long* n_out, long long* total_blocks) {

@@ -38,6 +38,7 @@ class AttnPlan(C.Structure):
         ("n_merge", C.c_int32),
         ("total_int32", C.c_int32),
         ("max_item_pages", C.c_int32),
+        ("append_missing", C.c_int32),
     ]
 
 

@@ -62,7 +62,6 @@ struct AttnLaunch {
     float* lse;
     float* part_o;
     float* part_ml;           // float2 pairs
-    int32_t* sem;
     uint32_t* work;           // 2 counters of this launch parity
     const int32_t* merge_reqs;  // requests with > 1 split (merge kernel rows)
     int32_t n_merge;

@@ -18,9 +18,7 @@ namespace asv {
 
 namespace {
 thread_local std::string g_last_error;
-constexpr int64_t kSemBytes = 256 * 1024;  // 65536 (request, kv head) semaphores
-constexpr int64_t kWorkBytes = 256;        // per-parity dynamic-schedule counters
-constexpr int64_t kHeadBytes = kSemBytes + kWorkBytes;
+constexpr int64_t kHeadBytes = 256;  // per-parity dynamic-schedule counters; partials follow
 constexpr int64_t kBlockBytes = 16 * 128 * 2;
 
 int group_of(const asv_attn_shape* s) { return s->num_q_heads / s->num_kv_heads; }
@@ -63,7 +61,7 @@ using namespace asv;
 extern "C" {
 
 const char* asv_last_error(void) { return g_last_error.c_str(); }
-int asv_abi_version(void) { return 1; }
+int asv_abi_version(void) { return 2; }
 
 int64_t asv_struct_size(const char* name) {
     if (name == nullptr) return -1;
@@ -254,6 +252,7 @@ int asv_attn_plan_build(const asv_attn_shape* shape, int32_t batch, const int32_
         if (best_ns[static_cast<size_t>(r)] > 1) plan_buf[off_merge + k++] = r;
     }
     pl.max_item_pages = 0;
+    pl.append_missing = 0;
 
     // split_base: partial slots are request-major (the merge walks them)
     int32_t* sb = plan_buf + off_split;
@@ -292,6 +291,7 @@ int asv_attn_plan_build(const asv_attn_shape* shape, int32_t batch, const int32_
             d[4] = seq_lens[r];
             d[5] = k;
             d[6] = (s == k - 1 && app < owned) ? pages[app] : -1;
+            if (s == k - 1 && app >= owned) ++pl.append_missing;
             d[7] = 0;
             for (int j = 0; j < kMaxItemPages; ++j) d[8 + j] = (pb + j < pe) ? pages[pb + j] : 0;
             pl.max_item_pages = std::max(pl.max_item_pages, pe - pb);
@@ -337,8 +337,9 @@ int asv_decode_attention(const asv_attn_shape* shape, const asv_attn_args* a, vo
     if ((a->k_new == nullptr) != (a->v_new == nullptr))
         return fail(ASV_ERR_INVALID, "k_new and v_new must both be set or both be null");
     const int n_kv = shape->num_kv_heads, n_q = shape->num_q_heads;
-    if (static_cast<int64_t>(pl.batch) * n_kv * 4 > kSemBytes)
-        return fail(ASV_ERR_INVALID, "batch * num_kv_heads exceeds the semaphore capacity");
+    if (a->k_new != nullptr && pl.append_missing > 0)
+        return fail(ASV_ERR_INVALID, "KV append requested but " + std::to_string(pl.append_missing) +
+                                         " request(s) own no page for position seq_len");
     const int64_t need = kHeadBytes + static_cast<int64_t>(pl.total_splits) * n_q * (128 * 4 + 8);
     if (a->workspace == nullptr || static_cast<int64_t>(a->workspace_bytes) < need)
         return fail(ASV_ERR_INVALID, "workspace too small for plan: need " + std::to_string(need));
@@ -353,7 +354,7 @@ int asv_decode_attention(const asv_attn_shape* shape, const asv_attn_args* a, vo
     L.group = n_q / n_kv;
     L.grid = pl.num_workers / nw;
     {
-        // the in-kernel merge uses a grid-wide barrier: never exceed co-residency
+        // persistent grid: never more CTAs than can be co-resident (the plan may come from another device)
         int dev = 0;
         cudaGetDevice(&dev);
         int32_t resident = 0;
@@ -391,8 +392,7 @@ int asv_decode_attention(const asv_attn_shape* shape, const asv_attn_args* a, vo
     L.out = a->out;
     L.lse = a->lse;
     char* ws = static_cast<char*>(a->workspace);
-    L.sem = reinterpret_cast<int32_t*>(ws);
-    L.work = reinterpret_cast<uint32_t*>(ws + kSemBytes) + 4 * (a->launch_index & 1u);
+    L.work = reinterpret_cast<uint32_t*>(ws) + 4 * (a->launch_index & 1u);
     // partial outputs first (16-byte aligned float4 rows), then the (m, l) pairs
     L.part_o = reinterpret_cast<float*>(ws + kHeadBytes);
     L.part_ml = reinterpret_cast<float*>(ws + kHeadBytes + static_cast<int64_t>(pl.total_splits) * n_q * 512);

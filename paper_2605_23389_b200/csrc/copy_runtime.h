@@ -11,6 +11,12 @@
 //    (measured: 100 us per 8 MiB page copy with multi-GB batch prefetches in
 //    flight, 1.3 us when idle); on its own thread that back-pressure never
 //    stalls the launch of decode iterations.
+//  * Serial mode (ASV_SERIAL=1, or automatically under a CUDA profiler /
+//    sanitizer injection): every posted operation runs inline on the posting
+//    thread and each flag write synchronises its stream and then sets the flag
+//    from the host; a flag wait is a host-side check (never a stream wait).  A
+//    profiler that serialises kernels across streams (Nsight Compute) would
+//    otherwise park a stream on a flag whose writer it never schedules.
 #pragma once
 
 #include <cuda.h>
@@ -18,6 +24,7 @@
 
 #include <atomic>
 #include <condition_variable>
+#include <cstdlib>
 #include <deque>
 #include <functional>
 #include <mutex>
@@ -27,9 +34,17 @@
 
 namespace asv {
 
+// ASV_SERIAL=1, or a CUDA injection library (ncu / nsys / compute-sanitizer) is loaded
+inline bool serial_mode_requested() {
+    if (const char* e = std::getenv("ASV_SERIAL")) return std::atoi(e) != 0;
+    return std::getenv("CUDA_INJECTION64_PATH") != nullptr;
+}
+
 class SeqFlags {
  public:
     static constexpr int kSlots = 8;
+    void set_serial(bool on) { serial_ = on; }
+    bool serial() const { return serial_; }
 
     void init() {
         if (cudaHostAlloc(reinterpret_cast<void**>(&host_), kSlots * sizeof(uint32_t),
@@ -55,11 +70,22 @@ class SeqFlags {
     }
     // `st` waits until flag[slot] >= v (cyclic 32-bit compare)
     void wait(cudaStream_t st, int slot, uint32_t v) const {
+        if (serial_) {  // everything before this point has completed (program order + stream syncs)
+            if (!reached(slot, v))
+                throw std::logic_error("serial mode: wait on sequence flag " + std::to_string(slot) + " >= " +
+                                       std::to_string(v) + " that no earlier operation writes");
+            return;
+        }
         check(wait_(reinterpret_cast<CUstream>(st), dev_ + slot * sizeof(uint32_t), v, CU_STREAM_WAIT_VALUE_GEQ),
               "cuStreamWaitValue32");
     }
     // `st` sets flag[slot] = v once its prior work is complete
     void write(cudaStream_t st, int slot, uint32_t v) const {
+        if (serial_) {
+            if (cudaStreamSynchronize(st) != cudaSuccess) throw std::runtime_error("serial mode: stream sync failed");
+            reinterpret_cast<volatile uint32_t*>(host_)[slot] = v;
+            return;
+        }
         check(write_(reinterpret_cast<CUstream>(st), dev_ + slot * sizeof(uint32_t), v, CU_STREAM_WRITE_VALUE_DEFAULT),
               "cuStreamWriteValue32");
     }
@@ -79,12 +105,23 @@ class SeqFlags {
     uint32_t* host_ = nullptr;
     CUdeviceptr dev_ = 0;
     Fn wait_ = nullptr, write_ = nullptr;
+    bool serial_ = false;
 };
 
 class CopyWorker {
  public:
-    void start() { th_ = std::thread([this] { loop(); }); }
+    // inline: post() runs the operation on the calling thread (serial mode), no worker thread
+    void start(bool inline_ops = false) {
+        inline_ = inline_ops;
+        if (!inline_) th_ = std::thread([this] { loop(); });
+    }
     void post(std::function<void()> fn, const char* label = "op") {
+        if (inline_) {
+            cur_.store(label);
+            fn();  // exceptions propagate to the caller
+            done_.fetch_add(1);
+            return;
+        }
         {
             std::lock_guard<std::mutex> lk(m_);
             q_.push_back({std::move(fn), label});
@@ -159,6 +196,7 @@ class CopyWorker {
     std::atomic<uint64_t> done_{0};
     std::string err_;
     std::thread th_;
+    bool inline_ = false;
 };
 
 }  // namespace asv

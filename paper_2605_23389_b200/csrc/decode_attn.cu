@@ -73,7 +73,6 @@ struct Params {
     float* lse;
     float* part_o;    // [slots * n_q][128]
     float2* part_ml;  // [slots * n_q]
-    int32_t* sem;     // [b * n_kv]
     uint32_t* work;   // [3]: grab counter, arrived warps, exited warps (this launch parity)
     const int32_t* merge_reqs;  // requests split more than once
     int32_t merge_rows;         // merge_reqs count * n_q
@@ -1028,7 +1027,6 @@ cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st) {
     p.lse = a.lse;
     p.part_o = a.part_o;
     p.part_ml = reinterpret_cast<float2*>(a.part_ml);
-    p.sem = a.sem;
     p.work = a.work;
     p.merge_reqs = a.merge_reqs;
     p.merge_rows = a.n_merge * a.n_q;

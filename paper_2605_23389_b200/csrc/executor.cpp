@@ -48,6 +48,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -132,7 +133,10 @@ class PagePool {
             if (!flags_->reached(q.slot, q.v)) {
                 if (!block) break;
                 const auto t0 = std::chrono::steady_clock::now();
-                while (!flags_->reached(q.slot, q.v)) std::this_thread::sleep_for(std::chrono::microseconds(20));
+                while (!flags_->reached(q.slot, q.v)) {
+                    if (health_) health_();  // a failed copy worker never writes the flag: throw, do not hang
+                    std::this_thread::sleep_for(std::chrono::microseconds(20));
+                }
                 wait_ms_ += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
                 block = false;  // one blocking wait, then drain whatever else finished
             }
@@ -144,8 +148,11 @@ class PagePool {
     int64_t size() const { return pages_; }
     int device() const { return device_; }
     double wait_ms() const { return wait_ms_; }
+    // called while spinning on a flag; throws when the thread that would write it has failed
+    void set_health_check(std::function<void()> f) { health_ = std::move(f); }
 
  private:
+    std::function<void()> health_;
     struct FreePage {
         int32_t page;
         int64_t hazard;
@@ -205,6 +212,10 @@ class GpuExecutor : public prefixsim::EngineObserver {
         }
         slice_ = 2 * static_cast<int64_t>(o.num_kv_heads) * 4096;
         flags_.init();
+        serial_ = serial_mode_requested();
+        flags_.set_serial(serial_);
+        dec_.set_health_check([this] { check_workers(); });
+        pre_.set_health_check([this] { check_workers(); });
         dec_.init(o.decode_device, dec_pages_, page_bytes_, slice_, &flags_);
         if (pair_ && peer) {
             ASV_CUDA(cudaSetDevice(o.decode_device));
@@ -304,8 +315,8 @@ class GpuExecutor : public prefixsim::EngineObserver {
         std::memset(stats_.logical_bytes, 0, sizeof(stats_.logical_bytes));
         std::memset(stats_.logical_count, 0, sizeof(stats_.logical_count));
         if (o.execute_transfers) warm_up_copies();
-        worker_.start();
-        launcher_.start();
+        worker_.start(serial_);
+        launcher_.start(serial_);
         if (std::getenv("ASV_WATCHDOG") != nullptr) {
             watchdog_ = std::thread([this] {
                 while (!watchdog_stop_.load()) {
@@ -507,8 +518,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
             throw std::runtime_error(asv_last_error());
         }
         if (plan.total_splits > ws_splits_) throw std::runtime_error("attention workspace too small");
-        if (worker_.failed()) throw CudaError("copy worker: " + worker_.error());
-        if (launcher_.failed()) throw CudaError("launch worker: " + launcher_.error());
+        check_workers();
         // admitted requests whose KV is still in flight: the iteration waits for it
         std::vector<std::pair<int, uint32_t>> waits;
         for (const auto& m : running) {
@@ -623,8 +633,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
         launcher_.drain();
         worker_.drain();
         phase_.store(4);
-        if (worker_.failed()) throw CudaError("copy worker: " + worker_.error());
-        if (launcher_.failed()) throw CudaError("launch worker: " + launcher_.error());
+        check_workers();
         ASV_CUDA(cudaSetDevice(o_.decode_device));
         ASV_CUDA(cudaStreamSynchronize(compute_));
         ASV_CUDA(cudaSetDevice(xfer_device()));
@@ -1284,6 +1293,11 @@ class GpuExecutor : public prefixsim::EngineObserver {
         });
     }
 
+    void check_workers() {
+        if (worker_.failed()) throw CudaError("copy worker: " + worker_.error());
+        if (launcher_.failed()) throw CudaError("launch worker: " + launcher_.error());
+    }
+
     uint64_t* ts_slot(size_t slot) const { return ts_arena_ + slot * static_cast<size_t>(workers_) * 2; }
 
     // retire every executed iteration up to and including `e`, in order
@@ -1317,7 +1331,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
         if (!flags_.reached(kIter, static_cast<uint32_t>(e + 1))) {
             const auto t0 = clock_now();
             while (!flags_.reached(kIter, static_cast<uint32_t>(e + 1))) {
-                if (launcher_.failed()) throw CudaError("launch worker: " + launcher_.error());
+                check_workers();  // the iteration may be parked on a copy lane whose worker failed
                 std::this_thread::sleep_for(std::chrono::microseconds(20));
             }
             host_wait_ms_ += ms_since(t0);
@@ -1382,6 +1396,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
     int64_t open_timer_[kLanes] = {-1, -1, -1, -1, -1, -1, -1, -1};  // per lane: timer of the open group
     static_assert(kLanes == 8, "open_timer_ initialiser lists one entry per lane");
     SeqFlags flags_;
+    bool serial_ = false;                   // profiler-safe ordering (copy_runtime.h serial mode)
     CopyWorker worker_;                     // issues every copy-stream operation
     CopyWorker launcher_;                   // issues every compute-stream operation (iterations)
     std::thread watchdog_;                  // ASV_WATCHDOG=1: progress report every 5 s (debugging)

@@ -186,10 +186,11 @@ class RefEngine:
         if not os.path.exists(REF_SO):
             raise RuntimeError("oracle/_ref/libprefixsim_ref.so missing (reference not built)")
         self.h = C.CDLL(REF_SO)
-        self.h.ref_run_config_jsonl.restype = C.c_int
-        self.h.ref_run_config_jsonl.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p),
-                                                C.POINTER(C.c_longlong), C.POINTER(C.c_double),
-                                                C.POINTER(C.c_longlong)]
+        for fn in ("ref_run_config_jsonl", "ref_run_config_timed"):
+            f = getattr(self.h, fn)
+            f.restype = C.c_int
+            f.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p), C.POINTER(C.c_longlong),
+                          C.POINTER(C.c_double), C.POINTER(C.c_longlong)]
         for fn in ("ref_dfs_batch", "ref_dfs_flat_oracle"):
             f = getattr(self.h, fn)
             f.restype = C.c_int
@@ -198,21 +199,26 @@ class RefEngine:
         self.h.ref_free.argtypes = [C.c_void_p]
         self.h.ref_last_error.restype = C.c_char_p
 
-    def run_config_jsonl(self, config, policy=None):
+    def run_config_jsonl(self, config, policy=None, _fn="ref_run_config_jsonl"):
+        """(log, seconds of run_experiment, iterations)"""
         import json as _json
         text = config if isinstance(config, str) else _json.dumps(config)
         out = C.c_void_p()
         n = C.c_longlong(0)
         secs = C.c_double(0)
         its = C.c_longlong(0)
-        rc = self.h.ref_run_config_jsonl(text.encode(), policy.encode() if policy else None,
-                                         C.byref(out), C.byref(n), C.byref(secs), C.byref(its))
+        rc = getattr(self.h, _fn)(text.encode(), policy.encode() if policy else None,
+                                  C.byref(out), C.byref(n), C.byref(secs), C.byref(its))
         if rc != 0:
             raise RuntimeError(self.h.ref_last_error().decode())
         try:
             return C.string_at(out.value, n.value).decode(), secs.value, its.value
         finally:
             self.h.ref_free(out)
+
+    def run_config_timed(self, config, policy=None):
+        """(log, seconds of the decision engine alone — Simulation::run, no calibration/ingest, iterations)"""
+        return self.run_config_jsonl(config, policy, _fn="ref_run_config_timed")
 
     def dfs(self, residents, b_max, k_min, flat_oracle=False):
         arr = np.ascontiguousarray(np.asarray(residents, dtype=np.int64).reshape(-1, 3))

@@ -137,7 +137,7 @@ def test_constant_v_known_answer(oracle):
     assert np.all(got == np.float32(0.375))
 
 
-def test_repeat_launch_rearms_semaphores(oracle):
+def test_repeat_launch_rearms_work_counters(oracle):
     _run_case(oracle, 32, 32, 1, 0, [3000, 2500, 10], seed=51, repeat=3, append=False)
 
 

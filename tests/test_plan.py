@@ -97,3 +97,14 @@ def test_plan_errors_follow_reference_messages():
         build([40], append=False, short_table=True)
     with pytest.raises(ValueError, match="group size"):
         build([10], n_q=24, n_kv=8)
+
+
+def test_plan_flags_requests_without_an_append_page():
+    """A request whose page list stops at ceil(seq/16) pages (no page for token index seq) is
+    counted in append_missing, so a launch that appends K/V rows is rejected rather than
+    silently dropping the row (asv_decode_attention checks it)."""
+    plan, _, _, _ = build([16, 17, 32, 40], append=True)
+    assert plan.append_missing == 0
+    plan, _, _, _ = build([16, 17, 32, 40], append=False)
+    # seq 16 and 32 end exactly on a page boundary: their append position needs one more page
+    assert plan.append_missing == 2
