@@ -292,6 +292,27 @@ typedef struct asv_engine_opts {
                                    device) into its host-pool pages, on its own PCIe stream; a later
                                    host->GPU fetch of the request waits for it (pool_insert happens
                                    at transfer completion).  Prefill compute itself stays virtual. */
+    int32_t probe_bubble;       /* 1: per-warp %globaltimer start/end of EVERY attention launch of every
+                                   timed iteration -> measured intra-iteration bubble per iteration
+                                   (reference bubble_from_per_request cost_model.hpp:149-155,
+                                   IterationRecord.bubble_ms cluster_sim.hpp:489).  Off: no probe. */
+    double* bubble_out;         /* optional [bubble_out_cap]: measured bubble (ms, idle time per warp summed
+                                   over the iteration's launches) of each timed iteration, in order */
+    int64_t bubble_out_cap;
+    /* Content-check test mode (1): every KV row and query is a pure function of (global request id,
+     * token position, layer, K|V|Q, head) — 128 values int8/128 (queries int8/8) from splitmix64, see
+     * oracle/attn_oracle.c asv_oracle_content_row — the host pool is per request (not aliased) and
+     * filled with the prompt rows, every iteration uploads its queries and appended rows, the device
+     * pools start poisoned (NaN), and every iteration's attention output of every layer is captured.
+     * Requires execute_transfers, exec_begin = copy_begin = 0, exec_end = -1, no full_step, no
+     * prefill offload; batches <= 1024 rows. */
+    int32_t content_check;
+    const char* capture_path;   /* content_check: binary file, one record per executed iteration:
+                                   int64 seq; int32 b, L, n_q, head; int64 ids[b] (global request ids,
+                                   running order); int32 lens[b] (= prefix_len, attended tokens);
+                                   bf16 out[L][b][n_q][128] when head == -1 (every capture_every-th
+                                   iteration, by seq) else out[L][b][128] of query head `head` */
+    int64_t capture_every;
 } asv_engine_opts;
 
 /* transfer kinds for the per-kind byte counters */
@@ -330,9 +351,10 @@ typedef struct asv_engine_stats {
     int64_t h2d_bytes_window;     /* the physical moves above restricted to the timed window */
     int64_t d2h_bytes_window;
     int64_t p2p_bytes_window;
-    double measured_idle_frac;    /* 1 - sum(warp busy) / (warps x launch span), layer-0 launch of each
-                                     timed iteration, from per-warp %globaltimer */
-    double measured_bubble_ms;    /* sum over timed iterations of the mean idle time per warp x layers */
+    double measured_idle_frac;    /* probe_bubble: 1 - sum(warp busy) / (warps x launch span) over every
+                                     attention launch of the timed iterations (per-warp %globaltimer) */
+    double measured_bubble_ms;    /* probe_bubble: sum over timed iterations of the idle time per warp,
+                                     summed over the iteration's launches */
     double pcie_union_ms;         /* union of the PCIe copy-group intervals (both directions) inside the
                                      window: time the host link had work (with a separate prefetch GPU: the union
                                      of its timed PCIe copy groups, from the first one) */
@@ -344,6 +366,12 @@ typedef struct asv_engine_stats {
     int64_t offload_bytes;        /* prefill_offload D2H bytes executed (== logical prefill_offload bytes
                                      of the executed span) */
     int64_t offload_bytes_window; /* the same restricted to the timed window */
+    /* probe_bubble: distribution of the measured per-iteration bubble over the timed iterations */
+    int64_t bubble_iterations;
+    double bubble_p50_ms, bubble_p90_ms, bubble_p99_ms, bubble_max_ms;
+    int64_t content_inplace_bytes;        /* content mode: merged-FCFS prompts written in place (not a
+                                             reference transfer, not in h2d_bytes) */
+    int64_t content_iterations_captured;  /* content mode: records written to capture_path */
 } asv_engine_stats;
 
 int asv_engine_run(const char* config_json, const char* policy_override, const asv_engine_opts* opts,

@@ -199,3 +199,132 @@ void asv_oracle_get_row(const uint8_t* page, int n_kv, int layer, int kv, int he
     const int64_t blk = (((int64_t)layer * 2 + kv) * n_kv + head) * 4096;
     for (int d = 0; d < 128; ++d) memcpy(&row128[d], page + blk + swz_off(t, d), 2);
 }
+
+/* ------------------------------------------------------------------------ */
+/* Content-check restatement (engine test mode asv_engine_opts.content_check,  */
+/* include/asv.h): every K/V row and query of the executed engine is a pure     */
+/* function of (global request id, token position, layer, kind, head), so the  */
+/* attention output of any executed iteration follows from the iteration's     */
+/* (request id, prefix_len) list alone — PAPER Eq. 2 over rows 0..s-1 of that */
+/* request, independent of pages, copies and pools.                           */
+/*   key  = ((((id << 21 | pos) << 6 | layer) << 2 | kind) << 8) | head,       */
+/*          kind 0 = K, 1 = V, 2 = Q                                           */
+/*   seed = mix(key + G); word w (0..15) = mix(seed + (w+1) G), G = golden     */
+/*   value[8w + j] = (int8)(word >> 8j) / 128  (queries: / 8)                  */
+/* mix = the splitmix64 finalizer (reference prng.hpp:14-19).                 */
+/* ------------------------------------------------------------------------ */
+static inline uint64_t cc_mix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+static void cc_row_f32(int64_t id, int64_t pos, int layer, int kind, int head, float* out) {
+    const uint64_t G = 0x9E3779B97F4A7C15ULL;
+    const uint64_t key = ((((((uint64_t)id << 21) | (uint64_t)pos) << 6 | (uint64_t)layer) << 2 | (uint64_t)kind)
+                          << 8) | (uint64_t)head;
+    const uint64_t seed = cc_mix(key + G);
+    const float scale = kind == 2 ? 1.f / 8.f : 1.f / 128.f;
+    for (int w = 0; w < 16; ++w) {
+        const uint64_t v = cc_mix(seed + (uint64_t)(w + 1) * G);
+        for (int j = 0; j < 8; ++j) out[8 * w + j] = (float)(int8_t)(v >> (8 * j)) * scale;
+    }
+}
+
+/* bf16 bits of one content row (tests) */
+void asv_oracle_content_row(int64_t id, int64_t pos, int layer, int kind, int head, uint16_t* out128) {
+    float f[128];
+    cc_row_f32(id, pos, layer, kind, head, f);
+    for (int d = 0; d < 128; ++d) {
+        uint32_t u;
+        memcpy(&u, &f[d], 4);
+        out128[d] = (uint16_t)(u >> 16);
+    }
+}
+
+typedef struct {
+    int n_q, n_kv, L, batch, only_kvh;
+    const int64_t* ids;
+    const int32_t* lens;
+    float sm_scale;
+    float* out;  /* [L][b][n_q][128] */
+    int next;
+    pthread_mutex_t mu;
+} cc_job_t;
+
+/* one (request, layer, kv head): the g query heads of the group, online softmax in double */
+static void cc_one(const cc_job_t* j, int r, int layer, int kvh) {
+    const int g = j->n_q / j->n_kv, s = j->lens[r];
+    const int64_t id = j->ids[r];
+    float q[8][128], k[128], v[128];
+    double m[8], l[8], o[8][128];
+    for (int a = 0; a < g; ++a) {
+        cc_row_f32(id, s, layer, 2, kvh * g + a, q[a]);
+        m[a] = -INFINITY;
+        l[a] = 0.0;
+        for (int d = 0; d < 128; ++d) o[a][d] = 0.0;
+    }
+    for (int t = 0; t < s; ++t) {
+        cc_row_f32(id, t, layer, 0, kvh, k);
+        cc_row_f32(id, t, layer, 1, kvh, v);
+        for (int a = 0; a < g; ++a) {
+            float acc = 0.f;
+            for (int d = 0; d < 128; ++d) acc += q[a][d] * k[d];
+            const double sc = (double)(acc * j->sm_scale);
+            if (sc > m[a]) {
+                const double c = exp(m[a] - sc);
+                l[a] *= c;
+                for (int d = 0; d < 128; ++d) o[a][d] *= c;
+                m[a] = sc;
+            }
+            const double p = exp(sc - m[a]);
+            l[a] += p;
+            for (int d = 0; d < 128; ++d) o[a][d] += p * (double)v[d];
+        }
+    }
+    for (int a = 0; a < g; ++a) {
+        float* dst = j->out + (((int64_t)layer * j->batch + r) * j->n_q + kvh * g + a) * 128;
+        for (int d = 0; d < 128; ++d) dst[d] = s > 0 ? (float)(o[a][d] / l[a]) : 0.f;
+    }
+}
+
+static void* cc_worker(void* arg) {
+    cc_job_t* j = (cc_job_t*)arg;
+    const int nk = j->only_kvh >= 0 ? 1 : j->n_kv;
+    const int total = j->L * j->batch * nk;
+    for (;;) {
+        pthread_mutex_lock(&j->mu);
+        const int k = j->next++;
+        pthread_mutex_unlock(&j->mu);
+        if (k >= total) break;
+        cc_one(j, (k / nk) % j->batch, k / (nk * j->batch), j->only_kvh >= 0 ? j->only_kvh : k % nk);
+    }
+    return NULL;
+}
+
+/* Expected attention output of an executed content-mode iteration: every layer, every row
+ * (ids[r], lens[r]) in running order.  out: [L][batch][n_q][128] fp32 (only the query heads of kv
+ * head `only_kvh` are written when it is >= 0).  Returns 0 on success. */
+int asv_oracle_content_attention(int n_q, int n_kv, int num_layers, const int64_t* ids, const int32_t* lens,
+                                 int batch, float sm_scale, float* out, int threads, int only_kvh) {
+    if (n_kv <= 0 || n_q % n_kv != 0 || n_q / n_kv > 8 || batch < 1 || num_layers < 1 || only_kvh >= n_kv) return 1;
+    cc_job_t j;
+    j.only_kvh = only_kvh;
+    j.n_q = n_q;
+    j.n_kv = n_kv;
+    j.L = num_layers;
+    j.batch = batch;
+    j.ids = ids;
+    j.lens = lens;
+    j.sm_scale = sm_scale;
+    j.out = out;
+    j.next = 0;
+    pthread_mutex_init(&j.mu, NULL);
+    if (threads < 1) threads = 1;
+    if (threads > 256) threads = 256;
+    pthread_t tids[256];
+    for (int i = 0; i < threads; ++i) pthread_create(&tids[i], NULL, cc_worker, &j);
+    for (int i = 0; i < threads; ++i) pthread_join(tids[i], NULL);
+    pthread_mutex_destroy(&j.mu);
+    return 0;
+}

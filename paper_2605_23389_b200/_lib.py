@@ -116,6 +116,12 @@ class EngineOpts(C.Structure):
         ("full_step", C.c_int32),
         ("intermediate_size", C.c_int32),
         ("execute_prefill_offload", C.c_int32),
+        ("probe_bubble", C.c_int32),
+        ("bubble_out", C.c_void_p),
+        ("bubble_out_cap", C.c_int64),
+        ("content_check", C.c_int32),
+        ("capture_path", C.c_char_p),
+        ("capture_every", C.c_int64),
     ]
 
 
@@ -158,6 +164,13 @@ class EngineStats(C.Structure):
         ("weight_bytes", C.c_int64),
         ("offload_bytes", C.c_int64),
         ("offload_bytes_window", C.c_int64),
+        ("bubble_iterations", C.c_int64),
+        ("bubble_p50_ms", C.c_double),
+        ("bubble_p90_ms", C.c_double),
+        ("bubble_p99_ms", C.c_double),
+        ("bubble_max_ms", C.c_double),
+        ("content_inplace_bytes", C.c_int64),
+        ("content_iterations_captured", C.c_int64),
     ]
 
     def as_dict(self):

@@ -75,6 +75,9 @@ cudaError_t attn_occupancy(int group, int* blocks_per_sm);
 cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st);
 // n_int32 rounded up to a multiple of 4 (16-byte units); both pointers 16-byte aligned
 cudaError_t sm_copy(const int32_t* src, int32_t* dst, int64_t n_int32, cudaStream_t st);
+// per attention launch l: out[3l..3l+2] = (first warp start, last warp end, summed warp busy) of the
+// launch's per-warp %globaltimer pairs ts[l][workers][2], which it zeroes (measured bubble)
+cudaError_t warp_span_reduce(uint64_t* ts, int32_t workers, int32_t launches, uint64_t* out, cudaStream_t st);
 
 // device-to-device KV page moves on the SMs (kv_move.cu): pages per launch (kernel parameter arrays)
 constexpr int kMoveChunk = 1024;

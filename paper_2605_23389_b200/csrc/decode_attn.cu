@@ -939,6 +939,8 @@ int attn_warps_per_cta(int group, bool f16) {
 }
 
 __global__ void sm_copy_kernel(const int4* __restrict__ src, int4* __restrict__ dst, int64_t n16);
+__global__ void warp_span_reduce_kernel(unsigned long long* __restrict__ ts, int32_t workers,
+                                        unsigned long long* __restrict__ out);
 
 cudaError_t attn_occupancy(int group, int* blocks_per_sm) {
     // both KV types: same shared memory and occupancy; loading both keeps lazy module
@@ -955,6 +957,8 @@ cudaError_t attn_occupancy(int group, int* blocks_per_sm) {
     e = cudaFuncGetAttributes(&fa, merge_splits_kernel<false>);
     if (e != cudaSuccess) return e;
     e = cudaFuncGetAttributes(&fa, merge_splits_kernel<true>);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncGetAttributes(&fa, warp_span_reduce_kernel);
     if (e != cudaSuccess) return e;
     return cudaFuncGetAttributes(&fa, sm_copy_kernel);
 }
@@ -1001,6 +1005,53 @@ cudaError_t sm_copy(const int32_t* src, int32_t* dst, int64_t n_int32, cudaStrea
     if (blocks > sms) blocks = sms;
     sm_copy_kernel<<<static_cast<unsigned>(blocks), threads, 0, st>>>(reinterpret_cast<const int4*>(src),
                                                                       reinterpret_cast<int4*>(dst), n16);
+    return cudaGetLastError();
+}
+
+// Measured bubble: one CTA per attention launch reduces the launch's
+// per-warp (start, end) %globaltimer pairs to (first start, last end, summed busy
+// time of the warps that ran).  idle = (last end - first start) * warps - busy.
+__global__ void warp_span_reduce_kernel(unsigned long long* __restrict__ ts, int32_t workers,
+                                        unsigned long long* __restrict__ out) {
+    unsigned long long* t = ts + static_cast<int64_t>(blockIdx.x) * workers * 2;
+    unsigned long long lo = ~0ull, hi = 0, busy = 0;
+    for (int w = threadIdx.x; w < workers; w += blockDim.x) {
+        const unsigned long long a = t[2 * w], b = t[2 * w + 1];
+        t[2 * w] = t[2 * w + 1] = 0;  // consumed: a warp that does not run next time is skipped, not stale
+        if (b <= a) continue;
+        lo = min(lo, a);
+        hi = max(hi, b);
+        busy += b - a;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        busy += __shfl_xor_sync(0xffffffffu, busy, o);
+    }
+    __shared__ unsigned long long s_lo[8], s_hi[8], s_busy[8];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        s_lo[warp] = lo;
+        s_hi[warp] = hi;
+        s_busy[warp] = busy;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
+            lo = min(lo, s_lo[w]);
+            hi = max(hi, s_hi[w]);
+            busy += s_busy[w];
+        }
+        out[3 * blockIdx.x] = lo;
+        out[3 * blockIdx.x + 1] = hi;
+        out[3 * blockIdx.x + 2] = busy;
+    }
+}
+
+cudaError_t warp_span_reduce(uint64_t* ts, int32_t workers, int32_t launches, uint64_t* out, cudaStream_t st) {
+    if (launches <= 0) return cudaSuccess;
+    warp_span_reduce_kernel<<<launches, 256, 0, st>>>(reinterpret_cast<unsigned long long*>(ts), workers,
+                                                      reinterpret_cast<unsigned long long*>(out));
     return cudaGetLastError();
 }
 

@@ -182,6 +182,94 @@ struct ReqKV {
     int64_t prefix = 0;
 };
 
+// Content mode (asv_engine_opts.content_check, a test mode): every KV row and
+// every query is a pure function of (global request id, token position,
+// layer, K|V|Q, head), so the output of any executed iteration can be checked
+// against an independent CPU restatement (oracle/attn_oracle.c,
+// asv_oracle_content_attention) without shadowing the page pools: a page moved
+// to the wrong place, reused too early, or copied with the wrong byte count
+// changes the attention output.  Values are k/128 (k an int8 from splitmix64),
+// queries k/8: exact in bf16, and the 16x query scale makes each softmax peak
+// on a few keys so one wrong page moves the output by O(1).
+namespace content {
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ULL;
+inline uint64_t mix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+enum Kind { kK = 0, kV = 1, kQ = 2 };
+inline uint64_t key(int64_t req, int64_t pos, int layer, int kind, int head) {
+    return ((((static_cast<uint64_t>(req) << 21 | static_cast<uint64_t>(pos)) << 6 | static_cast<uint64_t>(layer))
+                 << 2 |
+             static_cast<uint64_t>(kind))
+            << 8) |
+           static_cast<uint64_t>(head);
+}
+// the 128 bf16 values of one row
+inline void row(uint64_t k, bool query, uint16_t* out) {
+    const uint64_t seed = mix(k + kGolden);
+    const float scale = query ? 1.f / 8.f : 1.f / 128.f;
+    for (int w = 0; w < 16; ++w) {
+        const uint64_t v = mix(seed + static_cast<uint64_t>(w + 1) * kGolden);
+        for (int j = 0; j < 8; ++j) {
+            const float f = static_cast<float>(static_cast<int8_t>(v >> (8 * j))) * scale;
+            uint32_t u;
+            std::memcpy(&u, &f, 4);
+            out[w * 8 + j] = static_cast<uint16_t>(u >> 16);  // exact: <= 8 significant bits
+        }
+    }
+}
+}  // namespace content
+
+// Per-request host-pool pages of content mode (no aliasing): pinned arena, bump
+// allocated; a page gets the prompt rows it covers when it is first handed out,
+// later rows arrive through the engine's own D2H write-backs.
+class ContentStore {
+ public:
+    void init(char* arena, int64_t arena_pages, int64_t page_bytes, int32_t layers, int32_t n_kv) {
+        arena_ = arena;
+        cap_ = arena_pages;
+        page_bytes_ = page_bytes;
+        layers_ = layers;
+        n_kv_ = n_kv;
+    }
+    char* page(int64_t global_id, std::size_t local, int64_t j, int64_t prompt_len) {
+        if (local >= pages_.size()) pages_.resize(local + 1);
+        auto& v = pages_[local];
+        while (static_cast<int64_t>(v.size()) <= j) {
+            if (used_ >= cap_) throw std::runtime_error("content mode: host pool exhausted (raise host_pool_bytes)");
+            char* p = arena_ + used_++ * page_bytes_;
+            const int64_t t0 = static_cast<int64_t>(v.size()) * 16;
+            fill(p, global_id, t0, std::min<int64_t>(t0 + 16, prompt_len));
+            v.push_back(p);
+        }
+        return v[static_cast<std::size_t>(j)];
+    }
+
+ private:
+    // prompt rows [t0, t1) of the page starting at token t0 (page-major host layout, XOR swizzle)
+    void fill(char* p, int64_t id, int64_t t0, int64_t t1) const {
+        uint16_t r[128];
+        for (int64_t t = t0; t < t1; ++t) {
+            const int64_t tr = t - t0;
+            for (int l = 0; l < layers_; ++l) {
+                for (int kv = 0; kv < 2; ++kv) {
+                    for (int h = 0; h < n_kv_; ++h) {
+                        content::row(content::key(id, t, l, kv, h), false, r);
+                        char* blk = p + ((static_cast<int64_t>(l) * 2 + kv) * n_kv_ + h) * 4096 + tr * 256;
+                        for (int c = 0; c < 16; ++c) std::memcpy(blk + ((c ^ (tr & 7)) << 4), r + 8 * c, 16);
+                    }
+                }
+            }
+        }
+    }
+    char* arena_ = nullptr;
+    int64_t cap_ = 0, used_ = 0, page_bytes_ = 0;
+    int32_t layers_ = 0, n_kv_ = 0;
+    std::vector<std::vector<char*>> pages_;
+};
+
 class GpuExecutor : public prefixsim::EngineObserver {
  public:
     GpuExecutor(const asv_engine_opts& o, const prefixsim::SimConfig& sim, const prefixsim::ModelSpec& spec,
@@ -197,6 +285,13 @@ class GpuExecutor : public prefixsim::EngineObserver {
                                         std::to_string(spec.kv_bytes_per_token()) + ")");
         }
         pair_ = o.prefetch_device != o.decode_device || o.pair_mode != 0;
+        content_ = o.content_check != 0;
+        if (content_ && (!o.execute_transfers || o.exec_begin != 0 || o.exec_end >= 0 || o.copy_begin != 0 ||
+                         o.full_step || o.execute_prefill_offload)) {
+            throw std::invalid_argument(
+                "content_check needs execute_transfers, every iteration and KV move executed (exec_begin = "
+                "copy_begin = 0, exec_end = -1), attention-only steps and no prefill offload");
+        }
         const bool peer = o.prefetch_device != o.decode_device;
         const int64_t bmax = sim.b_max_blocks(), crb = sim.crb_capacity_blocks();
         dec_pages_ = sim.cluster.decode_hbm_blocks + (pair_ ? 0 : bmax + crb) + 64;
@@ -217,6 +312,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
         dec_.set_health_check([this] { check_workers(); });
         pre_.set_health_check([this] { check_workers(); });
         dec_.init(o.decode_device, dec_pages_, page_bytes_, slice_, &flags_);
+        if (content_) ASV_CUDA(cudaMemset(dec_.base(), 0xff, static_cast<size_t>(dec_pages_ * page_bytes_)));
         if (pair_ && peer) {
             ASV_CUDA(cudaSetDevice(o.decode_device));
             int can = 0;
@@ -230,7 +326,10 @@ class GpuExecutor : public prefixsim::EngineObserver {
             if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) ASV_CUDA(e);
             cudaGetLastError();
         }
-        if (pair_) pre_.init(o.prefetch_device, pre_pages_, page_bytes_, slice_, &flags_);
+        if (pair_) {
+            pre_.init(o.prefetch_device, pre_pages_, page_bytes_, slice_, &flags_);
+            if (content_) ASV_CUDA(cudaMemset(pre_.base(), 0xff, static_cast<size_t>(pre_pages_ * page_bytes_)));
+        }
         // streams
         ASV_CUDA(cudaSetDevice(o.decode_device));
         ASV_CUDA(cudaStreamCreateWithFlags(&compute_, cudaStreamNonBlocking));
@@ -250,6 +349,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
             ASV_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&arena_), static_cast<size_t>(arena_pages_ * page_bytes_),
                                    cudaHostAllocPortable));
             std::memset(arena_, 0, static_cast<size_t>(arena_pages_ * page_bytes_));
+            if (content_) content_store_.init(arena_, arena_pages_, page_bytes_, o.num_layers, o.num_kv_heads);
             if (o.execute_prefill_offload) {
                 // prefill output ring on the prefill (= prefetch) GPU: <= 512 MiB of pages that the
                 // offload copies read in rotation (the prefill compute is not executed)
@@ -263,11 +363,12 @@ class GpuExecutor : public prefixsim::EngineObserver {
         int32_t workers = 0;
         if (asv_attn_num_workers(&shape_, o.decode_device, &workers) != ASV_OK) throw CudaError(asv_last_error());
         workers_ = workers;
-        max_rows_ = std::min<int64_t>(dec_pages_, 16384);
+        max_rows_ = std::min<int64_t>(dec_pages_, content_ ? 1024 : 16384);
         const int64_t qbytes = max_rows_ * o.num_q_heads * 256;
         const int64_t kvbytes = max_rows_ * o.num_kv_heads * 256;
         ASV_CUDA(cudaMalloc(&q_, static_cast<size_t>(qbytes)));
-        ASV_CUDA(cudaMalloc(&out_, static_cast<size_t>(qbytes)));
+        // content mode keeps every layer's output of the iteration (checked against the oracle)
+        ASV_CUDA(cudaMalloc(&out_, static_cast<size_t>(qbytes * (content_ ? o.num_layers : 1))));
         if (o.execute_transfers) {  // e2e: every iteration's result lands in host memory
             ASV_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&result_host_), static_cast<size_t>(qbytes),
                                    cudaHostAllocMapped));
@@ -297,10 +398,27 @@ class GpuExecutor : public prefixsim::EngineObserver {
         slot_seq_.assign(static_cast<size_t>(ring_), 0);
         slot_b_.assign(static_cast<size_t>(ring_), 0);
         slot_waits_.assign(static_cast<size_t>(ring_), 0);
-        ts_host_.resize(static_cast<size_t>(2 * workers_));
-        // per-warp timestamps land in mapped host memory (no copy back, no copy-engine queue)
-        ASV_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ts_arena_),
-                               static_cast<size_t>(ring_) * static_cast<size_t>(workers_) * 16, cudaHostAllocMapped));
+        if (o.probe_bubble) {
+            // per-warp %globaltimer (start, end) of every attention launch of a timed iteration, in
+            // device memory; after the iteration one small kernel reduces each launch to (first start,
+            // last end, summed busy) in mapped host memory, read at retire
+            ASV_CUDA(cudaMalloc(&ts_dev_, static_cast<size_t>(o.num_layers) * workers_ * 16));
+            ASV_CUDA(cudaMemset(ts_dev_, 0, static_cast<size_t>(o.num_layers) * workers_ * 16));
+            ASV_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&span_host_),
+                                   static_cast<size_t>(ring_) * o.num_layers * 3 * 8, cudaHostAllocMapped));
+        }
+        if (content_) {
+            cap_words_ = max_rows_ * o.num_q_heads * 64 * o.num_layers;  // int32 words of one iteration's out
+            ASV_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&cap_host_),
+                                   static_cast<size_t>(ring_) * static_cast<size_t>(cap_words_) * 4,
+                                   cudaHostAllocMapped));
+            slot_ids_.assign(static_cast<size_t>(ring_), {});
+            slot_lens_.assign(static_cast<size_t>(ring_), {});
+            if (o.capture_path != nullptr) {
+                capture_ = std::fopen(o.capture_path, "wb");
+                if (capture_ == nullptr) throw std::runtime_error(std::string("cannot open ") + o.capture_path);
+            }
+        }
         for (int i = 0; i < ring_; ++i) {
             ASV_CUDA(cudaEventCreate(&att_beg_[static_cast<size_t>(i)]));
             ASV_CUDA(cudaEventCreate(&att_end_[static_cast<size_t>(i)]));
@@ -354,7 +472,10 @@ class GpuExecutor : public prefixsim::EngineObserver {
         if (plan_arena_dev_) cudaFree(plan_arena_dev_);
         for (auto e : att_beg_) cudaEventDestroy(e);
         for (auto e : att_end_) cudaEventDestroy(e);
-        if (ts_arena_) cudaFreeHost(ts_arena_);
+        if (ts_dev_) cudaFree(ts_dev_);
+        if (span_host_) cudaFreeHost(span_host_);
+        if (cap_host_) cudaFreeHost(cap_host_);
+        if (capture_) std::fclose(capture_);
         for (auto& pr : copy_timers_) {
             if (pr.a) cudaEventDestroy(pr.a);
             if (pr.b) cudaEventDestroy(pr.b);
@@ -396,7 +517,13 @@ class GpuExecutor : public prefixsim::EngineObserver {
         } else if (act == "admit" && a.from == "wait_queue" && !admit_moved_) {
             // merged-instance FCFS: the prompt is processed in place on the decode GPU
             ReqKV& r = kv(a.request_id);
-            if (r.pages.empty()) {
+            if (r.pages.empty() && content_) {
+                // content mode: the prompt's KV (computed in place by the merged instance) is written into
+                // its pages from the content store, so later iterations attend over real rows
+                begin_xfer_group(kUrgent);
+                fetch_from_host(a.request_id, &dec_, /*prefill_in_place=*/true);
+                end_xfer_group();
+            } else if (r.pages.empty()) {
                 r.prefix = a.blocks * 16;  // only the page count matters for the prompt's KV
                 for (int64_t i = 0; i < a.blocks; ++i) r.pages.push_back(dec_.alloc());
                 r.where = ReqKV::kDecode;
@@ -529,25 +656,41 @@ class GpuExecutor : public prefixsim::EngineObserver {
             }
         }
         const int64_t ready_waits = static_cast<int64_t>(waits.size());
-        // plan (+ for full steps the token positions = prefix lengths, for RoPE) in one upload
+        // plan (+ for full steps the token positions = prefix lengths, for RoPE; + in content mode
+        // the iteration's queries and appended K/V rows of every layer) in one upload
+        const int64_t b_rows = static_cast<int64_t>(running.size());
         const int64_t plan_words = (static_cast<int64_t>(plan.total_int32) + 3) & ~int64_t(3);
-        const int64_t pos_words = o_.full_step ? static_cast<int64_t>(running.size()) : 0;
-        const int64_t pw = plan_region(e, plan_words + ((pos_words + 3) & ~int64_t(3)));
+        const int64_t pos_words = o_.full_step ? b_rows : 0;
+        const int64_t q_words = content_ ? b_rows * o_.num_q_heads * 64 : 0;    // [L][b][n_q][128] bf16
+        const int64_t kv_words = content_ ? b_rows * o_.num_kv_heads * 64 : 0;  // [L][b][n_kv][128] (K, V)
+        const int64_t payload_words =
+            ((pos_words + 3) & ~int64_t(3)) + static_cast<int64_t>(o_.num_layers) * (q_words + 2 * kv_words);
+        const int64_t pw = plan_region(e, plan_words + payload_words);
         std::memcpy(plan_arena_host_ + pw, plan_scratch_.data(), static_cast<size_t>(plan.total_int32) * 4);
         for (int64_t i = 0; i < pos_words; ++i) plan_arena_host_[pw + plan_words + i] = seq_[static_cast<size_t>(i)];
+        if (content_) write_content_payload(running, plan_arena_host_ + pw + plan_words, q_words, kv_words);
         const bool open_window = timed && !window_open_;
         window_open_ = window_open_ || timed;
         const uint32_t launch0 = launches_;
         launches_ += static_cast<uint32_t>(o_.num_layers);
-        uint64_t* ts = timed ? ts_slot(slot) : nullptr;
-        const int64_t result_bytes = result_host_ ? static_cast<int64_t>(running.size()) * o_.num_q_heads * 256 : 0;
-        if (o_.full_step && static_cast<int64_t>(running.size()) > max_rows_full_)
+        const bool probe = timed && ts_dev_ != nullptr;
+        const int64_t result_bytes = result_host_ ? b_rows * o_.num_q_heads * 256 : 0;
+        if (o_.full_step && b_rows > max_rows_full_)
             throw std::runtime_error("full_step: batch exceeds the activation buffers");
+        if (content_) {
+            slot_ids_[slot].clear();
+            slot_lens_[slot].clear();
+            for (const auto& m : running) {
+                slot_ids_[slot].push_back(global_id(m.id));
+                slot_lens_[slot].push_back(static_cast<int32_t>(m.prefix_len));
+            }
+            slot_seq_[slot] = seq;
+        }
         // The launch worker enqueues the iteration (so a full compute queue never
         // stalls the decisions that issue future KV moves)
-        const int64_t upload_words = plan_words + pos_words;
-        launcher_.post([this, e, slot, pw, plan, waits = std::move(waits), open_window, launch0, ts, result_bytes,
-                        upload_words] {
+        const int64_t upload_words = plan_words + payload_words;
+        launcher_.post([this, e, slot, pw, plan, waits = std::move(waits), open_window, launch0, probe, result_bytes,
+                        upload_words, plan_words, pos_words, q_words, kv_words, b_rows] {
             ASV_CUDA(cudaSetDevice(o_.decode_device));
             if (open_window) ASV_CUDA(cudaEventRecord(win_beg_, compute_));
             for (const auto& [lane, v] : waits) flags_.wait(compute_, lane, v);
@@ -570,18 +713,34 @@ class GpuExecutor : public prefixsim::EngineObserver {
             args.sm_scale = 0.08838834764831845f;
             const int32_t b = pl.batch;
             const int32_t* positions = plan_arena_dev_ + pw + ((pl.total_int32 + 3) & ~3);
+            const int32_t* payload = plan_arena_dev_ + pw + plan_words + ((pos_words + 3) & ~int64_t(3));
             for (int l = 0; l < o_.num_layers; ++l) {
                 if (o_.full_step) layer_front(l, b, positions);  // RMSNorm, QKV + RoPE -> q_, k_new_, v_new_
+                if (content_) {  // this layer's queries / appended rows from the upload, its own output slice
+                    const int32_t* lp = payload + static_cast<int64_t>(l) * (q_words + 2 * kv_words);
+                    args.q = lp;
+                    args.k_new = lp + q_words;
+                    args.v_new = lp + q_words + kv_words;
+                    args.out = static_cast<char*>(out_) + static_cast<int64_t>(l) * b_rows * o_.num_q_heads * 256;
+                }
                 args.layer = l;
                 args.launch_index = launch0 + static_cast<uint32_t>(l);
-                args.warp_timestamps = l == 0 ? ts : nullptr;
+                args.warp_timestamps = probe ? ts_dev_ + static_cast<int64_t>(l) * workers_ * 2 : nullptr;
                 // layer 0 of attention-only steps reads the plan the upload kernel just wrote
                 args.pdl = (l == 0 && !o_.full_step) ? 0 : o_.pdl;
                 if (asv_decode_attention(&shape_, &args, compute_) != ASV_OK) throw CudaError(asv_last_error());
                 if (o_.full_step) layer_back(l, b);  // O + residual, RMSNorm, gate/up SiLU, down + residual
             }
             ASV_CUDA(cudaEventRecord(att_end_[slot], compute_));
-            if (result_bytes > 0) {  // the step's result (last layer's output / hidden state) read back
+            if (probe) {  // per launch: first warp start, last warp end, summed warp busy time
+                ASV_CUDA(warp_span_reduce(ts_dev_, workers_, o_.num_layers,
+                                          span_host_ + slot * static_cast<size_t>(o_.num_layers) * 3, compute_));
+            }
+            if (content_) {  // every layer's output of the iteration -> its capture slot
+                ASV_CUDA(sm_copy(static_cast<const int32_t*>(out_),
+                                 cap_host_ + slot * static_cast<size_t>(cap_words_),
+                                 b_rows * o_.num_q_heads * 64 * o_.num_layers, compute_));
+            } else if (result_bytes > 0) {  // the step's result (last layer's output / hidden state) read back
                 ASV_CUDA(sm_copy(static_cast<const int32_t*>(o_.full_step ? h_ : out_),
                                  reinterpret_cast<int32_t*>(result_host_), result_bytes / 4, compute_));
             }
@@ -598,7 +757,8 @@ class GpuExecutor : public prefixsim::EngineObserver {
             stats_.tokens_timed += static_cast<int64_t>(running.size());
             stats_.attn_launches += o_.num_layers;
             // attention (+ merge) per layer, the plan upload, and the e2e result read-back
-            stats_.kernel_launches_timed += o_.num_layers * (plan.n_merge > 0 ? 2 : 1) + 1 + (result_bytes > 0 ? 1 : 0);
+            stats_.kernel_launches_timed += o_.num_layers * (plan.n_merge > 0 ? 2 : 1) + 1 + (result_bytes > 0 ? 1 : 0) +
+                                            (probe ? 1 : 0);
             if (o_.full_step) {  // per layer: 2 RMSNorm + 4 linear launches per 256-row chunk
                 const int64_t chunks = (static_cast<int64_t>(running.size()) + 255) / 256;
                 // RMSNorm launches: 2 per layer unfused; fused, only layer 0's first one remains
@@ -711,6 +871,24 @@ class GpuExecutor : public prefixsim::EngineObserver {
         }
         stats_.iterations_total = iterations_total_;
         stats_.measured_idle_frac = span_ns_ > 0 ? 1.0 - busy_ns_ / span_ns_ : 0.0;
+        if (!bubble_iters_.empty()) {
+            if (o_.bubble_out != nullptr) {
+                const int64_t n = std::min<int64_t>(o_.bubble_out_cap, static_cast<int64_t>(bubble_iters_.size()));
+                std::copy(bubble_iters_.begin(), bubble_iters_.begin() + n, o_.bubble_out);
+            }
+            std::vector<double> v = bubble_iters_;
+            std::sort(v.begin(), v.end());
+            const auto rank = [&v](double p) {  // nearest rank (reference metrics.hpp nearest_rank)
+                const auto k = static_cast<std::size_t>(std::ceil(p * static_cast<double>(v.size())));
+                return v[std::min(v.size() - 1, k == 0 ? 0 : k - 1)];
+            };
+            stats_.bubble_p50_ms = rank(0.50);
+            stats_.bubble_p90_ms = rank(0.90);
+            stats_.bubble_p99_ms = rank(0.99);
+            stats_.bubble_max_ms = v.back();
+            stats_.bubble_iterations = static_cast<int64_t>(v.size());
+        }
+        if (capture_ != nullptr) std::fflush(capture_);
         stats_.virtual_window_ms = first_timed_start_ >= 0 ? last_timed_end_ms_ - first_timed_start_ : 0.0;
         stats_.virtual_decode_tok_s = log.iterations.empty() ? 0.0 : prefixsim::decode_throughput(log);
         stats_.host_decide_ms = host_ms_;
@@ -910,7 +1088,11 @@ class GpuExecutor : public prefixsim::EngineObserver {
         }
     }
 
-    char* host_page(prefixsim::RequestId id, int64_t j) const {
+    char* host_page(prefixsim::RequestId id, int64_t j) {
+        if (content_) {
+            return content_store_.page(global_id(id), static_cast<std::size_t>(id), j,
+                                       (*requests_)[static_cast<std::size_t>(id)].prompt_len);
+        }
         const int64_t a = (id * 7919 + j) % arena_pages_;
         return arena_ + a * page_bytes_;
     }
@@ -942,7 +1124,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
         return expect;
     }
 
-    void fetch_from_host(prefixsim::RequestId id, PagePool* pool) {
+    void fetch_from_host(prefixsim::RequestId id, PagePool* pool, bool prefill_in_place = false) {
         ReqKV& r = kv(id);
         const prefixsim::Request& q = (*requests_)[static_cast<std::size_t>(id)];
         r.prefix = q.prefix_len;
@@ -956,9 +1138,13 @@ class GpuExecutor : public prefixsim::EngineObserver {
         lane_wait_iteration(lane_, hz);
         lane_wait_host(lane_, r);
         const int64_t moved = post_copy_kv(r.pages, *pool, id, q.prefix_len, true);
-        timer_add(lane_, moved);
-        stats_.h2d_bytes += moved;
-        if (group_timed_) stats_.h2d_bytes_window += moved;
+        if (prefill_in_place) {
+            stats_.content_inplace_bytes += moved;  // not a reference transfer
+        } else {
+            timer_add(lane_, moved);
+            stats_.h2d_bytes += moved;
+            if (group_timed_) stats_.h2d_bytes_window += moved;
+        }
         r.ready_slot = lane_;  // this request is usable as soon as its own pages land
         r.ready_v = lane_signal(lane_);
     }
@@ -1298,7 +1484,54 @@ class GpuExecutor : public prefixsim::EngineObserver {
         if (launcher_.failed()) throw CudaError("launch worker: " + launcher_.error());
     }
 
-    uint64_t* ts_slot(size_t slot) const { return ts_arena_ + slot * static_cast<size_t>(workers_) * 2; }
+    // global request id of a shard-local one (request i of the trace -> shard i % count, Simulation
+    // renumbers its requests 0..n-1: cluster_sim.hpp:137-139)
+    int64_t global_id(prefixsim::RequestId local) const {
+        return static_cast<int64_t>(local) * std::max(1, o_.shard_count) + o_.shard_index;
+    }
+    // content mode: the iteration's queries and appended K/V rows, [L]{q[b][n_q], k[b][n_kv], v[b][n_kv]}
+    void write_content_payload(const std::vector<prefixsim::RunningMember>& running, int32_t* dst, int64_t q_words,
+                               int64_t kv_words) const {
+        for (int l = 0; l < o_.num_layers; ++l) {
+            auto* q = reinterpret_cast<uint16_t*>(dst + static_cast<int64_t>(l) * (q_words + 2 * kv_words));
+            uint16_t* k = q + 2 * q_words;
+            uint16_t* v = k + 2 * kv_words;
+            for (std::size_t r = 0; r < running.size(); ++r) {
+                const int64_t id = global_id(running[r].id), s = running[r].prefix_len;
+                for (int h = 0; h < o_.num_q_heads; ++h)
+                    content::row(content::key(id, s, l, content::kQ, h), true, q + (r * o_.num_q_heads + h) * 128);
+                for (int h = 0; h < o_.num_kv_heads; ++h) {
+                    content::row(content::key(id, s, l, content::kK, h), false, k + (r * o_.num_kv_heads + h) * 128);
+                    content::row(content::key(id, s, l, content::kV, h), false, v + (r * o_.num_kv_heads + h) * 128);
+                }
+            }
+        }
+    }
+    // content mode: one record of the capture file (asv.h asv_engine_opts.capture_path)
+    void write_capture(size_t slot) {
+        if (capture_ == nullptr) return;
+        const auto& ids = slot_ids_[slot];
+        const auto& lens = slot_lens_[slot];
+        const int64_t b = static_cast<int64_t>(ids.size());
+        const int64_t every = std::max<int64_t>(1, o_.capture_every);
+        const int64_t seq = slot_seq_[slot];
+        const bool full = seq % every == 0;
+        const int32_t hdr[4] = {static_cast<int32_t>(b), o_.num_layers, o_.num_q_heads,
+                                full ? -1 : static_cast<int32_t>(seq % o_.num_q_heads)};
+        std::fwrite(&seq, 8, 1, capture_);
+        std::fwrite(hdr, 4, 4, capture_);
+        std::fwrite(ids.data(), 8, static_cast<size_t>(b), capture_);
+        std::fwrite(lens.data(), 4, static_cast<size_t>(b), capture_);
+        const auto* out = reinterpret_cast<const uint16_t*>(cap_host_ + slot * static_cast<size_t>(cap_words_));
+        if (full) {
+            std::fwrite(out, 2, static_cast<size_t>(b * o_.num_q_heads * 128 * o_.num_layers), capture_);
+        } else {  // one head of every row and layer: [L][b][128]
+            const int h = hdr[3];
+            for (int64_t lr = 0; lr < b * o_.num_layers; ++lr)
+                std::fwrite(out + (lr * o_.num_q_heads + h) * 128, 2, 128, capture_);
+        }
+        ++stats_.content_iterations_captured;
+    }
 
     // retire every executed iteration up to and including `e`, in order
     void retire_through(int64_t e) {
@@ -1349,24 +1582,22 @@ class GpuExecutor : public prefixsim::EngineObserver {
                                  ",\"t0\":" + std::to_string(a) + ",\"t1\":" + std::to_string(b) + "}");
             }
             slot_timed_[slot] = 0;
-            // measured bubble of the layer-0 launch: idle warp time inside its span
-            std::memcpy(ts_host_.data(), ts_slot(slot), ts_host_.size() * 8);  // mapped, complete once kIter passed
-            uint64_t lo = UINT64_MAX, hi = 0;
-            double busy = 0.0;
-            for (int32_t w = 0; w < workers_; ++w) {
-                const uint64_t a = ts_host_[2 * w], b = ts_host_[2 * w + 1];
-                if (b <= a) continue;
-                lo = std::min(lo, a);
-                hi = std::max(hi, b);
-                busy += static_cast<double>(b - a);
-            }
-            if (hi > lo) {
-                const double span = static_cast<double>(hi - lo) * workers_;
-                busy_ns_ += busy;
-                span_ns_ += span;
-                stats_.measured_bubble_ms += (span - busy) / workers_ * 1e-6 * o_.num_layers;
+            if (span_host_ != nullptr) {  // measured bubble: idle warp time inside each launch's span
+                const uint64_t* sp = span_host_ + slot * static_cast<size_t>(o_.num_layers) * 3;  // mapped, complete
+                double idle_ms = 0.0;
+                for (int l = 0; l < o_.num_layers; ++l) {
+                    const uint64_t lo = sp[3 * l], hi = sp[3 * l + 1], busy = sp[3 * l + 2];
+                    if (hi <= lo) continue;
+                    const double span = static_cast<double>(hi - lo) * workers_;
+                    busy_ns_ += static_cast<double>(busy);
+                    span_ns_ += span;
+                    idle_ms += (span - static_cast<double>(busy)) / workers_ * 1e-6;
+                }
+                bubble_iters_.push_back(idle_ms);
+                stats_.measured_bubble_ms += idle_ms;
             }
         }
+        if (content_) write_capture(slot);
         dec_.reclaim(false);
         if (pair_) pre_.reclaim(false);
     }
@@ -1431,7 +1662,16 @@ class GpuExecutor : public prefixsim::EngineObserver {
     int64_t arena_words_ = 0, arena_head_ = 0;   // absolute word counter (position = head % arena)
     std::deque<std::pair<int64_t, int64_t>> live_plans_;  // (executed index, absolute begin) in issue order
     int64_t retired_upto_ = 0;                   // every executed iteration below this is retired
-    uint64_t* ts_arena_ = nullptr;
+    uint64_t* ts_dev_ = nullptr;     // probe_bubble: [L][workers][2] per-warp %globaltimer of one iteration
+    uint64_t* span_host_ = nullptr;  // probe_bubble: [ring][L][3] (first start, last end, busy sum), mapped
+    std::vector<double> bubble_iters_;  // measured bubble (ms) of every timed iteration
+    bool content_ = false;           // content_check test mode
+    ContentStore content_store_;
+    int32_t* cap_host_ = nullptr;    // content: [ring][L][rows][n_q][128] bf16 outputs, mapped
+    int64_t cap_words_ = 0;
+    FILE* capture_ = nullptr;
+    std::vector<std::vector<int64_t>> slot_ids_;
+    std::vector<std::vector<int32_t>> slot_lens_;
     std::vector<cudaEvent_t> att_beg_, att_end_;
     std::vector<int> slot_timed_;
     cudaEvent_t win_beg_ = nullptr, win_end_ = nullptr;
@@ -1451,7 +1691,6 @@ class GpuExecutor : public prefixsim::EngineObserver {
     std::vector<int64_t> slot_seq_, slot_b_, slot_waits_;
     double first_timed_start_ = -1.0, last_timed_end_ms_ = 0.0;
 
-    std::vector<uint64_t> ts_host_;
     double busy_ns_ = 0.0, span_ns_ = 0.0;
     asv_engine_stats stats_{};
 };

@@ -79,11 +79,17 @@ def engine_run(config, *, device: int = 0, prefetch_device: int | None = None,
                host_pool_bytes: int = 8 << 30, shard_index: int = 0, shard_count: int = 1,
                pdl: bool = True, run_ahead: int = 256, policy: str | None = None,
                pair_mode: bool = False, full_step: bool = False, intermediate_size: int = 0,
-               prefill_offload: bool | None = None, out_dir: str | None = None, return_log: bool = False):
+               prefill_offload: bool | None = None, out_dir: str | None = None, return_log: bool = False,
+               probe_bubble: bool = False, content_check: bool = False, capture_path: str | None = None,
+               capture_every: int = 1):
     """Run the decode engine on the GPU (asv_engine_run_ex): reference decisions executed for real.
 
     Returns the stats dict; with return_log=True, (stats, schema-1 JSONL log).  out_dir: also write
-    the reference's run artefacts there (log.jsonl, summary.json, CDF CSVs) plus gpu_stats.json."""
+    the reference's run artefacts there (log.jsonl, summary.json, CDF CSVs) plus gpu_stats.json.
+    probe_bubble: measure the intra-iteration bubble of every attention launch of the timed window
+    (stats["bubble_per_iteration_ms"] lists it per timed iteration).  content_check / capture_path /
+    capture_every: the content-check test mode (include/asv.h) writing every executed iteration's
+    attention outputs to capture_path (read it with read_capture)."""
     text = config if isinstance(config, str) else json.dumps(config)
     o = _lib.EngineOpts()
     o.decode_device = device
@@ -104,20 +110,61 @@ def engine_run(config, *, device: int = 0, prefetch_device: int | None = None,
     # and stay virtual when the decode GPU is alone (its PCIe link would carry the prefill instance's
     # traffic too; prefill_offload=True measures exactly that)
     if prefill_offload is None:
-        prefill_offload = execute_transfers and o.prefetch_device != o.decode_device
+        prefill_offload = execute_transfers and o.prefetch_device != o.decode_device and not content_check
     o.execute_prefill_offload = 1 if (execute_transfers and prefill_offload) else 0
+    o.probe_bubble = 1 if probe_bubble else 0
+    bubbles = None
+    if probe_bubble:
+        cap = max(1, exec_end - timed_begin) if exec_end >= 0 else 1 << 20
+        bubbles = np.zeros(cap, np.float64)
+        o.bubble_out = bubbles.ctypes.data
+        o.bubble_out_cap = cap
+    o.content_check = 1 if content_check else 0
+    o.capture_path = capture_path.encode() if capture_path else None
+    o.capture_every = capture_every
     st = _lib.EngineStats()
     h = _lib.lib()
+
+    def stats():
+        d = st.as_dict()
+        if bubbles is not None:
+            d["bubble_per_iteration_ms"] = bubbles[:d["bubble_iterations"]].tolist()
+        return d
     if out_dir is None and not return_log:
         _lib.check(h.asv_engine_run(text.encode(), policy.encode() if policy else None, C.byref(o), C.byref(st)))
-        return st.as_dict()
+        return stats()
     buf, n = C.c_void_p(), C.c_int64(0)
     _lib.check(h.asv_engine_run_ex(text.encode(), policy.encode() if policy else None, C.byref(o), C.byref(st),
                                    out_dir.encode() if out_dir else None,
                                    C.byref(buf) if return_log else None, C.byref(n) if return_log else None))
     if not return_log:
-        return st.as_dict()
+        return stats()
     try:
-        return st.as_dict(), C.string_at(buf.value, n.value).decode()
+        return stats(), C.string_at(buf.value, n.value).decode()
     finally:
         h.asv_free(buf)
+
+
+def read_capture(path: str):
+    """Records of a content-mode capture file (include/asv.h asv_engine_opts.capture_path):
+    dicts {seq, ids, lens, head, out} with out float32 [L][b][n_q][128] (head == -1) or [L][b][128]
+    (query head `head`)."""
+    recs = []
+    with open(path, "rb") as f:
+        data = f.read()
+    off = 0
+    while off < len(data):
+        seq = int(np.frombuffer(data, np.int64, 1, off)[0])
+        b, L, n_q, head = (int(x) for x in np.frombuffer(data, np.int32, 4, off + 8))
+        off += 24
+        ids = np.frombuffer(data, np.int64, b, off).copy()
+        off += 8 * b
+        lens = np.frombuffer(data, np.int32, b, off).copy()
+        off += 4 * b
+        n = L * b * (n_q if head < 0 else 1) * 128
+        raw = np.frombuffer(data, np.uint16, n, off)
+        off += 2 * n
+        out = (raw.astype(np.uint32) << 16).view(np.float32)
+        out = out.reshape((L, b, n_q, 128) if head < 0 else (L, b, 128))
+        recs.append({"seq": seq, "ids": ids, "lens": lens, "head": head, "out": out})
+    return recs

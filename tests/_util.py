@@ -134,6 +134,30 @@ class Oracle:
                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_float, C.c_void_p,
                       C.c_void_p, C.c_int, C.c_int]
 
+    def content_attention(self, n_q, n_kv, num_layers, ids, lens, sm_scale, threads=None, only_kvh=-1):
+        """Expected outputs of a content-mode engine iteration (rows (ids[r], lens[r])), fp32
+        [L][b][n_q][128]; with only_kvh >= 0 just that kv head's query heads are filled."""
+        f = self.h.asv_oracle_content_attention
+        f.restype = C.c_int
+        f.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_float, C.c_void_p,
+                      C.c_int, C.c_int]
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        lens = np.ascontiguousarray(lens, dtype=np.int32)
+        out = np.zeros((num_layers, len(ids), n_q, 128), np.float32)
+        rc = f(n_q, n_kv, num_layers, ids.ctypes.data, lens.ctypes.data, len(ids), float(sm_scale), out.ctypes.data,
+               threads or os.cpu_count() or 1, int(only_kvh))
+        assert rc == 0
+        return out
+
+    def content_row(self, req, pos, layer, kind, head):
+        """bf16 bits of one content row (kind 0 K, 1 V, 2 Q)"""
+        f = self.h.asv_oracle_content_row
+        f.restype = None
+        f.argtypes = [C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_void_p]
+        out = np.zeros(128, np.uint16)
+        f(req, pos, layer, kind, head, out.ctypes.data)
+        return out
+
     def attention(self, n_q, n_kv, num_layers, layer, q_bits, pool, seq_lens, indptr, indices,
                   sm_scale, threads=None, f16=False):
         """q_bits / pool hold bf16 bits (fp16 bits with f16=True)."""

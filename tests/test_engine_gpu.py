@@ -107,3 +107,34 @@ def test_gqa_13b_config_executes():
     assert st["iterations_timed"] == 20 and st["tokens_timed"] > 0 and st["window_ms"] > 0
     assert st["h2d_bytes"] > 0 and st["h2d_bytes"] % (40 * 2 * 8 * 256) == 0  # whole tokens of 160 KiB
     assert st["attn_bytes"] > 0 and st["attn_ms"] > 0
+
+
+def test_serial_mode_same_bytes_and_log(monkeypatch):
+    """ASV_SERIAL=1 (also chosen automatically under ncu / nsys / compute-sanitizer): every copy and
+    iteration is issued inline and flags are host-side, so a profiler that serialises kernels never
+    parks a stream on a flag; decisions and bytes moved are unchanged."""
+    from paper_2605_23389_b200 import engine
+    cfg = GOLDEN["configs"]["smoke"]
+    kw = dict(device=0, num_q_heads=32, num_kv_heads=32, num_layers=32, execute_transfers=True, exec_begin=0,
+              exec_end=-1, timed_begin=0, copy_begin=0, host_pool_bytes=1 << 30, pair_mode=True,
+              return_log=True)
+    a, log_a = engine.engine_run(cfg, **kw)
+    monkeypatch.setenv("ASV_SERIAL", "1")
+    b, log_b = engine.engine_run(cfg, **kw)
+    assert log_a == log_b
+    for k in ("h2d_bytes", "d2h_bytes", "p2p_bytes", "offload_bytes", "iterations_timed", "tokens_timed"):
+        assert a[k] == b[k], k
+
+
+def test_bubble_probe_every_layer_every_iteration():
+    """probe_bubble: per-warp %globaltimer of every attention launch, reduced per launch on the GPU;
+    one measured bubble per timed iteration (summed over its 32 launches)."""
+    from paper_2605_23389_b200 import engine
+    cfg = engine.load_config(os.path.join(ROOT, "configs", "c1_7b_b16.json"))
+    st = engine.engine_run(cfg, device=0, num_q_heads=32, num_kv_heads=32, num_layers=32, execute_transfers=False,
+                           exec_begin=100, timed_begin=103, exec_end=143, probe_bubble=True)
+    per = st["bubble_per_iteration_ms"]
+    assert st["bubble_iterations"] == len(per) == st["iterations_timed"] == 40
+    assert all(x >= 0 for x in per) and 0 <= st["measured_idle_frac"] < 0.5
+    assert st["bubble_p50_ms"] <= st["bubble_p90_ms"] <= st["bubble_p99_ms"] <= st["bubble_max_ms"]
+    assert abs(sum(per) - st["measured_bubble_ms"]) < 1e-6 * max(1.0, sum(per))

@@ -108,3 +108,47 @@ def test_known_answer_dominant_key(oracle):
     out, _ = oracle.attention(1, 1, L, 0, U.f32_to_bf16_bits(q), pool, [16], [0, 1], [0], 1.0)
     v5 = U.bf16_bits_to_f32(U.f32_to_bf16_bits(vb[5]))
     assert np.abs(out[0, 0] - v5).max() < 1e-6
+
+
+# ---------------------------------------------------------------- content-check restatement
+def _np_content_row(req, pos, layer, kind, head):
+    """numpy restatement of the content function documented in include/asv.h / attn_oracle.c."""
+    G = np.uint64(0x9E3779B97F4A7C15)
+    with np.errstate(over="ignore"):
+        def mix(z):
+            z = np.uint64(z)
+            z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+            z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+            return z ^ (z >> np.uint64(31))
+        key = ((((((req << 21) | pos) << 6 | layer) << 2 | kind) << 8) | head)
+        seed = mix(np.uint64(key) + G)
+        words = [mix(seed + np.uint64(w + 1) * G) for w in range(16)]
+    b = np.array(words, dtype=np.uint64).view(np.int8).astype(np.float32)  # little endian: byte j = >> 8j
+    return b * (1 / 8 if kind == 2 else 1 / 128)
+
+
+def test_content_rows_follow_the_documented_function():
+    o = U.Oracle()
+    for req, pos, layer, kind, head in [(0, 0, 0, 0, 0), (5, 1234, 3, 1, 17), (1 << 20, 77, 1, 2, 31)]:
+        got = U.bf16_bits_to_f32(o.content_row(req, pos, layer, kind, head))
+        assert np.array_equal(got, _np_content_row(req, pos, layer, kind, head))
+
+
+@pytest.mark.parametrize("n_q,n_kv", [(4, 4), (8, 2)])
+def test_content_attention_matches_numpy_restatement(n_q, n_kv):
+    o = U.Oracle()
+    ids, lens, L = [3, 11], [1, 37], 2
+    got = o.content_attention(n_q, n_kv, L, ids, lens, 0.08838834764831845)
+    g = n_q // n_kv
+    for l in range(L):
+        for r, (i, s) in enumerate(zip(ids, lens)):
+            for h in range(n_q):
+                q = _np_content_row(i, s, l, 2, h).astype(np.float64)
+                K = np.stack([_np_content_row(i, t, l, 0, h // g) for t in range(s)]).astype(np.float64)
+                V = np.stack([_np_content_row(i, t, l, 1, h // g) for t in range(s)]).astype(np.float64)
+                sc = K @ q * 0.08838834764831845
+                p = np.exp(sc - sc.max())
+                np.testing.assert_allclose(got[l, r, h], p @ V / p.sum(), rtol=1e-5, atol=1e-6)
+    only = o.content_attention(n_q, n_kv, L, ids, lens, 0.08838834764831845, only_kvh=1)
+    np.testing.assert_array_equal(only[:, :, g:2 * g], got[:, :, g:2 * g])
+    assert not only[:, :, :g].any()
