@@ -66,7 +66,14 @@ def main():
     ap.add_argument("--full")
     ap.add_argument("--tag", default="r01")
     ap.add_argument("--alg-bytes-per-launch", type=float, default=None)
+    ap.add_argument("--alg-json", default=None, help="gpurun_out/ncu_launch_alg.json of tools/ncu_bench_launch.py")
     a = ap.parse_args()
+    alg_src = None
+    if a.alg_json:
+        rec = json.load(open(a.alg_json))
+        a.alg_bytes_per_launch = rec["alg_bytes_per_launch"]
+        alg_src = (f"ncu --set full of one decode_attn launch of tools/ncu_bench_launch.py (C2 iteration "
+                   f"{rec['iteration']}, batch {rec['batch']}, {rec['tokens']} tokens; tag {a.tag})")
     prof = os.path.join(ROOT, "profiles")
     os.makedirs(prof, exist_ok=True)
     summary_path = os.path.join(prof, "ncu_summary.json")
@@ -86,6 +93,7 @@ def main():
         summary["bench_kernel"] = {"tag": a.tag, "kernel": main_k[0]["kernel"] if main_k else None,
                                    "captures": fl, "dram_bytes_per_launch": per,
                                    "alg_bytes_per_launch": a.alg_bytes_per_launch,
+                                   "source": alg_src,
                                    "note": "ncu --set full --clock-control none; one capture per launch"}
         with open(os.path.join(prof, f"ncu_{a.tag}_full.txt"), "w") as f:
             for k in fl:
