@@ -401,6 +401,10 @@ def main():
     # the attention-only step over the same window: the dominant kernel's roofline
     att = res if not full_headline else E.engine_run(dp_cfg, execute_transfers=False, **base_kw)
     d.barrier()
+    # the same attention-only window with the per-warp %globaltimer probe on every launch:
+    # a separate run, so the probe's stores never touch the roofline numbers above
+    probe = E.engine_run(dp_cfg, execute_transfers=False, probe_bubble=True, **base_kw)
+    d.barrier()
 
     e2e = e2e_res = e2e_att = e2e_pair1 = e2e_colo = None
     ek = max(K, E2E_MIN_STEPS)
@@ -571,10 +575,15 @@ def main():
             "links": links, "pairs": pairs,
             "virtual_clock_tok_s": res["virtual_decode_tok_s"],
             "bubble_ms_per_step_virtual": res["bubble_ms_timed"] / max(1, res["iterations_timed"]),
-            "bubble_measured": {"idle_frac": att["measured_idle_frac"],
-                                "ms_per_step": att["measured_bubble_ms"] / max(1, att["iterations_timed"]),
-                                "probe": "per-warp %globaltimer start/end of every attention launch of every "
-                                         "timed step (attention-only run)"},
+            "bubble_measured": {"idle_frac": probe["measured_idle_frac"],
+                                "ms_per_step": probe["measured_bubble_ms"] / max(1, probe["iterations_timed"]),
+                                "per_iteration_ms": {"p50": probe["bubble_p50_ms"], "p90": probe["bubble_p90_ms"],
+                                                     "p99": probe["bubble_p99_ms"], "max": probe["bubble_max_ms"],
+                                                     "iterations": probe["bubble_iterations"]},
+                                "probe": "per-warp %globaltimer start/end of every attention launch (all 32 layers) "
+                                         "of every timed step; bubble of a launch = sum over warps of (launch span - "
+                                         "warp busy) / warps; per iteration = sum over its launches (attention-only "
+                                         "run with the probe, separate from the roofline run)"},
             "host_decide_ms": res["host_decide_ms"],
             "logical_bytes_moved": res["logical_bytes"],
         }

@@ -47,7 +47,7 @@ std::vector<prefixsim::Request> load_workload(const prefixsim::ExperimentConfig&
 }
 
 // Data-parallel shard of a trace: request i goes to shard i % count (arrival
-// times and order preserved; Simulation::run re-numbers ids to local indices,
+// times and order preserved; PairOrchestrator::run re-numbers ids to local indices,
 // cluster_sim.hpp:137-139, so global id = local * count + index).
 void shard_requests(std::vector<prefixsim::Request>& reqs, int32_t index, int32_t count) {
     if (count < 1 || index < 0 || index >= count) throw std::invalid_argument("bad shard index/count");

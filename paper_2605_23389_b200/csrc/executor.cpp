@@ -1,8 +1,9 @@
 // GPU executor of the decode-iteration hot path (host C++ runtime).
 //
-// Subscribes to the reference-API engine (prefixsim::Simulation, virtual
-// clock => decisions bit-exact with the reference) and performs every decision
-// as real work on the B200:
+// The data plane of one (prefetch, decode) pair: prefixsim::PairOrchestrator
+// (include/prefixsim/cluster_sim.hpp; virtual clock => decisions bit-exact with
+// the reference) issues typed orders (KvMove, released, prompt_in_place,
+// decode_step) and this executor performs each as real work on the B200:
 //   * KV pages live in a device page pool (layout: include/asv.h); a request's
 //     KV is a list of pages, allocated at prefetch / growth, freed at release;
 //   * batch_prefetch / stray_prefetch (reference cluster_sim.hpp:362-366,
@@ -72,17 +73,6 @@ struct CudaError : std::runtime_error {
     } while (0)
 
 namespace {
-
-int xfer_kind(const std::string& k) {
-    if (k == "prefill_offload") return ASV_XFER_PREFILL_OFFLOAD;
-    if (k == "batch_prefetch") return ASV_XFER_BATCH_PREFETCH;
-    if (k == "stray_prefetch") return ASV_XFER_STRAY_PREFETCH;
-    if (k == "admit") return ASV_XFER_ADMIT;
-    if (k == "evict") return ASV_XFER_EVICT;
-    if (k == "spill") return ASV_XFER_SPILL;
-    if (k == "flush") return ASV_XFER_FLUSH;
-    return -1;
-}
 
 // Fixed pool of physical KV pages on one device.
 // Free pages are handed out oldest-released first, each with its hazard: the
@@ -270,7 +260,7 @@ class ContentStore {
     std::vector<std::vector<char*>> pages_;
 };
 
-class GpuExecutor : public prefixsim::EngineObserver {
+class GpuExecutor : public prefixsim::DataPlane {
  public:
     GpuExecutor(const asv_engine_opts& o, const prefixsim::SimConfig& sim, const prefixsim::ModelSpec& spec,
                 std::size_t num_requests)
@@ -505,103 +495,92 @@ class GpuExecutor : public prefixsim::EngineObserver {
         cudaStreamDestroy(prefill_);
     }
 
-    // ---------------------------------------------------------- observer
-    void on_action(const prefixsim::ActionRecord& a) override {
+    // ------------------------------------------------------- data plane (orders of the orchestrator)
+    void released(prefixsim::RequestId id) override {
         const auto t0 = clock_now();
-        const std::string& act = a.action;
-        if (act == "batch") {
-            pending_batch_.push_back(a.request_id);
-        } else if (act == "release") {
-            ReqKV& r = kv(a.request_id);
-            release_pages(r);
-        } else if (act == "admit" && a.from == "wait_queue" && !admit_moved_) {
-            // merged-instance FCFS: the prompt is processed in place on the decode GPU
-            ReqKV& r = kv(a.request_id);
-            if (r.pages.empty() && content_) {
-                // content mode: the prompt's KV (computed in place by the merged instance) is written into
-                // its pages from the content store, so later iterations attend over real rows
-                begin_xfer_group(kUrgent);
-                fetch_from_host(a.request_id, &dec_, /*prefill_in_place=*/true);
-                end_xfer_group();
-            } else if (r.pages.empty()) {
-                r.prefix = a.blocks * 16;  // only the page count matters for the prompt's KV
-                for (int64_t i = 0; i < a.blocks; ++i) r.pages.push_back(dec_.alloc());
-                r.where = ReqKV::kDecode;
-            }
-        }
-        admit_moved_ = false;
+        release_pages(kv(id));
         host_ms_ += ms_since(t0);
     }
 
-    void on_transfer(const prefixsim::TransferRecord& t) override {
+    // merged-instance FCFS: the prompt is processed in place on the decode GPU
+    void prompt_in_place(prefixsim::RequestId id, int64_t blocks) override {
+        const auto t0 = clock_now();
+        ReqKV& r = kv(id);
+        if (r.pages.empty() && content_) {
+            // content mode: the prompt's KV (computed in place by the merged instance) is written into
+            // its pages from the content store, so later iterations attend over real rows
+            begin_xfer_group(kUrgent);
+            fetch_from_host(id, &dec_, /*prefill_in_place=*/true);
+            end_xfer_group();
+        } else if (r.pages.empty()) {
+            r.prefix = blocks * 16;  // only the page count matters for the prompt's KV
+            for (int64_t i = 0; i < blocks; ++i) r.pages.push_back(dec_.alloc());
+            r.where = ReqKV::kDecode;
+        }
+        host_ms_ += ms_since(t0);
+    }
+
+    void kv_move(const prefixsim::KvMove& m) override {
         const auto t0 = clock_now();
         phase_.store(1);
-        const int k = xfer_kind(t.kind);
-        if (k >= 0) {
-            stats_.logical_bytes[k] += t.bytes;
-            stats_.logical_count[k] += 1;
-        }
+        const int k = static_cast<int>(m.route);  // KvRoute order == ASV_XFER_* order
+        stats_.logical_bytes[k] += m.bytes;
+        stats_.logical_count[k] += 1;
         if (!copies_active()) {
             // outside the executed span: keep the page bookkeeping, move nothing
-            bookkeep_transfer(k, t);
-            pending_batch_.clear();
+            bookkeep_move(m);
             host_ms_ += ms_since(t0);
             return;
         }
-        switch (k) {
-            case ASV_XFER_BATCH_PREFETCH: {
+        switch (m.route) {
+            case prefixsim::KvRoute::kBatchPrefetch:
                 begin_xfer_group();
-                for (const auto id : pending_batch_) fetch_from_host(id, staging_pool());
-                pending_batch_.clear();
+                for (const auto id : *m.members) fetch_from_host(id, staging_pool());
                 end_xfer_group();
                 break;
-            }
-            case ASV_XFER_STRAY_PREFETCH:
+            case prefixsim::KvRoute::kStrayPrefetch:
                 begin_xfer_group(kUrgent);
-                fetch_from_host(t.request_id, staging_pool());
+                fetch_from_host(m.request, staging_pool());
                 end_xfer_group();
                 break;
-            case ASV_XFER_ADMIT:
+            case prefixsim::KvRoute::kAdmit:
                 if (!aligned_) {
                     // FCFS swap-in / disaggregated admit: host pool -> decode pages (PCIe)
                     begin_xfer_group(kUrgent);
-                    fetch_from_host(t.request_id, &dec_);
+                    fetch_from_host(m.request, &dec_);
                     end_xfer_group();
                 } else {
-                    admit_to_decode(t.request_id);  // candidate buffer -> running (NVLink / in place)
+                    admit_to_decode(m.request);  // candidate buffer -> running (NVLink / in place)
                 }
-                admit_moved_ = true;
                 break;
-            case ASV_XFER_EVICT:
+            case prefixsim::KvRoute::kEvict:
                 if (!aligned_) {
                     begin_xfer_group(kD2H);
-                    write_back_to_host(t.request_id);
+                    write_back_to_host(m.request);
                     end_xfer_group();
                 } else {
-                    evict_to_prefetch(t.request_id);
+                    evict_to_prefetch(m.request);
                 }
                 break;
-            case ASV_XFER_SPILL:
-            case ASV_XFER_FLUSH:
+            case prefixsim::KvRoute::kSpill:
+            case prefixsim::KvRoute::kFlush:
                 begin_xfer_group(kD2H);
-                write_back_to_host(t.request_id);
+                write_back_to_host(m.request);
                 end_xfer_group();
                 break;
-            case ASV_XFER_PREFILL_OFFLOAD:
+            case prefixsim::KvRoute::kPrefillOffload:
                 if (o_.execute_prefill_offload) {
                     begin_xfer_group(kPrefill);
-                    offload_to_host(t.request_id, t.bytes);
+                    offload_to_host(m.request, m.bytes);
                     end_xfer_group();
                 }
-                break;
-            default:
                 break;
         }
         host_ms_ += ms_since(t0);
         host_copy_ms_ += ms_since(t0);
     }
 
-    void on_iteration(const prefixsim::IterationRecord& rec, const std::vector<prefixsim::RunningMember>& running) override {
+    void decode_step(const prefixsim::IterationRecord& rec, const std::vector<prefixsim::RunningMember>& running) override {
         const auto t0 = clock_now();
         phase_.store(2);
         ++iterations_total_;
@@ -915,24 +894,23 @@ class GpuExecutor : public prefixsim::EngineObserver {
         return o_.execute_transfers && cur_seq_ >= begin && (o_.exec_end < 0 || cur_seq_ < o_.exec_end);
     }
 
-    // page ownership changes of a transfer whose bytes are not moved
-    void bookkeep_transfer(int k, const prefixsim::TransferRecord& t) {
-        switch (k) {
-            case ASV_XFER_BATCH_PREFETCH:
-                for (const auto id : pending_batch_) fetch_from_host(id, staging_pool());
+    // page ownership changes of a move whose bytes are not moved
+    void bookkeep_move(const prefixsim::KvMove& m) {
+        switch (m.route) {
+            case prefixsim::KvRoute::kBatchPrefetch:
+                for (const auto id : *m.members) fetch_from_host(id, staging_pool());
                 break;
-            case ASV_XFER_STRAY_PREFETCH: fetch_from_host(t.request_id, staging_pool()); break;
-            case ASV_XFER_ADMIT:
-                if (!aligned_) fetch_from_host(t.request_id, &dec_);
-                else admit_to_decode(t.request_id);
-                admit_moved_ = true;
+            case prefixsim::KvRoute::kStrayPrefetch: fetch_from_host(m.request, staging_pool()); break;
+            case prefixsim::KvRoute::kAdmit:
+                if (!aligned_) fetch_from_host(m.request, &dec_);
+                else admit_to_decode(m.request);
                 break;
-            case ASV_XFER_EVICT:
-                if (!aligned_) write_back_to_host(t.request_id);
-                else evict_to_prefetch(t.request_id);
+            case prefixsim::KvRoute::kEvict:
+                if (!aligned_) write_back_to_host(m.request);
+                else evict_to_prefetch(m.request);
                 break;
-            case ASV_XFER_SPILL:
-            case ASV_XFER_FLUSH: write_back_to_host(t.request_id); break;
+            case prefixsim::KvRoute::kSpill:
+            case prefixsim::KvRoute::kFlush: write_back_to_host(m.request); break;
             default: break;
         }
     }
@@ -1484,7 +1462,7 @@ class GpuExecutor : public prefixsim::EngineObserver {
         if (launcher_.failed()) throw CudaError("launch worker: " + launcher_.error());
     }
 
-    // global request id of a shard-local one (request i of the trace -> shard i % count, Simulation
+    // global request id of a shard-local one (request i of the trace -> shard i % count, the orchestrator
     // renumbers its requests 0..n-1: cluster_sim.hpp:137-139)
     int64_t global_id(prefixsim::RequestId local) const {
         return static_cast<int64_t>(local) * std::max(1, o_.shard_count) + o_.shard_index;
@@ -1675,9 +1653,8 @@ class GpuExecutor : public prefixsim::EngineObserver {
     std::vector<cudaEvent_t> att_beg_, att_end_;
     std::vector<int> slot_timed_;
     cudaEvent_t win_beg_ = nullptr, win_end_ = nullptr;
-    bool window_open_ = false, last_timed_end_ = false, group_timed_ = false, admit_moved_ = false;
+    bool window_open_ = false, last_timed_end_ = false, group_timed_ = false;
     std::vector<ReqKV> reqs_;
-    std::vector<prefixsim::RequestId> pending_batch_;
     std::vector<std::pair<PagePool*, std::vector<int32_t>>> group_quarantine_;
     std::vector<CopyTimer> copy_timers_;  // events created by the engine thread, recorded by the worker
     std::vector<int32_t> seq_, indptr_, indices_;
@@ -1713,11 +1690,11 @@ int engine_run(const char* config_json, const char* policy_override, const asv_e
         std::vector<prefixsim::Request> reqs = load_workload(cfg);
         shard_requests(reqs, opts->shard_index, std::max(1, opts->shard_count));
         if (reqs.empty()) return fail(ASV_ERR_INVALID, "empty shard");
-        prefixsim::Simulation sim(cfg.sim, model, reqs);
+        prefixsim::PairOrchestrator sim(cfg.sim, model, reqs);
         GpuExecutor ex(*opts, cfg.sim, model.spec, reqs.size());
         ex.requests_ = &sim.requests();
         ex.aligned_ = cfg.sim.policy == prefixsim::Policy::kAligned;
-        sim.set_observer(&ex);
+        sim.attach(&ex);
         const auto t0 = std::chrono::steady_clock::now();
         prefixsim::MetricsLog log = sim.run();
         (void)t0;

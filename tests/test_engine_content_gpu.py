@@ -67,14 +67,14 @@ def reference_log(cfg, policy):
     return engine.run_config_jsonl(cfg, policy)  # pinned to the reference by test_engine_parity.py
 
 
-def run_content(cfg, policy, tmp_path, pair_mode=False):
+def run_content(cfg, policy, tmp_path, pair_mode=False, **kw):
     from paper_2605_23389_b200 import engine
     L = cfg["b200"]["num_layers"]
     cap = str(tmp_path / f"cap_{policy}_{int(pair_mode)}.bin")
     st, log = engine.engine_run(cfg, device=0, num_q_heads=32, num_kv_heads=32, num_layers=L,
                                 execute_transfers=True, exec_begin=0, exec_end=-1, timed_begin=0, copy_begin=0,
                                 host_pool_bytes=6 << 30, run_ahead=8, policy=policy, pair_mode=pair_mode,
-                                content_check=True, capture_path=cap, capture_every=8, return_log=True)
+                                content_check=True, capture_path=cap, capture_every=8, return_log=True, **kw)
     ref = reference_log(cfg, policy)
     assert log == ref, "decision log differs from the reference"
     iters = [json.loads(l) for l in ref.splitlines()[1:]]
@@ -145,3 +145,19 @@ def test_fcfs_swaps_c1_slice(tmp_path, policy):
 def test_reference_smoke_config_two_layers(tmp_path, policy, pair):
     st, iters, worst = run_content(smoke_l2(), policy, tmp_path, pair_mode=pair)
     assert st["iterations_total"] == len(iters) > 0
+
+
+def _device_count():
+    import torch
+    return torch.cuda.device_count()
+
+
+@pytest.mark.skipif(_device_count() < 2, reason="needs two GPUs (a real prefetch / decode pair)")
+def test_aligned_two_device_pair_c1_slice(tmp_path):
+    """The pair on two GPUs: candidate buffers, host prefetches and prefill offloads on GPU 1, decode on
+    GPU 0; admits / evicts are SM page moves through NVLink peer pointers (north-star (3))."""
+    cfg = c1_slice(tmp_path)
+    st, iters, worst = run_content(cfg, "aligned", tmp_path, prefetch_device=1)
+    assert st["p2p_bytes"] == _bytes(st, "admit", "evict") > 0
+    assert st["h2d_bytes"] == _bytes(st, "batch_prefetch", "stray_prefetch")
+    assert st["d2h_bytes"] == _bytes(st, "spill", "flush") > 0
