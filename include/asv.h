@@ -252,6 +252,20 @@ typedef struct asv_linear_args {
  * thread-block cluster and reduce through distributed shared memory, so no
  * workspace is needed.  Stream-ordered; no host synchronisation. */
 int asv_linear(const asv_linear_args* args, void* stream);
+
+/* Persistent stream-K CHAIN of up to 4 dependent linear layers in ONE launch (decode_chain.cu):
+ * phase i+1 may read what phase i writes (x, residual stream, fused-RMSNorm sums) — e.g. per
+ * decoder layer O-proj+residual -> gate/up+SiLU -> down+residual -> next layer's QKV+RoPE.  Every
+ * phase's (tile, 64-K block) units are split evenly over a persistent grid of 2 CTAs per SM; tiles
+ * cut between CTAs are reduced (fixed CTA order: deterministic) by the CTA holding their first K
+ * block; the weight stream runs ahead across phase boundaries.  Same per-phase semantics and
+ * weight layouts as asv_linear (all phases share `batch`; `pdl` is taken from phases[0]).
+ * The workspace holds the cross-CTA counters and partials of one device; launches that share a
+ * workspace must be stream-ordered (one compute stream). */
+typedef struct asv_linear_chain_ws asv_linear_chain_ws;
+int asv_linear_chain_ws_create(int32_t device, asv_linear_chain_ws** out);
+void asv_linear_chain_ws_destroy(asv_linear_chain_ws* ws);
+int asv_linear_chain(const asv_linear_args* phases, int32_t n, asv_linear_chain_ws* ws, void* stream);
 /* out[b][:] = h[b][:] * rsqrt(mean(h[b]^2) + eps) * gamma; rows [batch, rows_out) of out zeroed */
 int asv_rmsnorm(const void* h, const void* gamma, void* out, int32_t dim, int32_t batch, int32_t rows_out,
                 float eps, int32_t pdl, void* stream);

@@ -88,6 +88,7 @@ cudaError_t kv_move_preload();
 
 // decode-step linear layers (decode_gemm.cu)
 cudaError_t linear_preload();
+cudaError_t linear_chain_preload();
 cudaError_t rmsnorm_launch(const void* h, const void* gamma, void* out, int dim, int batch, int rows_out, float eps,
                            bool pdl, cudaStream_t st);
 cudaError_t rmsnorm_preload();

@@ -478,6 +478,7 @@ class GpuExecutor : public prefixsim::DataPlane {
         if (weights_) cudaFree(weights_);
         if (h_) cudaFree(h_);
         if (x_) cudaFree(x_);
+        if (chain_ws_) asv_linear_chain_ws_destroy(chain_ws_);
         if (act_) cudaFree(act_);
         if (ss_a_) cudaFree(ss_a_);
         if (ss_b_) cudaFree(ss_b_);
@@ -694,7 +695,8 @@ class GpuExecutor : public prefixsim::DataPlane {
             const int32_t* positions = plan_arena_dev_ + pw + ((pl.total_int32 + 3) & ~3);
             const int32_t* payload = plan_arena_dev_ + pw + plan_words + ((pos_words + 3) & ~int64_t(3));
             for (int l = 0; l < o_.num_layers; ++l) {
-                if (o_.full_step) layer_front(l, b, positions);  // RMSNorm, QKV + RoPE -> q_, k_new_, v_new_
+                // RMSNorm, QKV + RoPE -> q_, k_new_, v_new_ (in chain mode layer l > 0's QKV ran in the previous chain)
+                if (o_.full_step && (!chain_ || l == 0)) layer_front(l, b, positions);
                 if (content_) {  // this layer's queries / appended rows from the upload, its own output slice
                     const int32_t* lp = payload + static_cast<int64_t>(l) * (q_words + 2 * kv_words);
                     args.q = lp;
@@ -708,7 +710,10 @@ class GpuExecutor : public prefixsim::DataPlane {
                 // layer 0 of attention-only steps reads the plan the upload kernel just wrote
                 args.pdl = (l == 0 && !o_.full_step) ? 0 : o_.pdl;
                 if (asv_decode_attention(&shape_, &args, compute_) != ASV_OK) throw CudaError(asv_last_error());
-                if (o_.full_step) layer_back(l, b);  // O + residual, RMSNorm, gate/up SiLU, down + residual
+                if (o_.full_step) {  // O + residual, RMSNorm, gate/up SiLU, down + residual (+ next layer's QKV)
+                    if (chain_) layer_back_chain(l, b, positions);
+                    else layer_back(l, b);
+                }
             }
             ASV_CUDA(cudaEventRecord(att_end_[slot], compute_));
             if (probe) {  // per launch: first warp start, last warp end, summed warp busy time
@@ -742,7 +747,9 @@ class GpuExecutor : public prefixsim::DataPlane {
                 const int64_t chunks = (static_cast<int64_t>(running.size()) + 255) / 256;
                 // RMSNorm launches: 2 per layer unfused; fused, only layer 0's first one remains
                 const int64_t norms = fuse_norm_ ? 1 : 2 * o_.num_layers;
-                stats_.kernel_launches_timed += norms + o_.num_layers * 4 * chunks;
+                // chain mode: layer 0's QKV + one persistent GEMM-chain launch per layer and chunk
+                stats_.kernel_launches_timed += norms + (chain_ ? chunks * (1 + o_.num_layers)
+                                                                : o_.num_layers * 4 * chunks);
                 stats_.weight_bytes += o_.num_layers * weights_bytes_per_layer_;
             }
             if (first_timed_start_ < 0) first_timed_start_ = rec.start_ms;
@@ -1369,8 +1376,14 @@ class GpuExecutor : public prefixsim::DataPlane {
         ss_ld_ = static_cast<int32_t>(rows_pad);
         ASV_CUDA(cudaMalloc(&ss_a_, static_cast<size_t>(ss_parts_) * rows_pad * 4));
         ASV_CUDA(cudaMalloc(&ss_b_, static_cast<size_t>(ss_parts_) * rows_pad * 4));
+        // persistent stream-K chain per layer (decode_chain.cu): needs the fused norms; ASV_LINEAR_CHAIN=0
+        // keeps one launch per GEMM (A/B experiments)
+        const char* ce = std::getenv("ASV_LINEAR_CHAIN");
+        chain_ = fuse_norm_ && (ce == nullptr || std::atoi(ce) != 0);
+        if (chain_ && asv_linear_chain_ws_create(o_.decode_device, &chain_ws_) != ASV_OK)
+            throw CudaError(asv_last_error());
         ASV_CUDA(cudaStreamSynchronize(compute_));
-        if (linear_preload() != cudaSuccess || rmsnorm_preload() != cudaSuccess)
+        if (linear_preload() != cudaSuccess || rmsnorm_preload() != cudaSuccess || linear_chain_preload() != cudaSuccess)
             throw CudaError("full_step: kernel preload failed");
     }
 
@@ -1454,6 +1467,44 @@ class GpuExecutor : public prefixsim::DataPlane {
                 a.ss_ld = ss_ld_;
             }
             if (asv_linear(&a, compute_) != ASV_OK) throw CudaError(asv_last_error());
+        });
+    }
+
+    // chain mode: O + residual -> gate/up SiLU -> down + residual -> layer l+1's QKV + RoPE in ONE
+    // persistent launch per 256-row chunk (decode_chain.cu); the norms are fused as in layer_back
+    void layer_back_chain(int l, int32_t b, const int32_t* positions) {
+        const LayerW& lw = layers_[static_cast<size_t>(l)];
+        auto* h = static_cast<__nv_bfloat16*>(h_);
+        auto* act = static_cast<__nv_bfloat16*>(act_);
+        row_chunks(b, [&](int32_t r0, int32_t n) {
+            asv_linear_args ph[4];
+            ph[0] = lin(lw.o, hidden_, hidden_, static_cast<const __nv_bfloat16*>(out_) + int64_t(r0) * hidden_, n,
+                        h + int64_t(r0) * hidden_, hidden_, ASV_EPI_RESIDUAL);
+            ph[0].ss_out = ss_b_ + r0;
+            ph[0].ss_ld = ss_ld_;
+            ph[1] = lin(lw.gate_up, 2 * inter_, hidden_, h + int64_t(r0) * hidden_, n, act + int64_t(r0) * inter_,
+                        inter_, ASV_EPI_SILU_MUL);
+            fuse_in(ph[1], ss_b_, r0);
+            ph[2] = lin(lw.down, hidden_, inter_, act + int64_t(r0) * inter_, n, h + int64_t(r0) * hidden_, hidden_,
+                        ASV_EPI_RESIDUAL);
+            ph[2].ss_out = ss_a_ + r0;
+            ph[2].ss_ld = ss_ld_;
+            int nph = 3;
+            if (l + 1 < o_.num_layers) {
+                const LayerW& nw = layers_[static_cast<size_t>(l + 1)];
+                ph[3] = lin(nw.qkv, 128 * (o_.num_q_heads + 2 * o_.num_kv_heads), hidden_, h + int64_t(r0) * hidden_, n,
+                            nullptr, 0, ASV_EPI_QKV_ROPE);
+                fuse_in(ph[3], ss_a_, r0);
+                ph[3].positions = positions + r0;
+                ph[3].rope_theta = 10000.f;
+                ph[3].q = static_cast<__nv_bfloat16*>(q_) + int64_t(r0) * o_.num_q_heads * 128;
+                ph[3].k_out = static_cast<__nv_bfloat16*>(k_new_) + int64_t(r0) * o_.num_kv_heads * 128;
+                ph[3].v_out = static_cast<__nv_bfloat16*>(v_new_) + int64_t(r0) * o_.num_kv_heads * 128;
+                ph[3].n_q_heads = o_.num_q_heads;
+                ph[3].n_kv_heads = o_.num_kv_heads;
+                nph = 4;
+            }
+            if (asv_linear_chain(ph, nph, chain_ws_, compute_) != ASV_OK) throw CudaError(asv_last_error());
         });
     }
 
@@ -1628,6 +1679,8 @@ class GpuExecutor : public prefixsim::DataPlane {
     float *ss_a_ = nullptr, *ss_b_ = nullptr;  // fused RMSNorm: per-tile row sums of squares of h
     int32_t ss_parts_ = 0, ss_ld_ = 0;
     bool fuse_norm_ = false;
+    bool chain_ = false;                          // full step: one persistent GEMM chain per layer
+    asv_linear_chain_ws* chain_ws_ = nullptr;
     int32_t hidden_ = 0, inter_ = 0;
     int64_t max_rows_full_ = 0, weights_bytes_per_layer_ = 0;
     void *q_ = nullptr, *out_ = nullptr, *k_new_ = nullptr, *v_new_ = nullptr, *ws_ = nullptr;

@@ -16,6 +16,53 @@ from . import _lib
 STORE, RESIDUAL, SILU_MUL, QKV_ROPE = _lib.EPI_STORE, _lib.EPI_RESIDUAL, _lib.EPI_SILU_MUL, _lib.EPI_QKV_ROPE
 
 
+def _args(x, w, batch, y=None, epilogue=STORE, positions=None, rope_theta=10000.0, q=None, k_out=None, v_out=None,
+          n_q_heads=0, n_kv_heads=0, pdl=False, ss_out=None, ss_in=None, ss_eps=1e-5) -> _lib.LinearArgs:
+    if x.dtype != torch.bfloat16 or w.dtype != torch.bfloat16:
+        raise TypeError("x and w must be bfloat16")
+    n_out, k = w.shape
+    a = _lib.LinearArgs()
+    a.w, a.n_out, a.k = w.data_ptr(), n_out, k
+    a.x, a.x_rows, a.batch = x.data_ptr(), x.shape[0], batch
+    a.y = y.data_ptr() if y is not None else None
+    a.y_ld = y.shape[-1] if y is not None else 0
+    a.epilogue = epilogue
+    a.positions = positions.data_ptr() if positions is not None else None
+    a.rope_theta = rope_theta
+    a.q = q.data_ptr() if q is not None else None
+    a.k_out = k_out.data_ptr() if k_out is not None else None
+    a.v_out = v_out.data_ptr() if v_out is not None else None
+    a.n_q_heads, a.n_kv_heads = n_q_heads, n_kv_heads
+    a.pdl = 1 if pdl else 0
+    if ss_out is not None:
+        a.ss_out, a.ss_ld = ss_out.data_ptr(), ss_out.shape[-1]
+    if ss_in is not None:
+        a.ss_in, a.ss_parts, a.ss_ld, a.ss_dim, a.ss_eps = ss_in.data_ptr(), ss_in.shape[0], ss_in.shape[-1], k, ss_eps
+    return a
+
+
+class ChainWorkspace:
+    """Cross-CTA counters and partials of asv_linear_chain on one device (include/asv.h)."""
+
+    def __init__(self, device: int = 0):
+        self.h = C.c_void_p()
+        _lib.check(_lib.lib().asv_linear_chain_ws_create(device, C.byref(self.h)))
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.h.value:
+            _lib.lib().asv_linear_chain_ws_destroy(self.h)
+            self.h = None
+
+
+def linear_chain(phases: list[dict], ws: ChainWorkspace, stream=None) -> None:
+    """One persistent launch of up to 4 dependent linear layers; each dict holds linear()'s keyword
+    arguments (x, w, batch, y, epilogue, ...)."""
+    arr = (_lib.LinearArgs * len(phases))(*[_args(**ph) for ph in phases])
+    dev = phases[0]["x"].device
+    st = (stream or torch.cuda.current_stream(dev)).cuda_stream
+    _lib.check(_lib.lib().asv_linear_chain(arr, len(phases), ws.h, C.c_void_p(st)))
+
+
 def linear(x: torch.Tensor, w: torch.Tensor, batch: int, y: torch.Tensor | None = None,
            epilogue: int = STORE, positions: torch.Tensor | None = None, rope_theta: float = 10000.0,
            q: torch.Tensor | None = None, k_out: torch.Tensor | None = None, v_out: torch.Tensor | None = None,

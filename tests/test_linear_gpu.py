@@ -204,3 +204,92 @@ def test_fused_rmsnorm_between_linears(batch):
     gu = (xn @ wgu.float().T).view(batch, -1, 2, 64)
     ref = torch.nn.functional.silu(gu[:, :, 0].reshape(batch, -1)) * gu[:, :, 1].reshape(batch, -1)
     _check(act, ref.bfloat16(), "fused rmsnorm -> silu")
+
+
+# ------------------------------------------------------------ persistent stream-K chain
+@pytest.mark.parametrize("n_out,k,batch", [(128, 64, 1), (256, 512, 5), (4096, 4096, 16), (1024, 11008, 33),
+                                           (12288, 4096, 64), (512, 4096, 256), (384, 1024, 100)])
+def test_chain_single_phase_matches_torch(n_out, k, batch):
+    """asv_linear_chain with one phase = a stream-K GEMM (tiles cut between CTAs, owner reduction)."""
+    from paper_2605_23389_b200 import linear as L
+    ws = L.ChainWorkspace(0)
+    x = _x(batch, k, 1)
+    w = _rand((n_out, k), 2, 1 / math.sqrt(k))
+    y = torch.full((batch, n_out), float("nan"), dtype=torch.bfloat16, device="cuda")
+    ref = x[:batch].float() @ w.float().T
+    for i in range(2):  # second call: counters and partial slots are reused
+        L.linear_chain([dict(x=x, w=w, batch=batch, y=y, epilogue=L.STORE)], ws)
+        torch.cuda.synchronize()
+        _check(y, ref, f"chain store {n_out}x{k} b{batch} call {i}")
+
+
+def _layer_weights(d, inter, n_q, n_kv, seed):
+    wo = _rand((d, d), seed, 1 / math.sqrt(d))
+    wgu = _rand((2 * inter, d), seed + 1, 1 / math.sqrt(d))
+    wd = _rand((d, inter), seed + 2, 1 / math.sqrt(inter))
+    wqkv = _rand((128 * (n_q + 2 * n_kv), d), seed + 3, 1 / math.sqrt(d))
+    return wo, wgu, wd, wqkv
+
+
+@pytest.mark.parametrize("batch", [4, 37, 130, 256])
+def test_chain_decoder_layer_matches_per_gemm_launches(batch):
+    """One chain launch = O+residual(ss_out) -> gate/up SiLU (fused norm) -> down+residual(ss_out) ->
+    next QKV+RoPE (fused norm), against the same four GEMMs launched one by one (asv_linear, itself
+    checked against torch above) and against torch fp32; repeated launches are bit-identical."""
+    from paper_2605_23389_b200 import linear as L
+    d, inter, n_q, n_kv = 4096, 11008, 32, 32
+    rows = (batch + 15) // 16 * 16
+    wo, wgu, wd, wqkv = _layer_weights(d, inter, n_q, n_kv, 40)
+    attn = _x(batch, d, 41)
+    h0 = torch.zeros(rows, d, dtype=torch.bfloat16, device="cuda")
+    h0[:batch] = _rand((batch, d), 42)
+    pos = torch.randint(0, 16000, (batch,), dtype=torch.int32, device="cuda")
+
+    def run(chain, ws=None):
+        h = h0.clone()
+        act = torch.zeros(rows, inter, dtype=torch.bfloat16, device="cuda")
+        ss_b = torch.zeros(2 * d // 128, rows, dtype=torch.float32, device="cuda")
+        ss_a = torch.zeros(2 * d // 128, rows, dtype=torch.float32, device="cuda")
+        q = torch.zeros(batch, n_q, 128, dtype=torch.bfloat16, device="cuda")
+        kk = torch.zeros(batch, n_kv, 128, dtype=torch.bfloat16, device="cuda")
+        v = torch.zeros(batch, n_kv, 128, dtype=torch.bfloat16, device="cuda")
+        phases = [dict(x=attn, w=wo, batch=batch, y=h, epilogue=L.RESIDUAL, ss_out=ss_b, pdl=True),
+                  dict(x=h, w=wgu, batch=batch, y=act, epilogue=L.SILU_MUL, ss_in=ss_b, pdl=True),
+                  dict(x=act, w=wd, batch=batch, y=h, epilogue=L.RESIDUAL, ss_out=ss_a, pdl=True),
+                  dict(x=h, w=wqkv, batch=batch, epilogue=L.QKV_ROPE, positions=pos, q=q, k_out=kk, v_out=v,
+                       n_q_heads=n_q, n_kv_heads=n_kv, ss_in=ss_a, pdl=True)]
+        if chain:
+            L.linear_chain(phases, ws)
+        else:
+            for ph in phases:
+                L.linear(**ph)
+        torch.cuda.synchronize()
+        return h, act, q, kk, v
+
+    ws = L.ChainWorkspace(0)
+    got = run(True, ws)
+    want = run(False)
+    for name, g, w in zip(("h", "act", "q", "k", "v"), got, want):
+        _check(g[:batch], w[:batch].float(), f"chain vs per-GEMM {name} b{batch}")
+    again = run(True, ws)
+    for g, a in zip(got, again):
+        assert torch.equal(g, a), "chain launches are not deterministic"
+    # torch fp32 of the residual path (norm weights folded into the weights, as the engine does)
+    hf = (h0[:batch].float() + attn[:batch].float() @ wo.float().T).bfloat16().float()
+    xg = hf * torch.rsqrt(hf.pow(2).mean(-1, keepdim=True) + 1e-5)
+    gu = xg @ wgu.float().T
+    gg = gu.view(batch, -1, 2, 64)[:, :, 0].reshape(batch, -1)
+    uu = gu.view(batch, -1, 2, 64)[:, :, 1].reshape(batch, -1)
+    a = (torch.nn.functional.silu(gg) * uu).bfloat16().float()
+    _check(got[1][:batch], a, f"chain act vs torch b{batch}")
+    _check(got[0][:batch], hf + a @ wd.float().T, f"chain h vs torch b{batch}")
+
+
+def test_chain_rejects_mixed_batches():
+    from paper_2605_23389_b200 import linear as L
+    ws = L.ChainWorkspace(0)
+    x = _x(4, 128, 1)
+    w = _rand((128, 128), 2)
+    y = torch.empty(8, 128, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ValueError, match="same batch"):
+        L.linear_chain([dict(x=x, w=w, batch=4, y=y), dict(x=x, w=w, batch=3, y=y)], ws)

@@ -1,0 +1,87 @@
+#!/usr/bin/env python
+"""Decode GEMM stack of a full Llama-2-7B step (32 layers x O, gate/up, down, next QKV; fused norms)
+on one B200: one launch per GEMM (asv_linear, PDL-chained) vs one persistent stream-K chain per
+layer (asv_linear_chain).  Weights are 32 distinct layers (12.95 GB >> L2), CUDA events on the
+launching stream around the whole stack; reports us per layer and weight-streaming GB/s vs the
+measured HBM peak.  Env: BATCHES (default 4,16,64,128,256), REPS (default 5)."""
+import json
+import math
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2605_23389_b200 import linear as L  # noqa: E402
+
+D, INTER, NQ, NKV, LAYERS = 4096, 11008, 32, 32, 32
+
+
+def main():
+    dev = torch.device("cuda", 0)
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6450.0) \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6450.0
+
+    def w(n, k, seed):
+        g = torch.Generator(device=dev).manual_seed(seed)
+        return ((torch.rand(n, k, device=dev, generator=g) * 2 - 1) / math.sqrt(k)).to(torch.bfloat16)
+
+    layers = [dict(o=w(D, D, 10 * l), gu=w(2 * INTER, D, 10 * l + 1), down=w(D, INTER, 10 * l + 2),
+                   qkv=w(128 * (NQ + 2 * NKV), D, 10 * l + 3)) for l in range(LAYERS)]
+    wbytes = sum(t.numel() * 2 for ly in layers for t in ly.values())
+    ws = L.ChainWorkspace(0)
+    reps = int(os.environ.get("REPS", "5"))
+    for batch in [int(b) for b in os.environ.get("BATCHES", "4,16,64,128,256").split(",")]:
+        rows = (batch + 15) // 16 * 16
+        attn = (torch.rand(rows, D, device=dev) * 2 - 1).to(torch.bfloat16)
+        h = (torch.rand(rows, D, device=dev) * 2 - 1).to(torch.bfloat16)
+        act = torch.zeros(rows, INTER, dtype=torch.bfloat16, device=dev)
+        ss_a = torch.zeros(2 * D // 128, rows, dtype=torch.float32, device=dev)
+        ss_b = torch.zeros(2 * D // 128, rows, dtype=torch.float32, device=dev)
+        pos = torch.arange(batch, dtype=torch.int32, device=dev) + 1000
+        q = torch.zeros(batch, NQ, 128, dtype=torch.bfloat16, device=dev)
+        kk = torch.zeros(batch, NKV, 128, dtype=torch.bfloat16, device=dev)
+        v = torch.zeros(batch, NKV, 128, dtype=torch.bfloat16, device=dev)
+
+        def phases(l):
+            ly, nx = layers[l], layers[(l + 1) % LAYERS]
+            return [dict(x=attn, w=ly["o"], batch=batch, y=h, epilogue=L.RESIDUAL, ss_out=ss_b, pdl=True),
+                    dict(x=h, w=ly["gu"], batch=batch, y=act, epilogue=L.SILU_MUL, ss_in=ss_b, pdl=True),
+                    dict(x=act, w=ly["down"], batch=batch, y=h, epilogue=L.RESIDUAL, ss_out=ss_a, pdl=True),
+                    dict(x=h, w=nx["qkv"], batch=batch, epilogue=L.QKV_ROPE, positions=pos, q=q, k_out=kk, v_out=v,
+                         n_q_heads=NQ, n_kv_heads=NKV, ss_in=ss_a, pdl=True)]
+
+        plans = [phases(l) for l in range(LAYERS)]
+
+        def stack(chain):
+            for ph in plans:
+                if chain:
+                    L.linear_chain(ph, ws)
+                else:
+                    for p in ph:
+                        L.linear(**p)
+
+        res = {"batch": batch}
+        for mode in ("per_gemm", "chain"):
+            stack(mode == "chain")
+            torch.cuda.synchronize()
+            best = None
+            for _ in range(reps):
+                h.uniform_(-1, 1)  # keep values bounded across repetitions
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                stack(mode == "chain")
+                b.record()
+                b.synchronize()
+                ms = a.elapsed_time(b)
+                best = ms if best is None else min(best, ms)
+            gbps = wbytes / (best * 1e-3) / 1e9
+            res[mode] = {"us_per_layer": round(best * 1e3 / LAYERS, 2), "GBps": round(gbps, 1),
+                         "frac_hbm": round(gbps / peak, 3)}
+        res["speedup"] = round(res["per_gemm"]["us_per_layer"] / res["chain"]["us_per_layer"], 3)
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()
