@@ -19,6 +19,8 @@
 //    otherwise park a stream on a flag whose writer it never schedules.
 #pragma once
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX: a named range per posted operation (Nsight timelines)
+
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -118,7 +120,9 @@ class CopyWorker {
     void post(std::function<void()> fn, const char* label = "op") {
         if (inline_) {
             cur_.store(label);
+            nvtxRangePushA(label);
             fn();  // exceptions propagate to the caller
+            nvtxRangePop();
             done_.fetch_add(1);
             return;
         }
@@ -171,9 +175,12 @@ class CopyWorker {
                 busy_ = true;
             }
             if (!failed_.load()) {
+                nvtxRangePushA(cur_.load());
                 try {
                     fn();
+                    nvtxRangePop();
                 } catch (const std::exception& e) {
+                    nvtxRangePop();
                     std::lock_guard<std::mutex> lk(m_);
                     err_ = e.what();
                     failed_.store(true);

@@ -674,8 +674,12 @@ class GpuExecutor : public prefixsim::DataPlane {
             ASV_CUDA(cudaSetDevice(o_.decode_device));
             if (open_window) ASV_CUDA(cudaEventRecord(win_beg_, compute_));
             for (const auto& [lane, v] : waits) flags_.wait(compute_, lane, v);
-            if (asv_plan_upload(plan_arena_host_ + pw, plan_arena_dev_ + pw, upload_words, compute_) != ASV_OK)
+            if (serial_) {  // profilers cannot replay kernels that touch mapped host memory: copy engine
+                ASV_CUDA(cudaMemcpyAsync(plan_arena_dev_ + pw, plan_arena_host_ + pw, static_cast<size_t>(upload_words) * 4,
+                                         cudaMemcpyHostToDevice, compute_));
+            } else if (asv_plan_upload(plan_arena_host_ + pw, plan_arena_dev_ + pw, upload_words, compute_) != ASV_OK) {
                 throw CudaError(asv_last_error());
+            }
             ASV_CUDA(cudaEventRecord(att_beg_[slot], compute_));
             asv_attn_plan pl = plan;
             asv_attn_args args{};
@@ -721,12 +725,11 @@ class GpuExecutor : public prefixsim::DataPlane {
                                           span_host_ + slot * static_cast<size_t>(o_.num_layers) * 3, compute_));
             }
             if (content_) {  // every layer's output of the iteration -> its capture slot
-                ASV_CUDA(sm_copy(static_cast<const int32_t*>(out_),
-                                 cap_host_ + slot * static_cast<size_t>(cap_words_),
-                                 b_rows * o_.num_q_heads * 64 * o_.num_layers, compute_));
+                read_back(static_cast<const int32_t*>(out_), cap_host_ + slot * static_cast<size_t>(cap_words_),
+                          b_rows * o_.num_q_heads * 64 * o_.num_layers);
             } else if (result_bytes > 0) {  // the step's result (last layer's output / hidden state) read back
-                ASV_CUDA(sm_copy(static_cast<const int32_t*>(o_.full_step ? h_ : out_),
-                                 reinterpret_cast<int32_t*>(result_host_), result_bytes / 4, compute_));
+                read_back(static_cast<const int32_t*>(o_.full_step ? h_ : out_),
+                          reinterpret_cast<int32_t*>(result_host_), result_bytes / 4);
             }
             flags_.write(compute_, kIter, static_cast<uint32_t>(e + 1));  // executed iterations complete
         }, "iteration");
@@ -1506,6 +1509,17 @@ class GpuExecutor : public prefixsim::DataPlane {
             }
             if (asv_linear_chain(ph, nph, chain_ws_, compute_) != ASV_OK) throw CudaError(asv_last_error());
         });
+    }
+
+    // device -> mapped pinned host on the compute stream: an SM copy (never queued behind multi-GB
+    // copy-engine traffic), or the copy engine in serial mode (profilers cannot replay a kernel that
+    // writes mapped host memory)
+    void read_back(const int32_t* src, int32_t* dst, int64_t words) {
+        if (serial_) {
+            ASV_CUDA(cudaMemcpyAsync(dst, src, static_cast<size_t>(words) * 4, cudaMemcpyDeviceToHost, compute_));
+        } else {
+            ASV_CUDA(sm_copy(src, dst, words, compute_));
+        }
     }
 
     void check_workers() {

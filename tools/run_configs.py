@@ -30,6 +30,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--e2e", action="store_true")
     ap.add_argument("--full", action="store_true", help="also run the full decoder-layer step (tcgen05 GEMMs)")
+    ap.add_argument("--bubble", action="store_true",
+                    help="also run the attention-only step with the per-warp %%globaltimer probe on every launch "
+                         "(measured intra-iteration bubble per iteration: p50 / p90 / p99 / max)")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     from paper_2605_23389_b200 import engine as E
@@ -38,14 +41,16 @@ def main():
         cfg = E.load_config(os.path.join(ROOT, "configs", name + ".json"))
         at = cfg["b200"]
         row = {"config": name, "policy": pol or "aligned", "start": start, "pair_mode": pair}
-        modes = ["value"] + (["e2e"] if a.e2e else []) + (["full_step"] if a.full else [])
+        modes = ["value"] + (["e2e"] if a.e2e else []) + (["full_step"] if a.full else []) + \
+            (["bubble"] if a.bubble else [])
         for mode in modes:
             try:
                     st = E.engine_run(cfg, policy=pol, device=0, num_q_heads=at["num_q_heads"],
                                   num_kv_heads=at["num_kv_heads"], num_layers=at["num_layers"],
                                   execute_transfers=(mode == "e2e"), exec_begin=start, timed_begin=start + a.warmup,
                                   exec_end=start + a.warmup + a.steps, copy_begin=max(0, start - 400),
-                                  host_pool_bytes=2 << 30, pair_mode=pair, full_step=(mode == "full_step"))
+                                  host_pool_bytes=2 << 30, pair_mode=pair, full_step=(mode == "full_step"),
+                                  probe_bubble=(mode == "bubble"))
             except ValueError as exc:  # e.g. full_step weights next to a pool sized for KV alone
                 row[mode] = {"skipped": str(exc)}
                 continue
@@ -60,6 +65,11 @@ def main():
                          "h2d_gb": st["h2d_bytes_window"] / 1e9, "p2p_gb": st["p2p_bytes_window"] / 1e9,
                          "p2p_gbps": (st["p2p_bytes_window"] / (st["p2p_busy_ms"] * 1e-3) / 1e9
                                       if st["p2p_busy_ms"] > 0 else None)}
+            if mode == "bubble":
+                row[mode].update({"bubble_p50_ms": st["bubble_p50_ms"], "bubble_p90_ms": st["bubble_p90_ms"],
+                                  "bubble_p99_ms": st["bubble_p99_ms"], "bubble_max_ms": st["bubble_max_ms"],
+                                  "bubble_per_iteration_ms": st.get("bubble_per_iteration_ms", []),
+                                  "virtual_bubble_per_iteration": "reference cost model, same iterations"})
             if mode == "full_step":
                 row[mode]["hbm_gbps"] = ((st["attn_bytes"] + st["weight_bytes"]) / (st["window_ms"] * 1e-3) / 1e9
                                          if st["window_ms"] > 0 else 0)
