@@ -321,12 +321,22 @@ typedef struct asv_engine_opts {
      * Requires execute_transfers, exec_begin = copy_begin = 0, exec_end = -1, no full_step, no
      * prefill offload; batches <= 1024 rows. */
     int32_t content_check;
-    const char* capture_path;   /* content_check: binary file, one record per executed iteration:
+    const char* capture_path;   /* binary file, one record per executed iteration:
                                    int64 seq; int32 b, L, n_q, head; int64 ids[b] (global request ids,
-                                   running order); int32 lens[b] (= prefix_len, attended tokens);
-                                   bf16 out[L][b][n_q][128] when head == -1 (every capture_every-th
-                                   iteration, by seq) else out[L][b][128] of query head `head` */
+                                   running order); int32 lens[b] (each request's seq_len decoded from the
+                                   split descriptors of the UPLOADED plan = tokens the kernel attends);
+                                   content_check: bf16 out[L][b][n_q][128] when head == -1 (every
+                                   capture_every-th iteration, by seq) else out[L][b][128] of query head
+                                   `head`; without content_check head == -2 and no outputs follow */
     int64_t capture_every;
+    /* Decision clock.  0 (default): the reference's virtual clock (calibrated cost model), so batch
+     * composition, order and bytes moved are bit-exact with the reference (SURVEY §7 hard part 1).
+     * 1: wall clock — every executed iteration's duration is its MEASURED GPU time (CUDA events around
+     * its launches); the orchestrator waits for it before the next boundary, so arrivals, starvation
+     * clocks, batch gating and transfer completions are decided against measured time (the serving
+     * mode; logs then differ from the reference by design).  KV-move durations stay modelled
+     * (transfer_time); the data plane still orders every real copy. */
+    int32_t wall_clock;
 } asv_engine_opts;
 
 /* transfer kinds for the per-kind byte counters */
@@ -385,7 +395,7 @@ typedef struct asv_engine_stats {
     double bubble_p50_ms, bubble_p90_ms, bubble_p99_ms, bubble_max_ms;
     int64_t content_inplace_bytes;        /* content mode: merged-FCFS prompts written in place (not a
                                              reference transfer, not in h2d_bytes) */
-    int64_t content_iterations_captured;  /* content mode: records written to capture_path */
+    int64_t content_iterations_captured;  /* records written to capture_path */
 } asv_engine_stats;
 
 int asv_engine_run(const char* config_json, const char* policy_override, const asv_engine_opts* opts,

@@ -122,6 +122,7 @@ class EngineOpts(C.Structure):
         ("content_check", C.c_int32),
         ("capture_path", C.c_char_p),
         ("capture_every", C.c_int64),
+        ("wall_clock", C.c_int32),
     ]
 
 

@@ -402,12 +402,14 @@ class GpuExecutor : public prefixsim::DataPlane {
             ASV_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&cap_host_),
                                    static_cast<size_t>(ring_) * static_cast<size_t>(cap_words_) * 4,
                                    cudaHostAllocMapped));
+        }
+        if (content_ || o.capture_path != nullptr) {
             slot_ids_.assign(static_cast<size_t>(ring_), {});
             slot_lens_.assign(static_cast<size_t>(ring_), {});
-            if (o.capture_path != nullptr) {
-                capture_ = std::fopen(o.capture_path, "wb");
-                if (capture_ == nullptr) throw std::runtime_error(std::string("cannot open ") + o.capture_path);
-            }
+        }
+        if (o.capture_path != nullptr) {  // content mode: outputs too; otherwise each page table's lengths
+            capture_ = std::fopen(o.capture_path, "wb");
+            if (capture_ == nullptr) throw std::runtime_error(std::string("cannot open ") + o.capture_path);
         }
         for (int i = 0; i < ring_; ++i) {
             ASV_CUDA(cudaEventCreate(&att_beg_[static_cast<size_t>(i)]));
@@ -604,6 +606,7 @@ class GpuExecutor : public prefixsim::DataPlane {
         }
         const bool timed = seq >= o_.timed_begin;
         const int64_t e = executed_++;
+        last_exec_ = e;
         const size_t slot = static_cast<size_t>(e % ring_);
         // throttle: the slot's previous iteration must be complete before reuse
         if (e >= ring_) retire_through(e - ring_);
@@ -657,12 +660,16 @@ class GpuExecutor : public prefixsim::DataPlane {
         const int64_t result_bytes = result_host_ ? b_rows * o_.num_q_heads * 256 : 0;
         if (o_.full_step && b_rows > max_rows_full_)
             throw std::runtime_error("full_step: batch exceeds the activation buffers");
-        if (content_) {
+        if (content_ || capture_ != nullptr) {
+            // what the kernel attends over: each request's seq_len decoded from the split descriptors
+            // of the plan being uploaded (running order = the request index of the descriptor)
             slot_ids_[slot].clear();
-            slot_lens_[slot].clear();
-            for (const auto& m : running) {
-                slot_ids_[slot].push_back(global_id(m.id));
-                slot_lens_[slot].push_back(static_cast<int32_t>(m.prefix_len));
+            slot_lens_[slot].assign(static_cast<size_t>(b_rows), -1);
+            for (const auto& m : running) slot_ids_[slot].push_back(global_id(m.id));
+            const int32_t* pd = plan_arena_host_ + pw + plan.off_desc;
+            for (int32_t g = 0; g < plan.total_splits; ++g) {
+                const int32_t r = pd[static_cast<int64_t>(g) * 40], len = pd[static_cast<int64_t>(g) * 40 + 4];
+                if (r >= 0 && r < b_rows) slot_lens_[slot][static_cast<size_t>(r)] = len;
             }
             slot_seq_[slot] = seq;
         }
@@ -1511,6 +1518,25 @@ class GpuExecutor : public prefixsim::DataPlane {
         });
     }
 
+    // wall-clock mode: the measured GPU time of the iteration just enqueued (att_beg .. att_end of its
+    // slot: plan upload done -> every layer launch of the step complete); blocks until it is known
+    bool measured_step_ms(const prefixsim::IterationRecord& rec, double* ms) override {
+        if (!o_.wall_clock || last_exec_ < 0 || last_exec_seq_ == rec.seq) return false;
+        const bool exec = rec.seq >= o_.exec_begin && (o_.exec_end < 0 || rec.seq < o_.exec_end);
+        if (!exec) return false;
+        const auto t0 = clock_now();
+        last_exec_seq_ = rec.seq;
+        launcher_.drain();
+        check_workers();
+        const size_t slot = static_cast<size_t>(last_exec_ % ring_);
+        ASV_CUDA(cudaEventSynchronize(att_end_[slot]));
+        float f = 0.f;
+        ASV_CUDA(cudaEventElapsedTime(&f, att_beg_[slot], att_end_[slot]));
+        *ms = static_cast<double>(f);
+        host_ms_ += ms_since(t0);
+        return true;
+    }
+
     // device -> mapped pinned host on the compute stream: an SM copy (never queued behind multi-GB
     // copy-engine traffic), or the copy engine in serial mode (profilers cannot replay a kernel that
     // writes mapped host memory)
@@ -1560,11 +1586,15 @@ class GpuExecutor : public prefixsim::DataPlane {
         const int64_t seq = slot_seq_[slot];
         const bool full = seq % every == 0;
         const int32_t hdr[4] = {static_cast<int32_t>(b), o_.num_layers, o_.num_q_heads,
-                                full ? -1 : static_cast<int32_t>(seq % o_.num_q_heads)};
+                                !content_ ? -2 : full ? -1 : static_cast<int32_t>(seq % o_.num_q_heads)};
         std::fwrite(&seq, 8, 1, capture_);
         std::fwrite(hdr, 4, 4, capture_);
         std::fwrite(ids.data(), 8, static_cast<size_t>(b), capture_);
         std::fwrite(lens.data(), 4, static_cast<size_t>(b), capture_);
+        if (!content_) {  // page-table lengths only
+            ++stats_.content_iterations_captured;
+            return;
+        }
         const auto* out = reinterpret_cast<const uint16_t*>(cap_host_ + slot * static_cast<size_t>(cap_words_));
         if (full) {
             std::fwrite(out, 2, static_cast<size_t>(b * o_.num_q_heads * 128 * o_.num_layers), capture_);
@@ -1640,7 +1670,7 @@ class GpuExecutor : public prefixsim::DataPlane {
                 stats_.measured_bubble_ms += idle_ms;
             }
         }
-        if (content_) write_capture(slot);
+        if (capture_ != nullptr) write_capture(slot);
         dec_.reclaim(false);
         if (pair_) pre_.reclaim(false);
     }
@@ -1671,6 +1701,8 @@ class GpuExecutor : public prefixsim::DataPlane {
     static_assert(kLanes == 8, "open_timer_ initialiser lists one entry per lane");
     SeqFlags flags_;
     bool serial_ = false;                   // profiler-safe ordering (copy_runtime.h serial mode)
+    int64_t last_exec_ = -1;                // executed-iteration index of the latest decode_step
+    int64_t last_exec_seq_ = -1;            // wall clock: seq whose measured time was reported
     CopyWorker worker_;                     // issues every copy-stream operation
     CopyWorker launcher_;                   // issues every compute-stream operation (iterations)
     std::thread watchdog_;                  // ASV_WATCHDOG=1: progress report every 5 s (debugging)

@@ -81,7 +81,7 @@ def engine_run(config, *, device: int = 0, prefetch_device: int | None = None,
                pair_mode: bool = False, full_step: bool = False, intermediate_size: int = 0,
                prefill_offload: bool | None = None, out_dir: str | None = None, return_log: bool = False,
                probe_bubble: bool = False, content_check: bool = False, capture_path: str | None = None,
-               capture_every: int = 1):
+               capture_every: int = 1, wall_clock: bool = False):
     """Run the decode engine on the GPU (asv_engine_run_ex): reference decisions executed for real.
 
     Returns the stats dict; with return_log=True, (stats, schema-1 JSONL log).  out_dir: also write
@@ -89,7 +89,8 @@ def engine_run(config, *, device: int = 0, prefetch_device: int | None = None,
     probe_bubble: measure the intra-iteration bubble of every attention launch of the timed window
     (stats["bubble_per_iteration_ms"] lists it per timed iteration).  content_check / capture_path /
     capture_every: the content-check test mode (include/asv.h) writing every executed iteration's
-    attention outputs to capture_path (read it with read_capture)."""
+    attention outputs to capture_path (read it with read_capture).  wall_clock: decisions against
+    measured iteration times instead of the reference's virtual clock (asv.h wall_clock)."""
     text = config if isinstance(config, str) else json.dumps(config)
     o = _lib.EngineOpts()
     o.decode_device = device
@@ -122,6 +123,7 @@ def engine_run(config, *, device: int = 0, prefetch_device: int | None = None,
     o.content_check = 1 if content_check else 0
     o.capture_path = capture_path.encode() if capture_path else None
     o.capture_every = capture_every
+    o.wall_clock = 1 if wall_clock else 0
     st = _lib.EngineStats()
     h = _lib.lib()
 
@@ -146,9 +148,10 @@ def engine_run(config, *, device: int = 0, prefetch_device: int | None = None,
 
 
 def read_capture(path: str):
-    """Records of a content-mode capture file (include/asv.h asv_engine_opts.capture_path):
-    dicts {seq, ids, lens, head, out} with out float32 [L][b][n_q][128] (head == -1) or [L][b][128]
-    (query head `head`)."""
+    """Records of a capture file (include/asv.h asv_engine_opts.capture_path): dicts
+    {seq, ids, lens, head, out}; lens = each request's seq_len decoded from the uploaded plan; out
+    float32 [L][b][n_q][128] (head == -1), [L][b][128] (query head `head`) or None (head == -2: no
+    content mode, page-table lengths only)."""
     recs = []
     with open(path, "rb") as f:
         data = f.read()
@@ -161,6 +164,9 @@ def read_capture(path: str):
         off += 8 * b
         lens = np.frombuffer(data, np.int32, b, off).copy()
         off += 4 * b
+        if head == -2:
+            recs.append({"seq": seq, "ids": ids, "lens": lens, "head": head, "out": None})
+            continue
         n = L * b * (n_q if head < 0 else 1) * 128
         raw = np.frombuffer(data, np.uint16, n, off)
         off += 2 * n
