@@ -42,7 +42,8 @@ struct asv_linear_chain_ws {
     int sms;
     uint32_t* done;    // [kMaxPhases] monotonically increasing tile counters
     uint32_t* arrive;  // [kMaxPhases][kMaxTiles] contributor arrivals per tile, reset by the owner
-    float* part;       // [2 * sms][256][128] contributor partials
+    float* part;       // [2 * sms][128][256] contributor partials (row-major: row, batch column)
+    float* pre;        // [2 * sms][128][256] owner's pre-reduced contributor sum
     uint32_t base[4];  // host: done[] value at the end of the previous launch
 };
 
@@ -86,6 +87,7 @@ struct ChainParams {
     uint32_t* done;
     uint32_t* arrive;
     float* part;
+    float* pre;
     ChainPhase ph[kMaxPhases];
 };
 
@@ -349,19 +351,50 @@ __global__ void __launch_bounds__(kThreads, 2)
                 const bool owner = u == tile0;
                 const int slot = p.nslots == 2 ? (seg & 1) : 0;
                 const int use = p.nslots == 2 ? (seg >> 1) : seg;
+                const int ncol = (p.batch + kChunk - 1) / kChunk * kChunk;
+                uint32_t* arrive = p.arrive + q * kMaxTiles + t;
+                const int last = owner ? cta_of(tile0 + P.kbs - 1, P.units, G) : c;  // contributors c+1..last
+                float* pre = p.pre + static_cast<int64_t>(c) * kBM * 256 + row * 256;
+                if (owner && last > c) {
+                    // while the MMA still runs this segment: sum the contributors' partials (their first
+                    // segments, ready early) in CTA order, 128-bit loads, two pieces in flight
+                    if (threadIdx.x == 0) wait_count(arrive, static_cast<uint32_t>(last - c));
+                    epi_bar();
+                    for (int c0 = 0; c0 < ncol; c0 += kChunk) {
+                        float4 acc[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 2
+                        for (int pc = c + 1; pc <= last; ++pc) {
+                            const float4* src = reinterpret_cast<const float4*>(
+                                p.part + (static_cast<int64_t>(pc) * kBM + row) * 256 + c0);
+                            float4 x[4];
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) x[k] = __ldcg(src + k);
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                acc[k].x += x[k].x;
+                                acc[k].y += x[k].y;
+                                acc[k].z += x[k].z;
+                                acc[k].w += x[k].w;
+                            }
+                        }
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) reinterpret_cast<float4*>(pre + c0)[k] = acc[k];
+                    }
+                }
                 mbar_wait(tfull0 + 8 * slot, static_cast<uint32_t>(use & 1));
                 tc_fence_after();
                 const uint32_t taddr = tmem + static_cast<uint32_t>(slot * p.ncols) + lane_off;
-                const int ncol = (p.batch + kChunk - 1) / kChunk * kChunk;
-                uint32_t* arrive = p.arrive + q * kMaxTiles + t;
                 if (!owner) {
                     // contributor: this CTA's first segment of the phase -> fp32 partial, then arrive
-                    float* dst = p.part + static_cast<int64_t>(c) * 256 * kBM;
+                    float4* dst = reinterpret_cast<float4*>(p.part + (static_cast<int64_t>(c) * kBM + row) * 256);
                     for (int c0 = 0; c0 < ncol; c0 += kChunk) {
                         float v[kChunk];
                         tmem_ld16(taddr + static_cast<uint32_t>(c0), v);
 #pragma unroll
-                        for (int i = 0; i < kChunk; ++i) dst[(c0 + i) * kBM + row] = v[i];
+                        for (int k = 0; k < 4; ++k)
+                            dst[c0 / 4 + k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
                     }
                     tc_fence_before();
                     __syncwarp();
@@ -370,12 +403,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                     epi_bar();
                     if (threadIdx.x == 0) red_release_add(arrive, 1u);
                 } else {
-                    const int last = cta_of(tile0 + P.kbs - 1, P.units, G);  // contributors: c+1 .. last
-                    if (threadIdx.x == 0) {
-                        if (last > c) wait_count(arrive, static_cast<uint32_t>(last - c));
-                        // the residual rows / positions this epilogue reads were written by earlier phases
-                        if (q > 0) wait_count(p.done + (q - 1), p.ph[q - 1].done_target);
-                    }
+                    // the residual rows / positions this epilogue reads were written by earlier phases
+                    if (threadIdx.x == 0 && q > 0) wait_count(p.done + (q - 1), p.ph[q - 1].done_target);
                     if (P.ss_in != nullptr) mbar_wait(rsfull0 + 8 * (q & 1), static_cast<uint32_t>((q >> 1) & 1));
                     epi_bar();
                     const float* rs = rsbuf + (q & 1) * 256;
@@ -387,10 +416,15 @@ __global__ void __launch_bounds__(kThreads, 2)
                             __syncwarp();
                             if (lane == 0) mbar_arrive(tempty0 + 8 * slot);
                         }
-                        for (int pc = c + 1; pc <= last; ++pc) {
-                            const float* src = p.part + static_cast<int64_t>(pc) * 256 * kBM + c0 * kBM + row;
+                        if (last > c) {  // own piece + the contributors' sum (this thread wrote it)
 #pragma unroll
-                            for (int i = 0; i < kChunk; ++i) v[i] += __ldcg(src + i * kBM);
+                            for (int k = 0; k < 4; ++k) {
+                                const float4 x = reinterpret_cast<const float4*>(pre + c0)[k];
+                                v[4 * k] += x.x;
+                                v[4 * k + 1] += x.y;
+                                v[4 * k + 2] += x.z;
+                                v[4 * k + 3] += x.w;
+                            }
                         }
 #pragma unroll
                         for (int i = 0; i < kChunk; ++i) chunk[i * kBM + row] = v[i];
@@ -474,6 +508,7 @@ int chain_run(const asv_linear_args* ph, int n, asv_linear_chain_ws* ws, cudaStr
     p.done = ws->done;
     p.arrive = ws->arrive;
     p.part = ws->part;
+    p.pre = ws->pre;
     int64_t min_units = INT64_MAX;
     for (int q = 0; q < n; ++q) {
         const asv_linear_args& a = ph[q];
@@ -574,6 +609,7 @@ int asv_linear_chain_ws_create(int32_t device, asv_linear_chain_ws** out) {
     e = cudaMalloc(&ws->done, asv::kMaxPhases * sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMalloc(&ws->arrive, asv::kMaxPhases * asv::kMaxTiles * sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMalloc(&ws->part, part);
+    if (e == cudaSuccess) e = cudaMalloc(&ws->pre, part);
     if (e == cudaSuccess) e = cudaMemset(ws->done, 0, asv::kMaxPhases * sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMemset(ws->arrive, 0, asv::kMaxPhases * asv::kMaxTiles * sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -594,6 +630,7 @@ void asv_linear_chain_ws_destroy(asv_linear_chain_ws* ws) {
     if (ws->done) cudaFree(ws->done);
     if (ws->arrive) cudaFree(ws->arrive);
     if (ws->part) cudaFree(ws->part);
+    if (ws->pre) cudaFree(ws->pre);
     cudaSetDevice(prev);
     delete ws;
 }

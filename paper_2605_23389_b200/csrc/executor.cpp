@@ -425,6 +425,7 @@ class GpuExecutor : public prefixsim::DataPlane {
         std::memset(stats_.logical_bytes, 0, sizeof(stats_.logical_bytes));
         std::memset(stats_.logical_count, 0, sizeof(stats_.logical_count));
         if (o.execute_transfers) warm_up_copies();
+        nvtxInitialize(nullptr);  // NVTX's lazy init is not thread-safe: do it before the workers start
         worker_.start(serial_);
         launcher_.start(serial_);
         if (std::getenv("ASV_WATCHDOG") != nullptr) {

@@ -88,8 +88,9 @@ def test_full_decode_step_runs_and_is_deterministic():
     for k, v in want.items():
         assert a["logical_bytes"][k] == v, k
     assert a["iterations_timed"] == b["iterations_timed"] == GOLDEN["logs"]["smoke:aligned"]["iterations"]
-    # per layer >= attention + 4 GEMM launches (the RMSNorms are fused into the GEMMs after layer 0)
-    assert a["window_ms"] > 0 and a["kernel_launches_timed"] > b["iterations_timed"] * 32 * 5
+    # per layer >= attention + one persistent GEMM chain (O, gate/up, down, next QKV; the RMSNorms are
+    # fused into the GEMMs after layer 0)
+    assert a["window_ms"] > 0 and a["kernel_launches_timed"] >= b["iterations_timed"] * 32 * 2
 
 
 def test_gqa_13b_config_executes():
