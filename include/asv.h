@@ -266,6 +266,10 @@ typedef struct asv_linear_chain_ws asv_linear_chain_ws;
 int asv_linear_chain_ws_create(int32_t device, asv_linear_chain_ws** out);
 void asv_linear_chain_ws_destroy(asv_linear_chain_ws* ws);
 int asv_linear_chain(const asv_linear_args* phases, int32_t n, asv_linear_chain_ws* ws, void* stream);
+/* Measurement only: enable (1) / disable (0) a per-CTA, per-phase %globaltimer timeline of the chain
+ * launches on `ws`; with `out` (capacity `cap` words) copies the last launch's [grid][4][6] stamps
+ * (decode_chain.cu kTraceSlots) and sets *n.  Synchronous. */
+int asv_linear_chain_ws_trace(asv_linear_chain_ws* ws, int32_t enable, uint64_t* out, int64_t cap, int64_t* n);
 /* out[b][:] = h[b][:] * rsqrt(mean(h[b]^2) + eps) * gamma; rows [batch, rows_out) of out zeroed */
 int asv_rmsnorm(const void* h, const void* gamma, void* out, int32_t dim, int32_t batch, int32_t rows_out,
                 float eps, int32_t pdl, void* stream);

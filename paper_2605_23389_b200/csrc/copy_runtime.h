@@ -26,7 +26,9 @@
 
 #include <atomic>
 #include <condition_variable>
+#include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <deque>
 #include <functional>
 #include <mutex>
@@ -36,10 +38,27 @@
 
 namespace asv {
 
-// ASV_SERIAL=1, or a CUDA injection library (ncu / nsys / compute-sanitizer) is loaded
+// ASV_SERIAL=1, or a CUDA injection library (ncu / nsys / compute-sanitizer) is loaded.  Nsight
+// Compute starts its target through an LD_PRELOAD launcher and does not leave CUDA_INJECTION64_PATH
+// in the environment (measured), so the process's own mappings are checked too.
 inline bool serial_mode_requested() {
     if (const char* e = std::getenv("ASV_SERIAL")) return std::atoi(e) != 0;
-    return std::getenv("CUDA_INJECTION64_PATH") != nullptr;
+    if (std::getenv("CUDA_INJECTION64_PATH") != nullptr) return true;
+    if (const char* pre = std::getenv("LD_PRELOAD")) {
+        const std::string s(pre);
+        if (s.find("TreeLauncher") != std::string::npos || s.find("nsight") != std::string::npos) return true;
+    }
+    std::FILE* f = std::fopen("/proc/self/maps", "r");
+    if (f == nullptr) return false;
+    char line[4096];
+    bool hit = false;
+    while (!hit && std::fgets(line, sizeof(line), f) != nullptr) {
+        hit = std::strstr(line, "cuda-injection") != nullptr || std::strstr(line, "InjectionTarget") != nullptr ||
+              std::strstr(line, "TreeLauncher") != nullptr || std::strstr(line, "libToolsInjection") != nullptr ||
+              std::strstr(line, "sanitizer-public") != nullptr || std::strstr(line, "libsanitizer-collection") != nullptr;
+    }
+    std::fclose(f);
+    return hit;
 }
 
 class SeqFlags {

@@ -45,6 +45,8 @@ struct asv_linear_chain_ws {
     float* part;       // [2 * sms][128][256] contributor partials (row-major: row, batch column)
     float* pre;        // [2 * sms][128][256] owner's pre-reduced contributor sum
     uint32_t base[4];  // host: done[] value at the end of the previous launch
+    unsigned long long* trace;  // optional timeline of the last launch (asv_linear_chain_ws_trace)
+    int32_t trace_grid;         // grid of the last traced launch
 };
 
 namespace asv {
@@ -59,6 +61,11 @@ constexpr int kRingBudget = 92 * 1024;   // + 10 KiB epilogue / scale buffers: t
 constexpr int kThreads = 256;
 constexpr int kProducerWarp = 4, kMmaWarp = 5, kHelperWarp0 = 6;
 constexpr int kChunk = 16;               // accumulator columns per epilogue round
+// timeline probe (asv_linear_chain_ws_trace): per CTA and phase, %globaltimer at
+//   0 producer: activations' dependency satisfied   1 producer: last unit issued
+//   2 epilogue: first segment accumulated            3 epilogue: last segment accumulated
+//   4 epilogue: contributors' partials complete      5 epilogue: phase finished (done / arrive bumped)
+constexpr int kTraceSlots = 6;
 
 struct alignas(64) ChainMaps {
     CUtensorMap w[kMaxPhases];
@@ -88,6 +95,7 @@ struct ChainParams {
     uint32_t* arrive;
     float* part;
     float* pre;
+    unsigned long long* trace;  // optional [grid][kMaxPhases][kTraceSlots] %globaltimer stamps
     ChainPhase ph[kMaxPhases];
 };
 
@@ -110,6 +118,12 @@ __device__ __forceinline__ void wait_count(const uint32_t* p, uint32_t target) {
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void stamp(const ChainParams& p, int c, int q, int k) {
+    if (p.trace == nullptr) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[(static_cast<int64_t>(c) * kMaxPhases + q) * kTraceSlots + k] = t;
 }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 __device__ __forceinline__ void helper_bar() { asm volatile("bar.sync 2, 64;" ::: "memory"); }
@@ -253,6 +267,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 } else {
                     wait_count(p.done + (q - 1), p.ph[q - 1].done_target);
                 }
+                stamp(p, c, q, 0);
                 fence_proxy_async();
                 for (int i = 0, st = s_pre; i < pre; ++i) {
                     tma_load_2d(smem_u32(smem + st * stage_bytes) + kABytes, &maps.x[q],
@@ -271,6 +286,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                         ph ^= 1;
                     }
                 }
+                stamp(p, c, q, 1);
             }
         }
     } else if (warp == kMmaWarp) {
@@ -358,7 +374,10 @@ __global__ void __launch_bounds__(kThreads, 2)
                 if (owner && last > c) {
                     // while the MMA still runs this segment: sum the contributors' partials (their first
                     // segments, ready early) in CTA order, 128-bit loads, two pieces in flight
-                    if (threadIdx.x == 0) wait_count(arrive, static_cast<uint32_t>(last - c));
+                    if (threadIdx.x == 0) {
+                        wait_count(arrive, static_cast<uint32_t>(last - c));
+                        stamp(p, c, q, 4);
+                    }
                     epi_bar();
                     for (int c0 = 0; c0 < ncol; c0 += kChunk) {
                         float4 acc[4];
@@ -385,6 +404,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 }
                 mbar_wait(tfull0 + 8 * slot, static_cast<uint32_t>(use & 1));
                 tc_fence_after();
+                if (threadIdx.x == 0) stamp(p, c, q, u == u0 ? 2 : 3);
                 const uint32_t taddr = tmem + static_cast<uint32_t>(slot * p.ncols) + lane_off;
                 if (!owner) {
                     // contributor: this CTA's first segment of the phase -> fp32 partial, then arrive
@@ -401,7 +421,10 @@ __global__ void __launch_bounds__(kThreads, 2)
                     if (lane == 0) mbar_arrive(tempty0 + 8 * slot);
                     __threadfence();
                     epi_bar();
-                    if (threadIdx.x == 0) red_release_add(arrive, 1u);
+                    if (threadIdx.x == 0) {
+                        red_release_add(arrive, 1u);
+                        stamp(p, c, q, 5);
+                    }
                 } else {
                     // the residual rows / positions this epilogue reads were written by earlier phases
                     if (threadIdx.x == 0 && q > 0) wait_count(p.done + (q - 1), p.ph[q - 1].done_target);
@@ -436,7 +459,10 @@ __global__ void __launch_bounds__(kThreads, 2)
                     fence_proxy_async();  // outputs are read by the next phase's TMA loads
                     __threadfence();
                     epi_bar();
-                    if (threadIdx.x == 0) red_release_add(p.done + q, 1u);
+                    if (threadIdx.x == 0) {
+                        red_release_add(p.done + q, 1u);
+                        stamp(p, c, q, 5);
+                    }
                 }
                 u = seg1;
             }
@@ -509,6 +535,7 @@ int chain_run(const asv_linear_args* ph, int n, asv_linear_chain_ws* ws, cudaStr
     p.arrive = ws->arrive;
     p.part = ws->part;
     p.pre = ws->pre;
+    p.trace = ws->trace;
     int64_t min_units = INT64_MAX;
     for (int q = 0; q < n; ++q) {
         const asv_linear_args& a = ph[q];
@@ -577,6 +604,7 @@ int chain_run(const asv_linear_args* ph, int n, asv_linear_chain_ws* ws, cudaStr
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = ph[0].pdl ? 1 : 0;
+    ws->trace_grid = grid;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, linear_chain_kernel, maps, p);
     if (e != cudaSuccess) return cuda_fail(e, "linear_chain launch");
     for (int q = 0; q < n; ++q) ws->base[q] = p.ph[q].done_target;
@@ -631,8 +659,32 @@ void asv_linear_chain_ws_destroy(asv_linear_chain_ws* ws) {
     if (ws->arrive) cudaFree(ws->arrive);
     if (ws->part) cudaFree(ws->part);
     if (ws->pre) cudaFree(ws->pre);
+    if (ws->trace) cudaFree(ws->trace);
     cudaSetDevice(prev);
     delete ws;
+}
+
+int asv_linear_chain_ws_trace(asv_linear_chain_ws* ws, int32_t enable, uint64_t* out, int64_t cap, int64_t* n) {
+    if (ws == nullptr) return asv::fail(ASV_ERR_INVALID, "linear_chain_ws_trace: null workspace");
+    const size_t words = static_cast<size_t>(2 * ws->sms) * asv::kMaxPhases * asv::kTraceSlots;
+    if (enable != 0 && ws->trace == nullptr) {
+        const cudaError_t e = cudaMalloc(&ws->trace, words * 8);
+        if (e != cudaSuccess) return asv::cuda_fail(e, "linear_chain_ws_trace");
+        cudaMemset(ws->trace, 0, words * 8);
+    }
+    if (enable == 0 && ws->trace != nullptr) {
+        cudaFree(ws->trace);
+        ws->trace = nullptr;
+    }
+    if (n != nullptr) *n = 0;
+    if (out != nullptr && ws->trace != nullptr) {
+        const size_t m = static_cast<size_t>(ws->trace_grid) * asv::kMaxPhases * asv::kTraceSlots;
+        if (static_cast<int64_t>(m) > cap) return asv::fail(ASV_ERR_INVALID, "linear_chain_ws_trace: out too small");
+        const cudaError_t e = cudaMemcpy(out, ws->trace, m * 8, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return asv::cuda_fail(e, "linear_chain_ws_trace copy");
+        if (n != nullptr) *n = static_cast<int64_t>(m);
+    }
+    return ASV_OK;
 }
 
 int asv_linear_chain(const asv_linear_args* phases, int32_t n, asv_linear_chain_ws* ws, void* stream) {

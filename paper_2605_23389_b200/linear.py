@@ -48,6 +48,20 @@ class ChainWorkspace:
         self.h = C.c_void_p()
         _lib.check(_lib.lib().asv_linear_chain_ws_create(device, C.byref(self.h)))
 
+    def trace(self, enable: bool | None = None):
+        """Measurement only: turn the per-CTA phase timeline on / off, or (enable=None) return the last
+        launch's stamps as a uint64 array [grid][4 phases][6] (decode_chain.cu kTraceSlots)."""
+        import numpy as np
+        h = _lib.lib()
+        if enable is not None:
+            _lib.check(h.asv_linear_chain_ws_trace(self.h, 1 if enable else 0, None, 0, None))
+            return None
+        cap = 2 * 148 * 4 * 6 * 4
+        buf = np.zeros(cap, np.uint64)
+        n = C.c_int64(0)
+        _lib.check(h.asv_linear_chain_ws_trace(self.h, 1, buf.ctypes.data_as(C.POINTER(C.c_uint64)), cap, C.byref(n)))
+        return buf[:n.value].reshape(-1, 4, 6)
+
     def __del__(self):
         if getattr(self, "h", None) and self.h.value:
             _lib.lib().asv_linear_chain_ws_destroy(self.h)
