@@ -246,6 +246,12 @@ typedef struct asv_linear_args {
     const float* ss_in;
     int32_t ss_parts, ss_ld, ss_dim;
     float ss_eps;
+    /* Optional (null = off): the weights of the NEXT linear on the stream ([next_n_out][next_k], same
+     * batch).  Once a CTA has issued its last weight load it prefetches a share of the first ring
+     * stages the next launch's CTAs will request into L2 (cp.async.bulk.prefetch.tensor), so HBM keeps
+     * streaming through this launch's tail and the next launch's prologue.  No effect on results. */
+    const void* next_w;
+    int32_t next_n_out, next_k;
 } asv_linear_args;
 
 /* One launch: one CTA per (128-row tile, K split); the K splits of a tile are one

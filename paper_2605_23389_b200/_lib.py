@@ -89,6 +89,9 @@ class LinearArgs(C.Structure):
         ("ss_ld", C.c_int32),
         ("ss_dim", C.c_int32),
         ("ss_eps", C.c_float),
+        ("next_w", C.c_void_p),
+        ("next_n_out", C.c_int32),
+        ("next_k", C.c_int32),
     ]
 
 

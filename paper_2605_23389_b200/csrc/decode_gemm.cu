@@ -53,6 +53,8 @@ struct LinearParams {
     const float* ss_in;
     int32_t ss_parts, ss_ld;
     float ss_inv_dim, ss_eps;
+    // next linear's first ring stages -> L2 (0 tiles: off)
+    int32_t next_tiles, next_splits, next_kb_per_split, next_kbs, next_pre;
 };
 
 using namespace tc;
@@ -62,7 +64,7 @@ using namespace tc;
 template <int EPI>
 __global__ void __launch_bounds__(128, 2)
     linear_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
-                  const LinearParams p) {
+                  const __grid_constant__ CUtensorMap tm_next, const LinearParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int stage_bytes = kABytes + p.bn * 128;
@@ -130,6 +132,17 @@ __global__ void __launch_bounds__(128, 2)
             if (++s == nst) {
                 s = 0;
                 ph ^= 1;
+            }
+        }
+        // every weight load of this CTA is issued: keep HBM busy through the tail and the next launch's
+        // prologue by pulling a share of the next linear's first ring stages into L2
+        if (p.next_tiles > 0) {
+            const int total = p.next_tiles * p.next_splits * p.next_pre;
+            for (int i = blockIdx.x; i < total; i += gridDim.x) {
+                const int j = i / p.next_pre, st = i - j * p.next_pre;
+                const int nt = j / p.next_splits, ns = j - nt * p.next_splits;
+                const int kb = ns * p.next_kb_per_split + st;
+                if (st < p.next_kb_per_split && kb < p.next_kbs) tma_prefetch_l2(&tm_next, kb * kBK, nt * kBM);
             }
         }
     } else if (warp == 1 && lane == 0) {
@@ -319,8 +332,8 @@ int smem_bytes(int bn) {
 }
 
 template <int EPI>
-cudaError_t launch_epi(const CUtensorMap& tw, const CUtensorMap& tx, const LinearParams& p, int grid, bool pdl,
-                       cudaStream_t st) {
+cudaError_t launch_epi(const CUtensorMap& tw, const CUtensorMap& tx, const CUtensorMap& tn, const LinearParams& p,
+                       int grid, bool pdl, cudaStream_t st) {
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(linear_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -349,7 +362,7 @@ cudaError_t launch_epi(const CUtensorMap& tw, const CUtensorMap& tx, const Linea
     }
     cfg.attrs = attr;
     cfg.numAttrs = n;
-    return cudaLaunchKernelEx(&cfg, linear_kernel<EPI>, tw, tx, p);
+    return cudaLaunchKernelEx(&cfg, linear_kernel<EPI>, tw, tx, tn, p);
 }
 
 }  // namespace
@@ -434,13 +447,30 @@ static int linear_run(const asv_linear_args* a, cudaStream_t st) {
     p.ss_ld = a->ss_ld;
     p.ss_inv_dim = a->ss_dim > 0 ? 1.f / static_cast<float>(a->ss_dim) : 0.f;
     p.ss_eps = a->ss_eps;
+    // the next linear's weights: its first ring stages are prefetched into L2 by this launch's tail
+    // (ASV_LINEAR_NEXT_PF=0 turns it off, =N caps the stages per next CTA; A/B experiments)
+    CUtensorMap tn = tw;
+    static const int next_pf = [] {
+        const char* e = getenv("ASV_LINEAR_NEXT_PF");
+        return e != nullptr ? atoi(e) : -1;
+    }();
+    if (a->next_w != nullptr && next_pf != 0 && a->next_n_out > 0 && a->next_n_out % kBM == 0 && a->next_k > 0 &&
+        a->next_k % kBK == 0 && make_map(&tn, a->next_w, static_cast<uint64_t>(a->next_n_out),
+                                         static_cast<uint64_t>(a->next_k), kBM)) {
+        const int nsp = linear_splits(a->next_n_out, a->next_k, sms);
+        p.next_tiles = a->next_n_out / kBM;
+        p.next_splits = nsp;
+        p.next_kbs = a->next_k / kBK;
+        p.next_kb_per_split = (p.next_kbs + nsp - 1) / nsp;
+        p.next_pre = next_pf > 0 ? next_pf : stages_for(bn);
+    }
     const int grid = tiles * splits;
     cudaError_t e;
     switch (a->epilogue) {
-        case ASV_EPI_STORE: e = launch_epi<ASV_EPI_STORE>(tw, tx, p, grid, a->pdl != 0, st); break;
-        case ASV_EPI_RESIDUAL: e = launch_epi<ASV_EPI_RESIDUAL>(tw, tx, p, grid, a->pdl != 0, st); break;
-        case ASV_EPI_SILU_MUL: e = launch_epi<ASV_EPI_SILU_MUL>(tw, tx, p, grid, a->pdl != 0, st); break;
-        case ASV_EPI_QKV_ROPE: e = launch_epi<ASV_EPI_QKV_ROPE>(tw, tx, p, grid, a->pdl != 0, st); break;
+        case ASV_EPI_STORE: e = launch_epi<ASV_EPI_STORE>(tw, tx, tn, p, grid, a->pdl != 0, st); break;
+        case ASV_EPI_RESIDUAL: e = launch_epi<ASV_EPI_RESIDUAL>(tw, tx, tn, p, grid, a->pdl != 0, st); break;
+        case ASV_EPI_SILU_MUL: e = launch_epi<ASV_EPI_SILU_MUL>(tw, tx, tn, p, grid, a->pdl != 0, st); break;
+        case ASV_EPI_QKV_ROPE: e = launch_epi<ASV_EPI_QKV_ROPE>(tw, tx, tn, p, grid, a->pdl != 0, st); break;
         default: return fail(ASV_ERR_INVALID, "linear: unknown epilogue");
     }
     if (e != cudaSuccess) return cuda_fail(e, "linear launch");

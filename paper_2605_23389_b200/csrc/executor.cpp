@@ -1387,10 +1387,11 @@ class GpuExecutor : public prefixsim::DataPlane {
         ss_ld_ = static_cast<int32_t>(rows_pad);
         ASV_CUDA(cudaMalloc(&ss_a_, static_cast<size_t>(ss_parts_) * rows_pad * 4));
         ASV_CUDA(cudaMalloc(&ss_b_, static_cast<size_t>(ss_parts_) * rows_pad * 4));
-        // persistent stream-K chain per layer (decode_chain.cu): needs the fused norms; ASV_LINEAR_CHAIN=0
-        // keeps one launch per GEMM (A/B experiments)
+        // persistent stream-K chain per layer (decode_chain.cu), opt-in with ASV_LINEAR_CHAIN=1: measured
+        // slower than one launch per GEMM (its cross-CTA split-K reduction sits on every phase boundary,
+        // DESIGN §4), so the default stays one launch per GEMM with the next weights prefetched into L2
         const char* ce = std::getenv("ASV_LINEAR_CHAIN");
-        chain_ = fuse_norm_ && (ce == nullptr || std::atoi(ce) != 0);
+        chain_ = fuse_norm_ && ce != nullptr && std::atoi(ce) != 0;
         if (chain_ && asv_linear_chain_ws_create(o_.decode_device, &chain_ws_) != ASV_OK)
             throw CudaError(asv_last_error());
         ASV_CUDA(cudaStreamSynchronize(compute_));
@@ -1417,6 +1418,13 @@ class GpuExecutor : public prefixsim::DataPlane {
     template <typename F>
     static void row_chunks(int32_t b, F&& f) {
         for (int32_t r0 = 0; r0 < b; r0 += 256) f(r0, std::min<int32_t>(256, b - r0));
+    }
+    // the weights of the linear launched right after this one: its first ring stages are pulled into L2
+    // by this launch's tail (asv.h next_w)
+    static void next_weights(asv_linear_args& a, const void* w, int32_t n_out, int32_t k) {
+        a.next_w = w;
+        a.next_n_out = n_out;
+        a.next_k = k;
     }
     // the next linear takes the raw residual stream h and applies RMSNorm in its epilogue
     void fuse_in(asv_linear_args& a, const float* ss, int32_t r0) const {
@@ -1457,6 +1465,7 @@ class GpuExecutor : public prefixsim::DataPlane {
             if (fuse_norm_) {
                 a.ss_out = ss_b_ + r0;
                 a.ss_ld = ss_ld_;
+                next_weights(a, lw.gate_up, 2 * inter_, hidden_);  // no RMSNorm launch in between
             }
             if (asv_linear(&a, compute_) != ASV_OK) throw CudaError(asv_last_error());
         });
@@ -1468,6 +1477,7 @@ class GpuExecutor : public prefixsim::DataPlane {
             asv_linear_args a = lin(lw.gate_up, 2 * inter_, hidden_, xin + int64_t(r0) * hidden_, n,
                                     act + int64_t(r0) * inter_, inter_, ASV_EPI_SILU_MUL);
             if (fuse_norm_) fuse_in(a, ss_b_, r0);
+            next_weights(a, lw.down, hidden_, inter_);
             if (asv_linear(&a, compute_) != ASV_OK) throw CudaError(asv_last_error());
         });
         row_chunks(b, [&](int32_t r0, int32_t n) {  // h += act . Wd^T
@@ -1476,6 +1486,9 @@ class GpuExecutor : public prefixsim::DataPlane {
             if (fuse_norm_) {  // for the next layer's QKV
                 a.ss_out = ss_a_ + r0;
                 a.ss_ld = ss_ld_;
+                if (l + 1 < o_.num_layers)
+                    next_weights(a, layers_[static_cast<size_t>(l + 1)].qkv, 128 * (o_.num_q_heads + 2 * o_.num_kv_heads),
+                                 hidden_);
             }
             if (asv_linear(&a, compute_) != ASV_OK) throw CudaError(asv_last_error());
         });

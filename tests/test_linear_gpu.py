@@ -293,3 +293,24 @@ def test_chain_rejects_mixed_batches():
     y = torch.empty(8, 128, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(ValueError, match="same batch"):
         L.linear_chain([dict(x=x, w=w, batch=4, y=y), dict(x=x, w=w, batch=3, y=y)], ws)
+
+
+def test_next_weights_l2_prefetch_leaves_results_unchanged():
+    """asv.h next_w: a launch's tail prefetches the next linear's first ring stages into L2 — pure
+    data movement, the outputs are bit-identical with and without it."""
+    from paper_2605_23389_b200 import linear as L
+    batch, d, inter = 6, 4096, 11008
+    x = _x(batch, d, 81)
+    wo = _rand((d, d), 82, 1 / math.sqrt(d))
+    wgu = _rand((2 * inter, d), 83, 1 / math.sqrt(d))
+    outs = []
+    for nxt in (None, wgu):
+        h = _rand((batch, d), 84)
+        L.linear(x, wo, batch, h, L.RESIDUAL, pdl=True, next_w=nxt)
+        act = torch.zeros(batch, inter, dtype=torch.bfloat16, device="cuda")
+        hx = torch.zeros(16, d, dtype=torch.bfloat16, device="cuda")
+        hx[:batch] = h
+        L.linear(hx, wgu, batch, act, L.SILU_MUL, pdl=True)
+        torch.cuda.synchronize()
+        outs.append((h.clone(), act.clone()))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
