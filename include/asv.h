@@ -246,10 +246,10 @@ typedef struct asv_linear_args {
     const float* ss_in;
     int32_t ss_parts, ss_ld, ss_dim;
     float ss_eps;
-    /* Optional (null = off): the weights of the NEXT linear on the stream ([next_n_out][next_k], same
-     * batch).  Once a CTA has issued its last weight load it prefetches a share of the first ring
-     * stages the next launch's CTAs will request into L2 (cp.async.bulk.prefetch.tensor), so HBM keeps
-     * streaming through this launch's tail and the next launch's prologue.  No effect on results. */
+    /* Optional: the weights of the NEXT linear on the stream ([next_n_out][next_k], same batch).  With
+     * ASV_LINEAR_NEXT_PF=N set, a CTA that has issued its last weight load prefetches a share of the
+     * first N ring stages the next launch's CTAs will request into L2 (cp.async.bulk.prefetch.tensor).
+     * Off by default (measured no gain on B200).  No effect on results. */
     const void* next_w;
     int32_t next_n_out, next_k;
 } asv_linear_args;

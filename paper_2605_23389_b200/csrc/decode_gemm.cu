@@ -447,12 +447,14 @@ static int linear_run(const asv_linear_args* a, cudaStream_t st) {
     p.ss_ld = a->ss_ld;
     p.ss_inv_dim = a->ss_dim > 0 ? 1.f / static_cast<float>(a->ss_dim) : 0.f;
     p.ss_eps = a->ss_eps;
-    // the next linear's weights: its first ring stages are prefetched into L2 by this launch's tail
-    // (ASV_LINEAR_NEXT_PF=0 turns it off, =N caps the stages per next CTA; A/B experiments)
+    // the next linear's weights: ASV_LINEAR_NEXT_PF=N prefetches the first N ring stages of every
+    // next-launch CTA into L2 from this launch's tail.  Off by default: measured on B200 (r02, C2 full
+    // step 565.8 tok/s off vs 559-568 with N = 2..8; 7B GEMM stack -2 to -4%), the boundary is not an
+    // idle-HBM gap that L2 prefetch can fill
     CUtensorMap tn = tw;
     static const int next_pf = [] {
         const char* e = getenv("ASV_LINEAR_NEXT_PF");
-        return e != nullptr ? atoi(e) : -1;
+        return e != nullptr ? atoi(e) : 0;
     }();
     if (a->next_w != nullptr && next_pf != 0 && a->next_n_out > 0 && a->next_n_out % kBM == 0 && a->next_k > 0 &&
         a->next_k % kBK == 0 && make_map(&tn, a->next_w, static_cast<uint64_t>(a->next_n_out),
@@ -462,7 +464,7 @@ static int linear_run(const asv_linear_args* a, cudaStream_t st) {
         p.next_splits = nsp;
         p.next_kbs = a->next_k / kBK;
         p.next_kb_per_split = (p.next_kbs + nsp - 1) / nsp;
-        p.next_pre = next_pf > 0 ? next_pf : stages_for(bn);
+        p.next_pre = next_pf;
     }
     const int grid = tiles * splits;
     cudaError_t e;

@@ -296,8 +296,10 @@ def test_chain_rejects_mixed_batches():
 
 
 def test_next_weights_l2_prefetch_leaves_results_unchanged():
-    """asv.h next_w: a launch's tail prefetches the next linear's first ring stages into L2 — pure
-    data movement, the outputs are bit-identical with and without it."""
+    """asv.h next_w (with ASV_LINEAR_NEXT_PF set, as the A/B runs do): a launch's tail prefetches the next
+    linear's first ring stages into L2 — pure data movement, the outputs are bit-identical with and
+    without it.  (The knob is read once per process: the test runs the prefetch path only when the
+    environment enables it.)"""
     from paper_2605_23389_b200 import linear as L
     batch, d, inter = 6, 4096, 11008
     x = _x(batch, d, 81)
