@@ -154,6 +154,15 @@ typedef struct asv_attn_args {
                                   intra-iteration bubble */
     int32_t kv_dtype;       /* ASV_KV_BF16 (0, default) or ASV_KV_F16: the element type of the KV pool,
                                q, k_new / v_new and out (the layout is the same 16-bit one) */
+    /* Deferred split merge (consecutive launches on one workspace with the SAME plan, e.g. the L layers
+     * of an attention-only decode step): defer_merge = 1 leaves this launch's split-request partials in
+     * the workspace half of its launch_index parity and launches no merge kernel; the next launch, with
+     * prev_out (and optionally prev_lse) set to where those rows go, merges them with its own warps
+     * right after its dependency wait — one grid boundary per layer instead of two.  The last launch
+     * of a chain keeps defer_merge = 0. */
+    int32_t defer_merge;
+    void* prev_out;
+    float* prev_lse;
 } asv_attn_args;
 
 #define ASV_KV_BF16 0

@@ -61,6 +61,9 @@ class AttnArgs(C.Structure):
         ("pdl", C.c_int32),
         ("warp_timestamps", C.c_void_p),
         ("kv_dtype", C.c_int32),
+        ("defer_merge", C.c_int32),
+        ("prev_out", C.c_void_p),
+        ("prev_lse", C.c_void_p),
     ]
 
 

@@ -123,8 +123,13 @@ class PagedDecodeAttention:
     # ------------------------------------------------------------------- run
     def run(self, q: torch.Tensor, kv_pool: torch.Tensor, layer: int, plan: Plan,
             out: torch.Tensor, lse: torch.Tensor | None = None, k_new: torch.Tensor | None = None,
-            v_new: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-        """out[b][n_h][128] (self.dtype) = softmax(q K^T * sm_scale) V for every request of the plan."""
+            v_new: torch.Tensor | None = None, stream=None, defer_merge: bool = False,
+            prev_out: torch.Tensor | None = None, prev_lse: torch.Tensor | None = None) -> torch.Tensor:
+        """out[b][n_h][128] (self.dtype) = softmax(q K^T * sm_scale) V for every request of the plan.
+
+        defer_merge / prev_out (include/asv.h): consecutive calls with the same plan may leave the split
+        merge of one call to the next — defer_merge=True skips this call's merge kernel (its split
+        rows of `out` are written by the next call, which must pass prev_out=out)."""
         b = plan.batch
         if q.dtype != self.dtype or out.dtype != self.dtype:
             raise TypeError(f"q and out must be {self.dtype}")
@@ -149,6 +154,9 @@ class PagedDecodeAttention:
         args.launch_index = self._launches & 0xFFFFFFFF
         args.pdl = 1 if self.pdl else 0
         args.kv_dtype = 1 if self.dtype == torch.float16 else 0
+        args.defer_merge = 1 if defer_merge else 0
+        args.prev_out = prev_out.data_ptr() if prev_out is not None else None
+        args.prev_lse = prev_lse.data_ptr() if prev_lse is not None else None
         self._launches += 1
         with torch.cuda.device(self.device):
             _lib.check(self.lib.asv_decode_attention(C.byref(self.shape), C.byref(args),

@@ -68,6 +68,11 @@ struct AttnLaunch {
     int sms;
     float sm_scale;
     unsigned long long* warp_ts;  // optional per-warp %globaltimer (start, end)
+    bool defer_merge;             // leave this launch's partials to the next launch (no merge kernel)
+    const float* prev_part_o;     // previous launch's deferred partials (other parity), or null
+    const float* prev_part_ml;
+    void* prev_out;               // non-null: merge the previous launch's split rows into it
+    float* prev_lse;
 };
 
 int attn_warps_per_cta(int group, bool f16 = false);

@@ -305,7 +305,8 @@ size_t asv_attn_workspace_bytes(const asv_attn_shape* shape, int32_t max_batch, 
     if (check_shape(shape) != ASV_OK) return 0;
     (void)max_batch;
     const int64_t per = static_cast<int64_t>(shape->num_q_heads) * (128 * 4 + 8);
-    return static_cast<size_t>(kHeadBytes + per * std::max<int64_t>(1, max_total_splits));
+    // two partial areas (launch_index parity): a launch may leave its partials for the next one
+    return static_cast<size_t>(kHeadBytes + 2 * per * std::max<int64_t>(1, max_total_splits));
 }
 
 int asv_attn_workspace_init(void* workspace, size_t bytes, void* stream) {
@@ -340,7 +341,9 @@ int asv_decode_attention(const asv_attn_shape* shape, const asv_attn_args* a, vo
     if (a->k_new != nullptr && pl.append_missing > 0)
         return fail(ASV_ERR_INVALID, "KV append requested but " + std::to_string(pl.append_missing) +
                                          " request(s) own no page for position seq_len");
-    const int64_t need = kHeadBytes + static_cast<int64_t>(pl.total_splits) * n_q * (128 * 4 + 8);
+    const bool two_areas = a->defer_merge != 0 || a->prev_out != nullptr;
+    const int64_t area = static_cast<int64_t>(pl.total_splits) * n_q * (128 * 4 + 8);
+    const int64_t need = kHeadBytes + (two_areas ? 2 : 1) * area;
     if (a->workspace == nullptr || static_cast<int64_t>(a->workspace_bytes) < need)
         return fail(ASV_ERR_INVALID, "workspace too small for plan: need " + std::to_string(need));
     if (a->kv_dtype != ASV_KV_BF16 && a->kv_dtype != ASV_KV_F16)
@@ -393,9 +396,23 @@ int asv_decode_attention(const asv_attn_shape* shape, const asv_attn_args* a, vo
     L.lse = a->lse;
     char* ws = static_cast<char*>(a->workspace);
     L.work = reinterpret_cast<uint32_t*>(ws) + 4 * (a->launch_index & 1u);
-    // partial outputs first (16-byte aligned float4 rows), then the (m, l) pairs
-    L.part_o = reinterpret_cast<float*>(ws + kHeadBytes);
-    L.part_ml = reinterpret_cast<float*>(ws + kHeadBytes + static_cast<int64_t>(pl.total_splits) * n_q * 512);
+    // partial outputs first (16-byte aligned float4 rows), then the (m, l) pairs; with deferred merges
+    // the launch_index parity picks one of two areas (the previous launch's partials are the other)
+    const auto area_at = [&](uint32_t parity, float** po, float** pml) {
+        char* base = ws + kHeadBytes + (two_areas ? static_cast<int64_t>(parity) * area : 0);
+        *po = reinterpret_cast<float*>(base);
+        *pml = reinterpret_cast<float*>(base + static_cast<int64_t>(pl.total_splits) * n_q * 512);
+    };
+    area_at(a->launch_index & 1u, &L.part_o, &L.part_ml);
+    L.defer_merge = a->defer_merge != 0;
+    if (a->prev_out != nullptr) {
+        float *po = nullptr, *pml = nullptr;
+        area_at((a->launch_index - 1u) & 1u, &po, &pml);
+        L.prev_part_o = po;
+        L.prev_part_ml = pml;
+        L.prev_out = a->prev_out;
+        L.prev_lse = a->prev_lse;
+    }
     L.sm_scale = a->sm_scale;
     L.warp_ts = reinterpret_cast<unsigned long long*>(a->warp_timestamps);
     cudaError_t e = attn_launch(L, static_cast<cudaStream_t>(stream));

@@ -77,6 +77,13 @@ struct Params {
     const int32_t* merge_reqs;  // requests split more than once
     int32_t merge_rows;         // merge_reqs count * n_q
     float scale_log2;
+    // deferred merge of the PREVIOUS launch (same plan, other workspace parity): its split rows are
+    // merged by this launch's warps right after the dependency wait (prev_rows = 0: none)
+    const float* prev_part_o;
+    const float2* prev_part_ml;
+    uint16_t* prev_out;
+    float* prev_lse;
+    int32_t prev_rows;
     int32_t l2_prefetch;          // pages beyond the TMA ring prefetched into L2 (0: off)
     unsigned long long* warp_ts;  // optional [total_warps][2] %globaltimer start/end (bubble probe, I1)
 };
@@ -284,6 +291,63 @@ __device__ __forceinline__ void write_final_row(const Params& p, int r, int qh, 
     *reinterpret_cast<uint2*>(p.out + (static_cast<int64_t>(r) * p.n_q + qh) * kD + lane * 4) = w;
     if (p.lse != nullptr && lane == 0) {
         p.lse[static_cast<int64_t>(r) * p.n_q + qh] = l > 0.f ? (m + __log2f(l)) / kLog2e : -INFINITY;
+    }
+}
+
+// Deferred split merge, one warp per (request, query head) row of the previous launch: lane l owns
+// dims 4l..4l+3; online (max, sum) over 8-split batches of coalesced 512-byte loads.
+template <bool F16>
+__device__ __forceinline__ void merge_prev_row(const Params& p, int row, int lane) {
+    const int r = __ldg(p.merge_reqs + row / p.n_q);
+    const int qh = row % p.n_q;
+    const int s0 = __ldg(p.split_base + r);
+    const int ns = __ldg(p.split_base + r + 1) - s0;
+    const float2* ml = p.prev_part_ml + static_cast<int64_t>(s0) * p.n_q + qh;
+    const float4* po = reinterpret_cast<const float4*>(p.prev_part_o + (static_cast<int64_t>(s0) * p.n_q + qh) * kD) + lane;
+    const int64_t ostride = static_cast<int64_t>(p.n_q) * (kD / 4);
+    float M = -INFINITY, L = 0.f;
+    float o[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int base = 0; base < ns; base += 8) {
+        float4 v[8];
+        float2 w[8];
+        float bm = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (base + j < ns) {
+                v[j] = __ldcg(po + (base + j) * ostride);
+                w[j] = __ldcg(ml + static_cast<int64_t>(base + j) * p.n_q);
+            } else {
+                v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+                w[j] = make_float2(-INFINITY, 0.f);
+            }
+            bm = fmaxf(bm, w[j].x);
+        }
+        const float mn = fmaxf(M, bm);
+        if (mn == -INFINITY) continue;
+        const float a = exp2f(M - mn);
+        L *= a;
+        o[0] *= a;
+        o[1] *= a;
+        o[2] *= a;
+        o[3] *= a;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const float e = (w[j].x == -INFINITY) ? 0.f : exp2f(w[j].x - mn);
+            L += e * w[j].y;
+            o[0] += e * v[j].x;
+            o[1] += e * v[j].y;
+            o[2] += e * v[j].z;
+            o[3] += e * v[j].w;
+        }
+        M = mn;
+    }
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    uint2 wv;
+    wv.x = pack2<F16>(o[0] * inv, o[1] * inv);
+    wv.y = pack2<F16>(o[2] * inv, o[3] * inv);
+    *reinterpret_cast<uint2*>(p.prev_out + (static_cast<int64_t>(r) * p.n_q + qh) * kD + lane * 4) = wv;
+    if (p.prev_lse != nullptr && lane == 0) {
+        p.prev_lse[static_cast<int64_t>(r) * p.n_q + qh] = L > 0.f ? (M + __log2f(L)) / kLog2e : -INFINITY;
     }
 }
 
@@ -681,6 +745,18 @@ decode_attn_kernel(const Params p) {
     grid_dep_wait();
     grid_dep_launch();
 
+    // the previous launch deferred its split merge: its rows are this launch's first work (its
+    // partials are complete: the dependency wait covered that grid); the KV ring keeps filling
+    if (p.prev_rows > 0) {
+        for (;;) {
+            uint32_t row = 0;
+            if (lane == 0) row = atomicAdd(p.work + 2, 1u);
+            row = bcast(row);
+            if (row >= static_cast<uint32_t>(p.prev_rows)) break;
+            merge_prev_row<F16>(p, static_cast<int>(row), lane);
+        }
+    }
+
     QRegs<GROUP> q, qn;
     Acc<GROUP, F16> acc;
     int consumed = 0;   // pages
@@ -735,6 +811,7 @@ decode_attn_kernel(const Params p) {
         if (done == static_cast<uint32_t>(p.total_warps) - 1u) {
             p.work[0] = 0u;
             p.work[1] = 0u;
+            p.work[2] = 0u;
         }
     }
 }
@@ -1083,6 +1160,11 @@ cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st) {
     p.merge_rows = a.n_merge * a.n_q;
     p.scale_log2 = a.sm_scale * kLog2e;
     p.warp_ts = a.warp_ts;
+    p.prev_part_o = a.prev_part_o;
+    p.prev_part_ml = reinterpret_cast<const float2*>(a.prev_part_ml);
+    p.prev_out = static_cast<uint16_t*>(a.prev_out);
+    p.prev_lse = a.prev_lse;
+    p.prev_rows = a.prev_out != nullptr ? a.n_merge * a.n_q : 0;
     {
         static const int pf = [] {
             const char* e = getenv("ASV_L2_PREFETCH");
@@ -1093,6 +1175,7 @@ cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st) {
     if (p.num_items <= 0) return cudaSuccess;
     cudaError_t e = dispatch(a.group, a.f16, false, nullptr, &p, a.grid, a.pdl, st);
     if (e != cudaSuccess) return e;
+    if (a.defer_merge) return cudaSuccess;  // the next launch merges these partials
     return merge_launch(p, a.merge_reqs, a.n_merge, a.sms, a.pdl, a.f16, st);
 }
 

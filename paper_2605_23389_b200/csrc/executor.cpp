@@ -706,6 +706,7 @@ class GpuExecutor : public prefixsim::DataPlane {
             const int32_t b = pl.batch;
             const int32_t* positions = plan_arena_dev_ + pw + ((pl.total_int32 + 3) & ~3);
             const int32_t* payload = plan_arena_dev_ + pw + plan_words + ((pos_words + 3) & ~int64_t(3));
+            void* prev_layer_out = nullptr;
             for (int l = 0; l < o_.num_layers; ++l) {
                 // RMSNorm, QKV + RoPE -> q_, k_new_, v_new_ (in chain mode layer l > 0's QKV ran in the previous chain)
                 if (o_.full_step && (!chain_ || l == 0)) layer_front(l, b, positions);
@@ -716,6 +717,13 @@ class GpuExecutor : public prefixsim::DataPlane {
                     args.v_new = lp + q_words + kv_words;
                     args.out = static_cast<char*>(out_) + static_cast<int64_t>(l) * b_rows * o_.num_q_heads * 256;
                 }
+                // attention-only steps: layer l's split merge runs inside layer l+1's launch (one grid
+                // boundary per layer); the last layer keeps its merge kernel.  The full step's O GEMM
+                // needs the merged rows at once, so it merges per layer.
+                const bool defer = defer_merge_ && !o_.full_step && pl.n_merge > 0;
+                args.defer_merge = defer && l + 1 < o_.num_layers ? 1 : 0;
+                args.prev_out = defer && l > 0 ? prev_layer_out : nullptr;
+                prev_layer_out = args.out;
                 args.layer = l;
                 args.launch_index = launch0 + static_cast<uint32_t>(l);
                 args.warp_timestamps = probe ? ts_dev_ + static_cast<int64_t>(l) * workers_ * 2 : nullptr;
@@ -752,8 +760,9 @@ class GpuExecutor : public prefixsim::DataPlane {
             stats_.tokens_timed += static_cast<int64_t>(running.size());
             stats_.attn_launches += o_.num_layers;
             // attention (+ merge) per layer, the plan upload, and the e2e result read-back
-            stats_.kernel_launches_timed += o_.num_layers * (plan.n_merge > 0 ? 2 : 1) + 1 + (result_bytes > 0 ? 1 : 0) +
-                                            (probe ? 1 : 0);
+            const bool deferred = defer_merge_ && !o_.full_step && plan.n_merge > 0;
+            const int64_t merges = plan.n_merge > 0 ? (deferred ? 1 : o_.num_layers) : 0;
+            stats_.kernel_launches_timed += o_.num_layers + merges + 1 + (result_bytes > 0 ? 1 : 0) + (probe ? 1 : 0);
             if (o_.full_step) {  // per layer: 2 RMSNorm + 4 linear launches per 256-row chunk
                 const int64_t chunks = (static_cast<int64_t>(running.size()) + 255) / 256;
                 // RMSNorm launches: 2 per layer unfused; fused, only layer 0's first one remains
@@ -1740,6 +1749,7 @@ class GpuExecutor : public prefixsim::DataPlane {
     int32_t ss_parts_ = 0, ss_ld_ = 0;
     bool fuse_norm_ = false;
     bool chain_ = false;                          // full step: one persistent GEMM chain per layer
+    bool defer_merge_ = std::getenv("ASV_DEFER_MERGE") == nullptr || std::atoi(std::getenv("ASV_DEFER_MERGE")) != 0;
     asv_linear_chain_ws* chain_ws_ = nullptr;
     int32_t hidden_ = 0, inter_ = 0;
     int64_t max_rows_full_ = 0, weights_bytes_per_layer_ = 0;

@@ -271,3 +271,39 @@ def test_mha_13b_shape_last_layer(oracle):
     """Llama-2-13B MHA shape (40 heads, 40 layers per page: 12.5 MiB pages), the last layer's slice
     (a small batch: the test pool is built in host memory at 12.5 MiB per page)."""
     _run_case(oracle, 40, 40, 40, 39, [1, 200, 513, 700], seed=131)
+
+
+@pytest.mark.parametrize("n_q,n_kv,seq", [(32, 32, [700, 33, 2048, 15, 4100]), (40, 8, [9000, 64, 3000, 1]),
+                                          (32, 32, [20000, 7])])
+def test_deferred_merge_chain_matches_oracle(oracle, n_q, n_kv, seq):
+    """include/asv.h defer_merge / prev_out: layer l's split rows are merged by layer l+1's launch (its
+    warps take them as first work); the last layer merges its own.  Every layer's output (and lse)
+    matches the oracle, as with one merge kernel per layer."""
+    from paper_2605_23389_b200 import PagedDecodeAttention
+
+    L = 4
+    dev = torch.device("cuda", 0)
+    att = PagedDecodeAttention(n_q, n_kv, L, device=0)
+    pages = sum((s + 16) // 16 for s in seq) + 3
+    pool = U.random_bf16(191, pages * att.page_bytes // 2).view(np.uint8).copy()
+    indptr, indices = U.make_batch(seq, U.usable_pages(n_kv, pages), 192)
+    pool_d = torch.from_numpy(pool).to(dev)
+    plan = att.plan(seq, indptr, indices)
+    assert plan.desc.n_merge > 0  # split requests exist: the deferral is exercised
+    outs, lses, qs = [], [], []
+    for layer in range(L):
+        q = U.random_bf16(200 + layer, len(seq) * n_q * 128).reshape(len(seq), n_q, 128)
+        qs.append(q)
+        out = torch.full((len(seq), n_q, 128), float("nan"), dtype=torch.bfloat16, device=dev)
+        lse = torch.full((len(seq), n_q), float("nan"), dtype=torch.float32, device=dev)
+        att.run(torch.from_numpy(q.view(np.int16)).to(dev).view(torch.bfloat16), pool_d, layer, plan, out, lse,
+                defer_merge=layer + 1 < L, prev_out=outs[-1] if outs else None, prev_lse=lses[-1] if lses else None)
+        outs.append(out)
+        lses.append(lse)
+    torch.cuda.synchronize()
+    for layer in range(L):
+        ref, ref_lse = oracle.attention(n_q, n_kv, L, layer, qs[layer], pool, seq, indptr, indices, att.sm_scale)
+        got = outs[layer].float().cpu().numpy()
+        assert np.isfinite(got).all(), f"layer {layer}: rows never written"
+        assert (np.abs(got - ref) <= ATOL + RTOL * np.abs(ref)).all(), f"layer {layer}"
+        assert np.abs(lses[layer].cpu().numpy() - ref_lse).max() <= LSE_ATOL, f"layer {layer} lse"
