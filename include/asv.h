@@ -285,6 +285,12 @@ int asv_linear_chain(const asv_linear_args* phases, int32_t n, asv_linear_chain_
  * launches on `ws`; with `out` (capacity `cap` words) copies the last launch's [grid][4][6] stamps
  * (decode_chain.cu kTraceSlots) and sets *n.  Synchronous. */
 int asv_linear_chain_ws_trace(asv_linear_chain_ws* ws, int32_t enable, uint64_t* out, int64_t cap, int64_t* n);
+/* Measurement only: per-CTA %globaltimer timeline of asv_linear launches (decode_gemm.cu kTrSlots:
+ * entry, dependency satisfied, last weight load issued, first stage landed, accumulator complete,
+ * cluster reduce entered, exit, SM id).  enable=1 arms the probe for the next 64 launches (grid <= 512);
+ * `out` (capacity `cap` words) receives [launches][512][8] stamps of the armed launches and *n the word
+ * count; enable=0 with out=NULL frees the probe.  Synchronous (device-wide). */
+int asv_linear_trace(int32_t enable, uint64_t* out, int64_t cap, int64_t* n);
 /* out[b][:] = h[b][:] * rsqrt(mean(h[b]^2) + eps) * gamma; rows [batch, rows_out) of out zeroed */
 int asv_rmsnorm(const void* h, const void* gamma, void* out, int32_t dim, int32_t batch, int32_t rows_out,
                 float eps, int32_t pdl, void* stream);

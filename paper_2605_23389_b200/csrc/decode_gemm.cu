@@ -55,7 +55,19 @@ struct LinearParams {
     float ss_inv_dim, ss_eps;
     // next linear's first ring stages -> L2 (0 tiles: off)
     int32_t next_tiles, next_splits, next_kb_per_split, next_kbs, next_pre;
+    unsigned long long* trace;       // optional [grid][kTrSlots] %globaltimer stamps (asv_linear_trace)
 };
+
+// timeline probe (asv_linear_trace, measurement only): per CTA of a launch
+//   0 entry  1 producer: activations' dependency satisfied  2 producer: last weight load issued
+//   3 MMA: first stage landed  4 accumulator complete  5 cluster reduce entered  6 exit  7 SM id
+constexpr int kTrSlots = 8, kTrLaunches = 64, kTrCtas = 512;
+__device__ __forceinline__ void trace_stamp(const LinearParams& p, int slot) {
+    if (p.trace == nullptr) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[static_cast<int64_t>(blockIdx.x) * kTrSlots + slot] = t;
+}
 
 using namespace tc;
 
@@ -76,6 +88,12 @@ __global__ void __launch_bounds__(128, 2)
     float* rs = reinterpret_cast<float*>(tmem_slot + 4);  // fused RMSNorm: 1/rms per batch column of this CTA
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0 && p.trace != nullptr) {
+        trace_stamp(p, 0);
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        p.trace[static_cast<int64_t>(blockIdx.x) * kTrSlots + 7] = smid;
+    }
     const int tile = blockIdx.x / p.splits, split = blockIdx.x % p.splits;
     const int kb0 = split * p.kb_per_split;
     const int kb1 = min(kb0 + p.kb_per_split, p.k / kBK);
@@ -118,6 +136,7 @@ __global__ void __launch_bounds__(128, 2)
             tma_load_2d(smem_u32(smem + i * stage_bytes), &tm_w, (kb0 + i) * kBK, tile * kBM, full0 + 8 * i, pw);
         }
         grid_dep_wait();
+        trace_stamp(p, 1);
         for (int i = 0; i < pre; ++i) {
             tma_load_2d(smem_u32(smem + i * stage_bytes) + kABytes, &tm_x, (kb0 + i) * kBK, 0, full0 + 8 * i, px);
         }
@@ -134,6 +153,7 @@ __global__ void __launch_bounds__(128, 2)
                 ph ^= 1;
             }
         }
+        trace_stamp(p, 2);
         // every weight load of this CTA is issued: keep HBM busy through the tail and the next launch's
         // prologue by pulling a share of the next linear's first ring stages into L2
         if (p.next_tiles > 0) {
@@ -152,6 +172,7 @@ __global__ void __launch_bounds__(128, 2)
         uint32_t ph = 0;
         for (int kb = kb0; kb < kb1; ++kb) {
             mbar_wait(full0 + 8 * s, ph);
+            if (kb == kb0) trace_stamp(p, 3);
             tc_fence_after();
             const uint32_t a = smem_u32(smem + s * stage_bytes);
             const uint64_t ad = umma_desc_sw128(a), bd = umma_desc_sw128(a + kABytes);
@@ -191,6 +212,7 @@ __global__ void __launch_bounds__(128, 2)
     // ---- epilogue 1: TMEM -> this CTA's smem as [bn][128] fp32 (the ring is free:
     // every stage was consumed by an MMA that has completed)
     mbar_wait(done, 0);
+    if (threadIdx.x == 0) trace_stamp(p, 4);
     tc_fence_after();
     const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16);
     float* part = reinterpret_cast<float*>(smem);
@@ -215,6 +237,7 @@ __global__ void __launch_bounds__(128, 2)
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     }
     grid_dep_wait();  // outputs / residual / positions may belong to the previous kernel
+    if (threadIdx.x == 0) trace_stamp(p, 5);
     const int per = (p.batch + p.splits - 1) / p.splits;
     const int cb = split * per, ce = min(cb + per, p.batch);
     const int r = threadIdx.x & 63;
@@ -283,9 +306,13 @@ __global__ void __launch_bounds__(128, 2)
         asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
         asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     }
+    if (threadIdx.x == 0) trace_stamp(p, 6);
 }
 
 // ------------------------------------------------------------------ host side
+unsigned long long* g_trace = nullptr;  // [kTrLaunches][kTrCtas][kTrSlots] (asv_linear_trace)
+int g_trace_seq = 0;
+std::mutex g_trace_mu;
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -467,6 +494,11 @@ static int linear_run(const asv_linear_args* a, cudaStream_t st) {
         p.next_pre = next_pf;
     }
     const int grid = tiles * splits;
+    {
+        std::lock_guard<std::mutex> lk(g_trace_mu);
+        if (g_trace != nullptr && grid <= kTrCtas && g_trace_seq < kTrLaunches)
+            p.trace = g_trace + static_cast<int64_t>(g_trace_seq++) * kTrCtas * kTrSlots;
+    }
     cudaError_t e;
     switch (a->epilogue) {
         case ASV_EPI_STORE: e = launch_epi<ASV_EPI_STORE>(tw, tx, tn, p, grid, a->pdl != 0, st); break;
@@ -585,6 +617,33 @@ extern "C" {
 
 int asv_linear(const asv_linear_args* args, void* stream) {
     return asv::linear_run(args, static_cast<cudaStream_t>(stream));
+}
+
+int asv_linear_trace(int32_t enable, uint64_t* out, int64_t cap, int64_t* n) {
+    std::lock_guard<std::mutex> lk(asv::g_trace_mu);
+    const size_t words = static_cast<size_t>(asv::kTrLaunches) * asv::kTrCtas * asv::kTrSlots;
+    if (out != nullptr) {
+        if (asv::g_trace == nullptr) return asv::fail(ASV_ERR_INVALID, "linear_trace: not enabled");
+        const size_t m = static_cast<size_t>(asv::g_trace_seq) * asv::kTrCtas * asv::kTrSlots;
+        if (static_cast<int64_t>(m) > cap) return asv::fail(ASV_ERR_INVALID, "linear_trace: out too small");
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e == cudaSuccess) e = cudaMemcpy(out, asv::g_trace, m * 8, cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) return asv::cuda_fail(e, "linear_trace copy");
+        if (n != nullptr) *n = static_cast<int64_t>(m);
+    }
+    if (enable != 0) {  // (re)arm: the next kTrLaunches launches record
+        if (asv::g_trace == nullptr) {
+            const cudaError_t e = cudaMalloc(&asv::g_trace, words * 8);
+            if (e != cudaSuccess) return asv::cuda_fail(e, "linear_trace");
+        }
+        cudaMemset(asv::g_trace, 0, words * 8);
+        asv::g_trace_seq = 0;
+    } else if (out == nullptr && asv::g_trace != nullptr) {
+        cudaFree(asv::g_trace);
+        asv::g_trace = nullptr;
+        asv::g_trace_seq = 0;
+    }
+    return ASV_OK;
 }
 
 int asv_rmsnorm(const void* h, const void* gamma, void* out, int32_t dim, int32_t batch, int32_t rows_out, float eps,
