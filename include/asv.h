@@ -285,10 +285,14 @@ int asv_linear_chain(const asv_linear_args* phases, int32_t n, asv_linear_chain_
  * launches on `ws`; with `out` (capacity `cap` words) copies the last launch's [grid][4][6] stamps
  * (decode_chain.cu kTraceSlots) and sets *n.  Synchronous. */
 int asv_linear_chain_ws_trace(asv_linear_chain_ws* ws, int32_t enable, uint64_t* out, int64_t cap, int64_t* n);
+/* Measurement only: force every following asv_linear launch to `splits` K splits (cluster size,
+ * 1-8) and `stages` ring stages (2-8; 0 keeps the schedule's); splits = 0 restores the automatic
+ * schedule (decode_gemm.cu linear_plan).  Results are identical up to fp32 summation order. */
+int asv_linear_set_schedule(int32_t splits, int32_t stages);
 /* Measurement only: per-CTA %globaltimer timeline of asv_linear launches (decode_gemm.cu kTrSlots:
  * entry, dependency satisfied, last weight load issued, first stage landed, accumulator complete,
- * cluster reduce entered, exit, SM id).  enable=1 arms the probe for the next 64 launches (grid <= 512);
- * `out` (capacity `cap` words) receives [launches][512][8] stamps of the armed launches and *n the word
+ * cluster reduce entered, exit, SM id).  enable=1 arms the probe for the next 64 launches (grid <= 1024);
+ * `out` (capacity `cap` words) receives [launches][1024][8] stamps of the armed launches and *n the word
  * count; enable=0 with out=NULL frees the probe.  Synchronous (device-wide). */
 int asv_linear_trace(int32_t enable, uint64_t* out, int64_t cap, int64_t* n);
 /* out[b][:] = h[b][:] * rsqrt(mean(h[b]^2) + eps) * gamma; rows [batch, rows_out) of out zeroed */

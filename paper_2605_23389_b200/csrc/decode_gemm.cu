@@ -22,9 +22,12 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <mutex>
+#include <utility>
+#include <vector>
 
 #include "../../include/asv.h"
 #include "asv_internal.h"
@@ -36,6 +39,10 @@ namespace {
 constexpr int kMaxStages = 8;
 constexpr int kSmemBudget = 100 * 1024;  // ring <= ~100 KiB: two CTAs per SM keep more of W in flight
 constexpr int kMaxSplits = 8;            // K splits of a tile = one portable thread-block cluster
+constexpr int kResCols = 64;             // epilogue inputs staged in smem during the main loop: <= 64 columns
+constexpr int kResBytes = kResCols * 128 * 2;  // residual rows of this CTA's columns (bf16), or positions
+// smem the schedule reserves per epilogue for its staged inputs (STORE, RESIDUAL, SILU_MUL, QKV_ROPE)
+constexpr int kStageMargin[4] = {0, 2048, 0, 1024};
 
 struct LinearParams {
     int32_t n_out, k, batch, bn;     // bn: batch padded to a multiple of 16 (MMA N)
@@ -56,12 +63,15 @@ struct LinearParams {
     // next linear's first ring stages -> L2 (0 tiles: off)
     int32_t next_tiles, next_splits, next_kb_per_split, next_kbs, next_pre;
     unsigned long long* trace;       // optional [grid][kTrSlots] %globaltimer stamps (asv_linear_trace)
+    int32_t staged_bytes;            // smem bytes of the staged inputs
+    int32_t stage_in;                // 1: the idle warps stage the epilogue's inputs (residual rows /
+                                     // positions of this CTA's columns) in smem during the main loop
 };
 
 // timeline probe (asv_linear_trace, measurement only): per CTA of a launch
 //   0 entry  1 producer: activations' dependency satisfied  2 producer: last weight load issued
 //   3 MMA: first stage landed  4 accumulator complete  5 cluster reduce entered  6 exit  7 SM id
-constexpr int kTrSlots = 8, kTrLaunches = 64, kTrCtas = 512;
+constexpr int kTrSlots = 8, kTrLaunches = 64, kTrCtas = 1024;
 __device__ __forceinline__ void trace_stamp(const LinearParams& p, int slot) {
     if (p.trace == nullptr) return;
     unsigned long long t;
@@ -86,6 +96,8 @@ __global__ void __launch_bounds__(128, 2)
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kMaxStages + 1);
     float* rs = reinterpret_cast<float*>(tmem_slot + 4);  // fused RMSNorm: 1/rms per batch column of this CTA
+    // epilogue inputs staged during the main loop (stage_in): residual rows [column][128] bf16 or positions
+    uint8_t* staged = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(rs + 256) + 15) & ~uintptr_t(15));
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0 && p.trace != nullptr) {
@@ -188,14 +200,30 @@ __global__ void __launch_bounds__(128, 2)
             }
         }
         umma_commit(done);  // accumulator complete
-    } else if (warp >= 2 && p.ss_in != nullptr) {
-        // fused RMSNorm: the two idle warps turn the producer's partial sums of squares into
-        // 1/rms for this CTA's batch columns while the main loop runs (8 independent partial
-        // sums per column, combined in a fixed order: deterministic)
+    } else if (warp >= 2 && (p.ss_in != nullptr || p.stage_in != 0)) {
         grid_dep_wait();
         const int per_c = (p.batch + p.splits - 1) / p.splits;
         const int c0 = split * per_c, c1 = min(c0 + per_c, p.batch);
-        for (int c = c0 + static_cast<int>(threadIdx.x) - 64; c < c1; c += 64) {
+        if (p.stage_in != 0) {
+            // the epilogue's other inputs (written by the previous kernel) come to smem now, so the
+            // reduce after the last MMA has no global-memory round trip on its critical path
+            const int t = static_cast<int>(threadIdx.x) - 64;
+            if constexpr (EPI == ASV_EPI_RESIDUAL) {
+                uint4* dst = reinterpret_cast<uint4*>(staged);
+                for (int i = t; i < (c1 - c0) * 16; i += 64) {
+                    const int c = i >> 4, j = i & 15;
+                    dst[i] = __ldcg(reinterpret_cast<const uint4*>(p.y + static_cast<int64_t>(c0 + c) * p.y_ld +
+                                                                   tile * kBM) + j);
+                }
+            } else if constexpr (EPI == ASV_EPI_QKV_ROPE) {
+                int32_t* dst = reinterpret_cast<int32_t*>(staged);
+                for (int c = c0 + t; c < c1; c += 64) dst[c - c0] = __ldcg(p.positions + c);
+            }
+        }
+        // fused RMSNorm: the two idle warps turn the producer's partial sums of squares into
+        // 1/rms for this CTA's batch columns while the main loop runs (8 independent partial
+        // sums per column, combined in a fixed order: deterministic)
+        for (int c = c0 + static_cast<int>(threadIdx.x) - 64; p.ss_in != nullptr && c < c1; c += 64) {
             float acc8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
             int i = 0;
             for (; i + 8 <= p.ss_parts; i += 8) {
@@ -245,17 +273,28 @@ __global__ void __launch_bounds__(128, 2)
     for (int c = cb + (threadIdx.x >> 6); c < ce; c += 2) {
         float lo = 0.f, hi = 0.f;
         const uint32_t off_lo = part_s + static_cast<uint32_t>((c * kBM + r) * 4);
-        for (int s2 = 0; s2 < p.splits; ++s2) {
-            uint32_t ra = off_lo, rb = off_lo + 64 * 4;
-            if (p.splits > 1) {
-                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(off_lo), "r"(s2));
-                rb = ra + 64 * 4;
+        if (p.splits > 1) {
+            // every split's partial in flight at once, then summed in split order (deterministic)
+            float x0[kMaxSplits], x1[kMaxSplits];
+#pragma unroll
+            for (int s2 = 0; s2 < kMaxSplits; ++s2) {
+                if (s2 < p.splits) {
+                    uint32_t ra;
+                    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(off_lo), "r"(s2));
+                    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(x0[s2]) : "r"(ra));
+                    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(x1[s2]) : "r"(ra + 64 * 4));
+                }
             }
-            float x0, x1;
-            asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(x0) : "r"(ra) : "memory");
-            asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(x1) : "r"(rb) : "memory");
-            lo += x0;
-            hi += x1;
+#pragma unroll
+            for (int s2 = 0; s2 < kMaxSplits; ++s2) {
+                if (s2 < p.splits) {
+                    lo += x0[s2];
+                    hi += x1[s2];
+                }
+            }
+        } else {
+            lo = part[c * kBM + r];
+            hi = part[c * kBM + r + 64];
         }
         const int b = c;
         if (p.ss_in != nullptr) {
@@ -265,8 +304,14 @@ __global__ void __launch_bounds__(128, 2)
         if constexpr (EPI == ASV_EPI_STORE || EPI == ASV_EPI_RESIDUAL) {
             __nv_bfloat16* dst = p.y + static_cast<int64_t>(b) * p.y_ld + tile * kBM + r;
             if constexpr (EPI == ASV_EPI_RESIDUAL) {
-                lo += __bfloat162float(dst[0]);
-                hi += __bfloat162float(dst[64]);
+                if (p.stage_in != 0) {
+                    const __nv_bfloat16* res = reinterpret_cast<const __nv_bfloat16*>(staged) + (c - cb) * kBM + r;
+                    lo += __bfloat162float(res[0]);
+                    hi += __bfloat162float(res[64]);
+                } else {
+                    lo += __bfloat162float(dst[0]);
+                    hi += __bfloat162float(dst[64]);
+                }
             }
             const __nv_bfloat16 blo = __float2bfloat16(lo), bhi = __float2bfloat16(hi);
             dst[0] = blo;
@@ -292,7 +337,8 @@ __global__ void __launch_bounds__(128, 2)
             if (is_q || is_k) {
                 const float inv_freq = exp2f(-p.rope_log2_theta * (2.f * r / 128.f));  // theta^(-2r/128)
                 float sn, cs;
-                sincosf(static_cast<float>(p.positions[b]) * inv_freq, &sn, &cs);
+                const int32_t pos = p.stage_in != 0 ? reinterpret_cast<const int32_t*>(staged)[c - cb] : p.positions[b];
+                sincosf(static_cast<float>(pos) * inv_freq, &sn, &cs);
                 const float a0 = lo * cs - hi * sn, a1 = hi * cs + lo * sn;
                 lo = a0;
                 hi = a1;
@@ -311,7 +357,7 @@ __global__ void __launch_bounds__(128, 2)
 
 // ------------------------------------------------------------------ host side
 unsigned long long* g_trace = nullptr;  // [kTrLaunches][kTrCtas][kTrSlots] (asv_linear_trace)
-int g_trace_seq = 0;
+int g_trace_seq = 0, g_trace_skipped = 0;
 std::mutex g_trace_mu;
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -344,34 +390,28 @@ bool make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, ui
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int stages_for(int bn) {
-    static const int budget = [] {  // ASV_LINEAR_SMEM_KB: tuning experiments only
-        const char* e = getenv("ASV_LINEAR_SMEM_KB");
-        return e != nullptr ? atoi(e) * 1024 : kSmemBudget;
-    }();
-    const int st = budget / (kABytes + bn * 128);
-    return st < 2 ? 2 : st > kMaxStages ? kMaxStages : st;
-}
-// the epilogue reuses the ring for the [bn][128] fp32 accumulator tile
-int smem_bytes(int bn) {
-    const int ring = stages_for(bn) * (kABytes + bn * 128);
-    return (ring > bn * 512 ? ring : bn * 512) + 1024 + (2 * kMaxStages + 1) * 8 + 16 + 256 * 4;
+// smem of one CTA: the ring (the epilogue reuses it for the [bn][128] fp32 accumulator tile),
+// barriers, TMEM slot, 1/rms scales and the staged epilogue inputs (LinearParams::stage_in)
+int smem_for(int bn, int stages, int staged) {
+    const int ring = stages * (kABytes + bn * 128);
+    return (ring > bn * 512 ? ring : bn * 512) + 1024 + (2 * kMaxStages + 1) * 8 + 16 + 256 * 4 + 16 + staged;
 }
 
 template <int EPI>
+cudaError_t configure_epi() {
+    static cudaError_t once = cudaFuncSetAttribute(linear_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   227 * 1024);  // the sm_100 per-CTA maximum
+    return once;
+}
+template <int EPI>
 cudaError_t launch_epi(const CUtensorMap& tw, const CUtensorMap& tx, const CUtensorMap& tn, const LinearParams& p,
                        int grid, bool pdl, cudaStream_t st) {
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(linear_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             smem_bytes(256));
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    const cudaError_t ce = configure_epi<EPI>();
+    if (ce != cudaSuccess) return ce;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(128);
-    cfg.dynamicSmemBytes = smem_bytes(p.bn);
+    cfg.dynamicSmemBytes = smem_for(p.bn, p.stages, p.stage_in != 0 ? p.staged_bytes : 0);
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     int n = 0;
@@ -394,17 +434,90 @@ cudaError_t launch_epi(const CUtensorMap& tw, const CUtensorMap& tx, const CUten
 
 }  // namespace
 
-// K splits per tile: the largest power of two (<= kMaxSplits = one portable
-// cluster, every split >= 2 K blocks, none empty) with tiles x splits <= 2 CTAs
-// per SM.  Measured on B200 at batch 16 (us, splits 1/2/3/4/8): qkv 25/21/30/26/27,
-// o 24/16/14/12/12, gate_up 34/41/36/40/46, down 55/31/24/21/18 — a second
-// partial wave of short CTAs, or odd cluster sizes, cost more than they save.
-int linear_splits(int n_out, int k, int sms) {
+// Round-1 schedule (ASV_LINEAR_PLAN=0, A/B only): the largest power-of-two split with
+// tiles x splits <= 2 CTAs per SM and a fixed ~100 KiB ring.
+int linear_splits_r1(int n_out, int k, int sms) {
     const int tiles = n_out / kBM, kbs = k / kBK;
     int sp = 1;
     while (sp * 2 <= kMaxSplits && sp * 2 <= kbs / 2 && tiles * sp * 2 <= 2 * sms) sp *= 2;
     const int per = (kbs + sp - 1) / sp;
     return (kbs + per - 1) / per;
+}
+int stages_r1(int bn) {
+    const int st = kSmemBudget / (kABytes + bn * 128);
+    return st < 2 ? 2 : st > kMaxStages ? kMaxStages : st;
+}
+
+// Schedule of one decode linear layer: K splits per tile (= cluster size) and ring stages.
+// A weight-streaming GEMM runs at the rate its bytes in flight allow (Little's law; measured on
+// B200: ~16 MB in flight -> 6.0 TB/s, ~23 MB -> 6.9 TB/s, profiles/linear_trace_r02g.txt), so the
+// schedule maximises the grid's ring bytes in flight, CTAs x min(stages, K blocks per split) x
+// stage bytes (saturating at kFlyCap), over every (splits, stages) that runs in ONE wave: CTAs per
+// SM from shared memory and TMEM columns, and clusters filling at most kClusterFill of the slots
+// (GPC placement: a 3-CTA cluster schedule at 97% of the slots ran as two waves).  Near-ties go to
+// more, smaller CTAs.  Measured against every (splits, stages) of the 7B projections at batch
+// 4/16/64 (tools/linear_schedule_sweep.py, profiles/linear_sched_sweep_r02.jsonl): within 1.6% of
+// the best forced schedule in total, 3.8% faster than round 1's fixed ~100 KiB ring / power-of-two
+// split.  (cudaOccupancyMaxActiveClusters reports ~1 CTA per SM for this kernel whatever its
+// shared memory, so the model is explicit.)  Cached per shape.
+struct LinPlan {
+    int splits, stages;
+};
+LinPlan g_force{0, 0};
+std::mutex g_force_mu;
+constexpr double kFlyCap = 24e6, kFlyTie = 1.03, kClusterFill = 0.9;
+
+template <int EPI>
+LinPlan linear_plan(int n_out, int k, int bn, int sms) {
+    static std::mutex mu;
+    static std::vector<std::pair<uint64_t, LinPlan>> cache;
+    const uint64_t key = (static_cast<uint64_t>(n_out) << 40) ^ (static_cast<uint64_t>(k) << 16) ^
+                         (static_cast<uint64_t>(bn) << 4) ^ static_cast<uint64_t>(sms & 15);
+    std::lock_guard<std::mutex> lk(mu);
+    for (const auto& e : cache)
+        if (e.first == key) return e.second;
+    static const int mode = [] {
+        const char* e = getenv("ASV_LINEAR_PLAN");
+        return e != nullptr ? atoi(e) : 1;
+    }();
+    static const int verbose = [] {
+        const char* e = getenv("ASV_LINEAR_PLAN_LOG");
+        return e != nullptr ? atoi(e) : 0;
+    }();
+    const int tiles = n_out / kBM, kbs = k / kBK, stage_bytes = kABytes + bn * 128;
+    const int ncols = bn <= 32 ? 32 : bn <= 64 ? 64 : bn <= 128 ? 128 : 256;
+    LinPlan best{linear_splits_r1(n_out, k, sms), stages_r1(bn)};
+    if (mode != 0) {
+        double best_fly = -1.0;
+        int best_ctas = 0;
+        for (int sp = 1; sp <= kMaxSplits; ++sp) {
+            const int per = (kbs + sp - 1) / sp;
+            if ((sp > 1 && per < 2) || (kbs + per - 1) / per != sp) continue;
+            for (int st = 2; st <= kMaxStages; ++st) {
+                const int smem = smem_for(bn, st, kStageMargin[EPI]);
+                if (smem > 227 * 1024) break;
+                const int by_smem = (228 * 1024) / (smem + 1024), by_tmem = 512 / ncols;
+                const int slots = (by_smem < by_tmem ? by_smem : by_tmem) * sms;
+                const int ctas = tiles * sp;
+                if (ctas > (sp > 1 ? static_cast<int>(slots * kClusterFill) : slots)) continue;
+                double fly = static_cast<double>(ctas) * (st < per ? st : per) * stage_bytes;
+                if (fly > kFlyCap) fly = kFlyCap;
+                if (verbose > 1)
+                    fprintf(stderr, "  cand splits %d stages %d: %d CTAs, %d slots, %.1f MB in flight\n", sp, st, ctas,
+                            slots, fly / 1e6);
+                if (best_fly < 0.0 || fly > best_fly * kFlyTie || (fly * kFlyTie >= best_fly && ctas > best_ctas)) {
+                    best_fly = fly;
+                    best_ctas = ctas;
+                    best = LinPlan{sp, st};
+                }
+            }
+        }
+    }
+    cache.emplace_back(key, best);
+    if (verbose > 0)
+        fprintf(stderr, "asv_linear plan: n_out %d k %d bn %d epi %d -> splits %d stages %d (%d CTAs)\n", n_out, k, bn,
+                EPI, best.splits, best.stages, tiles * best.splits);
+    return best;
 }
 
 cudaError_t linear_preload() {
@@ -438,7 +551,22 @@ static int linear_run(const asv_linear_args* a, cudaStream_t st) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int tiles = a->n_out / kBM, kbs = a->k / kBK;
-    int splits = linear_splits(a->n_out, a->k, sms);
+    LinPlan plan{1, 2};
+    switch (a->epilogue) {
+        case ASV_EPI_STORE: plan = linear_plan<ASV_EPI_STORE>(a->n_out, a->k, bn, sms); break;
+        case ASV_EPI_RESIDUAL: plan = linear_plan<ASV_EPI_RESIDUAL>(a->n_out, a->k, bn, sms); break;
+        case ASV_EPI_SILU_MUL: plan = linear_plan<ASV_EPI_SILU_MUL>(a->n_out, a->k, bn, sms); break;
+        case ASV_EPI_QKV_ROPE: plan = linear_plan<ASV_EPI_QKV_ROPE>(a->n_out, a->k, bn, sms); break;
+        default: return fail(ASV_ERR_INVALID, "linear: unknown epilogue");
+    }
+    {
+        std::lock_guard<std::mutex> lk(g_force_mu);
+        if (g_force.splits > 0) {  // asv_linear_set_schedule (measurement only)
+            plan.splits = g_force.splits;
+            plan.stages = g_force.stages > 1 ? (g_force.stages > kMaxStages ? kMaxStages : g_force.stages) : plan.stages;
+        }
+    }
+    int splits = plan.splits;
     if (const char* e = getenv("ASV_LINEAR_SPLITS")) {  // tuning experiments only
         const int kbs_ = a->k / kBK, want = atoi(e);
         if (want >= 1 && want <= kMaxSplits && want <= kbs_) {
@@ -456,7 +584,7 @@ static int linear_run(const asv_linear_args* a, cudaStream_t st) {
     p.batch = a->batch;
     p.bn = bn;
     p.splits = splits;
-    p.stages = stages_for(bn);
+    p.stages = plan.stages;
     p.kb_per_split = (kbs + splits - 1) / splits;
     p.epi = a->epilogue;
     p.y = static_cast<__nv_bfloat16*>(a->y);
@@ -474,6 +602,21 @@ static int linear_run(const asv_linear_args* a, cudaStream_t st) {
     p.ss_ld = a->ss_ld;
     p.ss_inv_dim = a->ss_dim > 0 ? 1.f / static_cast<float>(a->ss_dim) : 0.f;
     p.ss_eps = a->ss_eps;
+    {
+        const int per = (a->batch + splits - 1) / splits;
+        if (a->epilogue == ASV_EPI_RESIDUAL) {
+            p.staged_bytes = per * kBM * 2;
+            p.stage_in = per <= kResCols && (reinterpret_cast<uintptr_t>(a->y) & 15) == 0 && a->y_ld % 8 == 0;
+        } else if (a->epilogue == ASV_EPI_QKV_ROPE) {
+            p.staged_bytes = (per * 4 + 15) / 16 * 16;
+            p.stage_in = p.staged_bytes <= kResBytes;
+        }
+        // never at the cost of the second CTA per SM (228 KiB per SM, 1 KiB reserved per CTA)
+        // never beyond the room the schedule left for them (it may cost a co-resident CTA)
+        if (p.staged_bytes > kStageMargin[a->epilogue]) p.stage_in = 0;
+        static const bool no_stage = getenv("ASV_LINEAR_NO_STAGE") != nullptr;  // A/B only
+        if (no_stage) p.stage_in = 0;
+    }
     // the next linear's weights: ASV_LINEAR_NEXT_PF=N prefetches the first N ring stages of every
     // next-launch CTA into L2 from this launch's tail.  Off by default: measured on B200 (r02, C2 full
     // step 565.8 tok/s off vs 559-568 with N = 2..8; 7B GEMM stack -2 to -4%), the boundary is not an
@@ -486,7 +629,7 @@ static int linear_run(const asv_linear_args* a, cudaStream_t st) {
     if (a->next_w != nullptr && next_pf != 0 && a->next_n_out > 0 && a->next_n_out % kBM == 0 && a->next_k > 0 &&
         a->next_k % kBK == 0 && make_map(&tn, a->next_w, static_cast<uint64_t>(a->next_n_out),
                                          static_cast<uint64_t>(a->next_k), kBM)) {
-        const int nsp = linear_splits(a->next_n_out, a->next_k, sms);
+        const int nsp = linear_splits_r1(a->next_n_out, a->next_k, sms);  // (opt-in experiment)
         p.next_tiles = a->next_n_out / kBM;
         p.next_splits = nsp;
         p.next_kbs = a->next_k / kBK;
@@ -496,7 +639,11 @@ static int linear_run(const asv_linear_args* a, cudaStream_t st) {
     const int grid = tiles * splits;
     {
         std::lock_guard<std::mutex> lk(g_trace_mu);
-        if (g_trace != nullptr && grid <= kTrCtas && g_trace_seq < kTrLaunches)
+        static const int skip = [] {  // ASV_LINEAR_TRACE_SKIP=n: record from the n-th armed launch on
+            const char* e = getenv("ASV_LINEAR_TRACE_SKIP");
+            return e != nullptr ? atoi(e) : 0;
+        }();
+        if (g_trace != nullptr && grid <= kTrCtas && g_trace_seq < kTrLaunches && g_trace_skipped++ >= skip)
             p.trace = g_trace + static_cast<int64_t>(g_trace_seq++) * kTrCtas * kTrSlots;
     }
     cudaError_t e;
@@ -619,6 +766,13 @@ int asv_linear(const asv_linear_args* args, void* stream) {
     return asv::linear_run(args, static_cast<cudaStream_t>(stream));
 }
 
+int asv_linear_set_schedule(int32_t splits, int32_t stages) {
+    if (splits < 0 || splits > asv::kMaxSplits || stages < 0) return asv::fail(ASV_ERR_INVALID, "linear_set_schedule");
+    std::lock_guard<std::mutex> lk(asv::g_force_mu);
+    asv::g_force = asv::LinPlan{splits, stages};
+    return ASV_OK;
+}
+
 int asv_linear_trace(int32_t enable, uint64_t* out, int64_t cap, int64_t* n) {
     std::lock_guard<std::mutex> lk(asv::g_trace_mu);
     const size_t words = static_cast<size_t>(asv::kTrLaunches) * asv::kTrCtas * asv::kTrSlots;
@@ -638,6 +792,7 @@ int asv_linear_trace(int32_t enable, uint64_t* out, int64_t cap, int64_t* n) {
         }
         cudaMemset(asv::g_trace, 0, words * 8);
         asv::g_trace_seq = 0;
+        asv::g_trace_skipped = 0;
     } else if (out == nullptr && asv::g_trace != nullptr) {
         cudaFree(asv::g_trace);
         asv::g_trace = nullptr;

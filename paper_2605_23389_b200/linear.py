@@ -46,17 +46,17 @@ def _args(x, w, batch, y=None, epilogue=STORE, positions=None, rope_theta=10000.
 
 def linear_trace(enable: bool | None = None):
     """Measurement only (asv_linear_trace): arm (True) / free (False) the per-CTA timeline of the next
-    64 asv_linear launches, or (None) return the armed launches' stamps as uint64 [launches][512][8]."""
+    64 asv_linear launches, or (None) return the armed launches' stamps as uint64 [launches][1024][8]."""
     import numpy as np
     h = _lib.lib()
     if enable is not None:
         _lib.check(h.asv_linear_trace(1 if enable else 0, None, 0, None))
         return None
-    cap = 64 * 512 * 8
+    cap = 64 * 1024 * 8
     buf = np.zeros(cap, np.uint64)
     n = C.c_int64(0)
     _lib.check(h.asv_linear_trace(0, buf.ctypes.data_as(C.POINTER(C.c_uint64)), cap, C.byref(n)))
-    return buf[:n.value].reshape(-1, 512, 8)
+    return buf[:n.value].reshape(-1, 1024, 8)
 
 
 class ChainWorkspace:
