@@ -478,7 +478,7 @@ def main():
                 "traffic_launch_alg_bytes": tr["alg_bytes"] if tr else None,
                 "traffic_ratio": tr["ratio"] if tr else None,
                 "traffic_source": tr["source"] if tr else None, "peak_source": peak_src,
-                "kernel": "decode_attn_kernel + merge_splits_kernel (split-KV, PDL-chained), per layer",
+                "kernel": "decode_attn_kernel (split-KV, PDL-chained; the previous layer's split merge folded into each launch, the last layer's by merge_splits_kernel), per layer",
                 "alg_bytes_per_launch": att["attn_bytes"] / launches,
                 "avg_launch_us": att["attn_ms"] * 1e3 / launches,
                 "frac_of_8TBps": achieved / 8000.0}

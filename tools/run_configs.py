@@ -34,10 +34,13 @@ def main():
                     help="also run the attention-only step with the per-warp %%globaltimer probe on every launch "
                          "(measured intra-iteration bubble per iteration: p50 / p90 / p99 / max)")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--only", default=None, help="comma-separated config names (default: all)")
     a = ap.parse_args()
     from paper_2605_23389_b200 import engine as E
     results = []
     for name, pol, start, pair in RUNS:
+        if a.only and name not in a.only.split(","):
+            continue
         cfg = E.load_config(os.path.join(ROOT, "configs", name + ".json"))
         at = cfg["b200"]
         row = {"config": name, "policy": pol or "aligned", "start": start, "pair_mode": pair}
