@@ -163,6 +163,10 @@ typedef struct asv_attn_args {
     int32_t defer_merge;
     void* prev_out;
     float* prev_lse;
+    /* Measurement experiment: l2_warm_items > 0 turns the call into an L2 prefetch of the first
+     * l2_warm_pages pages (K and V blocks of the launch's layer) of the first l2_warm_items work items,
+     * in the order the kernel's warps take them — no attention, no merge, no output. */
+    int32_t l2_warm_items, l2_warm_pages;
 } asv_attn_args;
 
 #define ASV_KV_BF16 0

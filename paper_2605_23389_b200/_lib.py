@@ -64,6 +64,8 @@ class AttnArgs(C.Structure):
         ("defer_merge", C.c_int32),
         ("prev_out", C.c_void_p),
         ("prev_lse", C.c_void_p),
+        ("l2_warm_items", C.c_int32),
+        ("l2_warm_pages", C.c_int32),
     ]
 
 

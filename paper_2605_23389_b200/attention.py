@@ -162,3 +162,25 @@ class PagedDecodeAttention:
             _lib.check(self.lib.asv_decode_attention(C.byref(self.shape), C.byref(args),
                                                       C.c_void_p(_stream_ptr(stream))))
         return out
+
+    def l2_warm(self, q: torch.Tensor, kv_pool: torch.Tensor, layer: int, plan: Plan, out: torch.Tensor,
+                items: int, pages: int, stream=None) -> None:
+        """Measurement experiment (asv.h l2_warm_items): prefetch into L2 the first `pages` pages of the
+        first `items` work items a later run(layer, plan) takes first; no attention is computed."""
+        args = _lib.AttnArgs()
+        args.q = q.data_ptr()
+        args.kv_pool = kv_pool.data_ptr()
+        args.pool_pages = kv_pool.numel() * kv_pool.element_size() // self.page_bytes
+        args.layer = int(layer)
+        args.plan_dev = plan.dev.data_ptr()
+        args.plan = C.pointer(plan.desc)
+        args.out = out.data_ptr()
+        args.workspace = self._ws.data_ptr()
+        args.workspace_bytes = self._ws.numel()
+        args.sm_scale = self.sm_scale
+        args.launch_index = self._launches & 0xFFFFFFFF
+        args.kv_dtype = 1 if self.dtype == torch.float16 else 0
+        args.l2_warm_items, args.l2_warm_pages = int(items), int(pages)
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.asv_decode_attention(C.byref(self.shape), C.byref(args),
+                                                      C.c_void_p(_stream_ptr(stream))))

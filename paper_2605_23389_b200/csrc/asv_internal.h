@@ -73,6 +73,8 @@ struct AttnLaunch {
     const float* prev_part_ml;
     void* prev_out;               // non-null: merge the previous launch's split rows into it
     float* prev_lse;
+    int32_t warm_items;           // > 0: L2-warm mode — only prefetch the first warm_pages pages of the
+    int32_t warm_pages;           //       first warm_items work items into L2 (no attention, no merge)
 };
 
 int attn_warps_per_cta(int group, bool f16 = false);

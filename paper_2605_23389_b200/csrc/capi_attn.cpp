@@ -405,6 +405,8 @@ int asv_decode_attention(const asv_attn_shape* shape, const asv_attn_args* a, vo
     };
     area_at(a->launch_index & 1u, &L.part_o, &L.part_ml);
     L.defer_merge = a->defer_merge != 0;
+    L.warm_items = a->l2_warm_items;
+    L.warm_pages = a->l2_warm_pages;
     if (a->prev_out != nullptr) {
         float *po = nullptr, *pml = nullptr;
         area_at((a->launch_index - 1u) & 1u, &po, &pml);

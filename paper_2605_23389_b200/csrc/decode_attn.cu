@@ -1132,6 +1132,27 @@ cudaError_t warp_span_reduce(uint64_t* ts, int32_t workers, int32_t launches, ui
     return cudaGetLastError();
 }
 
+// L2-warm mode (asv_attn_args.l2_warm_items): one thread per (item, page) of the first `items` work
+// items in the order the persistent warps take them (longest first) and the first `pages` pages of
+// each, two 4 KiB bulk L2 prefetches (K, V block).  Lets a side stream pull the first wave of a later
+// attention launch into L2 while other kernels leave HBM idle (measurement experiment).
+__global__ void attn_l2_warm_kernel(const Params p, int items, int pages) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int item = i / pages, j = i - item * pages;
+    if (item >= items || item >= p.num_items) return;
+    const int g = item / p.n_kv, head = item - g * p.n_kv;
+    const int32_t* gd = p.gdesc + static_cast<int64_t>(g) * kDescWords;
+    const int pb = __ldg(gd + 2), pe = __ldg(gd + 3);
+    if (pb + j >= pe) return;
+    int phys = __ldg(gd + 8 + j);
+    if (static_cast<uint32_t>(phys) >= static_cast<uint32_t>(p.usable_pages)) return;
+    phys += (phys / p.group_pages) * p.group_skip;
+    const char* blk = p.pool + static_cast<int64_t>(phys) * p.page_bytes + p.layer_off +
+                      static_cast<int64_t>(head) * kBlockBytes;
+    bulk_prefetch_l2(blk, kBlockBytes);
+    bulk_prefetch_l2(blk + p.v_off, kBlockBytes);
+}
+
 cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st) {
     Params p;
     p.q = static_cast<const uint16_t*>(a.q);
@@ -1173,6 +1194,12 @@ cudaError_t attn_launch(const AttnLaunch& a, cudaStream_t st) {
         p.l2_prefetch = pf;
     }
     if (p.num_items <= 0) return cudaSuccess;
+    if (a.warm_items > 0) {
+        const int pages = a.warm_pages > 0 ? a.warm_pages : 1;
+        const int64_t n = static_cast<int64_t>(a.warm_items < p.num_items ? a.warm_items : p.num_items) * pages;
+        attn_l2_warm_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(p, a.warm_items, pages);
+        return cudaGetLastError();
+    }
     cudaError_t e = dispatch(a.group, a.f16, false, nullptr, &p, a.grid, a.pdl, st);
     if (e != cudaSuccess) return e;
     if (a.defer_merge) return cudaSuccess;  // the next launch merges these partials
