@@ -440,8 +440,13 @@ def main():
         else:
             pkw.update(prefetch_device=dev + 1)
         d.barrier()
+        pair_err = None
         if d.rank % 2 == 0:
-            pr = E.engine_run(pr_cfg, execute_transfers=True, copy_begin=lead, full_step=full_headline, **pkw)
+            try:  # never measured on two physical GPUs before the driver's run: an error is reported, not fatal
+                pr = E.engine_run(pr_cfg, execute_transfers=True, copy_begin=lead, full_step=full_headline, **pkw)
+            except Exception as ex:  # noqa: BLE001
+                pair_err = f"{type(ex).__name__}: {ex}"
+                pr = _lib.EngineStats().as_dict()
         else:  # the prefetch rank's GPU is driven by its decode partner's engine
             pr = _lib.EngineStats().as_dict()
         d.barrier()
@@ -460,6 +465,9 @@ def main():
                          "global trace = N/2 copies of C2 sharded over the pairs; prefetch GPU pulls KV from "
                          "pinned host memory (PCIe) and carries the prefill offloads, admits / evicts are SM "
                          "page moves over NVLink peer pointers into / out of the decode GPU"}
+        n_err = int(d.reduce([1.0 if pair_err else 0.0], "SUM")[0])
+        if n_err:
+            pairs["error"] = {"failed_pairs": n_err, "rank0": pair_err}
 
     # ---- reductions (max window over ranks, summed tokens)
     def rate(st):

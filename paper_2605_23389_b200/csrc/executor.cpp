@@ -124,7 +124,8 @@ class PagePool {
                 if (!block) break;
                 const auto t0 = std::chrono::steady_clock::now();
                 while (!flags_->reached(q.slot, q.v)) {
-                    if (health_) health_();  // a failed copy worker never writes the flag: throw, do not hang
+                    // a failed copy worker never writes the flag, nor does a stalled device: throw, do not hang
+                    if (health_) health_(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
                     std::this_thread::sleep_for(std::chrono::microseconds(20));
                 }
                 wait_ms_ += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -139,10 +140,10 @@ class PagePool {
     int device() const { return device_; }
     double wait_ms() const { return wait_ms_; }
     // called while spinning on a flag; throws when the thread that would write it has failed
-    void set_health_check(std::function<void()> f) { health_ = std::move(f); }
+    void set_health_check(std::function<void(double)> f) { health_ = std::move(f); }
 
  private:
-    std::function<void()> health_;
+    std::function<void(double)> health_;  // (seconds this wait has lasted)
     struct FreePage {
         int32_t page;
         int64_t hazard;
@@ -298,9 +299,10 @@ class GpuExecutor : public prefixsim::DataPlane {
         slice_ = 2 * static_cast<int64_t>(o.num_kv_heads) * 4096;
         flags_.init();
         serial_ = serial_mode_requested();
+        if (stall_limit_s_ <= 0.0) stall_limit_s_ = serial_ ? 3600.0 : 180.0;
         flags_.set_serial(serial_);
-        dec_.set_health_check([this] { check_workers(); });
-        pre_.set_health_check([this] { check_workers(); });
+        dec_.set_health_check([this](double waited) { check_workers(waited, "page quarantine"); });
+        pre_.set_health_check([this](double waited) { check_workers(waited, "page quarantine"); });
         dec_.init(o.decode_device, dec_pages_, page_bytes_, slice_, &flags_);
         if (content_) ASV_CUDA(cudaMemset(dec_.base(), 0xff, static_cast<size_t>(dec_pages_ * page_bytes_)));
         if (pair_ && peer) {
@@ -1571,9 +1573,16 @@ class GpuExecutor : public prefixsim::DataPlane {
         }
     }
 
-    void check_workers() {
+    // every host wait loop calls this: a failed worker, or a wait that made no progress for
+    // stall_limit_s_ (a device that never writes the awaited flag), ends the run with an error instead
+    // of a hang (the destructor then forces every flag so the device drains)
+    void check_workers(double waited_s = 0.0, const char* what = "") {
         if (worker_.failed()) throw CudaError("copy worker: " + worker_.error());
         if (launcher_.failed()) throw CudaError("launch worker: " + launcher_.error());
+        if (waited_s > stall_limit_s_)
+            throw CudaError(std::string("no progress for ") + std::to_string(static_cast<int>(waited_s)) +
+                            " s waiting on " + what + " (flags: iter " + std::to_string(flags_.value(kIter)) +
+                            ", executed " + std::to_string(executed_) + "); ASV_STALL_TIMEOUT_S raises the limit");
     }
 
     // global request id of a shard-local one (request i of the trace -> shard i % count, the orchestrator
@@ -1660,7 +1669,7 @@ class GpuExecutor : public prefixsim::DataPlane {
         if (!flags_.reached(kIter, static_cast<uint32_t>(e + 1))) {
             const auto t0 = clock_now();
             while (!flags_.reached(kIter, static_cast<uint32_t>(e + 1))) {
-                check_workers();  // the iteration may be parked on a copy lane whose worker failed
+                check_workers(ms_since(t0) * 1e-3, "an iteration");  // parked on a failed copy lane, or stalled
                 std::this_thread::sleep_for(std::chrono::microseconds(20));
             }
             host_wait_ms_ += ms_since(t0);
@@ -1724,6 +1733,11 @@ class GpuExecutor : public prefixsim::DataPlane {
     static_assert(kLanes == 8, "open_timer_ initialiser lists one entry per lane");
     SeqFlags flags_;
     bool serial_ = false;                   // profiler-safe ordering (copy_runtime.h serial mode)
+    // host wait without progress that ends the run (s): generous under a profiler (kernel replays)
+    double stall_limit_s_ = [] {
+        const char* e = std::getenv("ASV_STALL_TIMEOUT_S");
+        return e != nullptr ? std::atof(e) : 0.0;
+    }();
     int64_t last_exec_ = -1;                // executed-iteration index of the latest decode_step
     int64_t last_exec_seq_ = -1;            // wall clock: seq whose measured time was reported
     CopyWorker worker_;                     // issues every copy-stream operation
