@@ -561,8 +561,10 @@ static int linear_run(const asv_linear_args* a, cudaStream_t st) {
     }
     {
         std::lock_guard<std::mutex> lk(g_force_mu);
-        if (g_force.splits > 0) {  // asv_linear_set_schedule (measurement only)
-            plan.splits = g_force.splits;
+        if (g_force.splits > 0) {  // asv_linear_set_schedule (measurement only); no empty split
+            const int kbs_ = a->k / kBK, want = g_force.splits < kbs_ ? g_force.splits : kbs_;
+            const int per = (kbs_ + want - 1) / want;
+            plan.splits = (kbs_ + per - 1) / per;
             plan.stages = g_force.stages > 1 ? (g_force.stages > kMaxStages ? kMaxStages : g_force.stages) : plan.stages;
         }
     }

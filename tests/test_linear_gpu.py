@@ -316,3 +316,56 @@ def test_next_weights_l2_prefetch_leaves_results_unchanged():
         torch.cuda.synchronize()
         outs.append((h.clone(), act.clone()))
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("epi", ["store", "residual", "silu", "qkv"])
+def test_every_schedule_matches_torch(epi):
+    """asv_linear_set_schedule forces (K splits = cluster size, ring stages); every schedule the
+    automatic choice may pick (decode_gemm.cu linear_plan: splits 1-8, stages 2-8) must give the
+    same result as torch — including odd cluster sizes, splits that leave a short last split, and the
+    staged-epilogue path (RESIDUAL / QKV with inputs staged in shared memory)."""
+    from paper_2605_23389_b200 import _lib
+    from paper_2605_23389_b200 import linear as L
+    h = _lib.lib()
+    k, batch = 1088, 5  # 17 K blocks: uneven splits for most split counts
+    n_out = 768 if epi == "qkv" else 512
+    x = _x(batch, k, 11)
+    w = _rand((n_out, k), 12, 1 / math.sqrt(k))
+    acc = x[:batch].float() @ w.float().T
+    try:
+        for sp in (1, 2, 3, 5, 6, 8):
+            for st in (2, 5, 8):
+                _lib.check(h.asv_linear_set_schedule(sp, st))
+                if epi == "store":
+                    y = torch.full((batch, n_out), float("nan"), dtype=torch.bfloat16, device="cuda")
+                    L.linear(x, w, batch, y, L.STORE)
+                    ref = acc
+                elif epi == "residual":
+                    y0 = _rand((batch, n_out), 13)
+                    y = y0.clone()
+                    L.linear(x, w, batch, y, L.RESIDUAL)
+                    ref = y0.float() + acc
+                elif epi == "silu":
+                    y = torch.full((batch, n_out // 2), float("nan"), dtype=torch.bfloat16, device="cuda")
+                    L.linear(x, w, batch, y, L.SILU_MUL)
+                    a4 = acc.view(batch, n_out // 128, 2, 64)
+                    ref = (torch.nn.functional.silu(a4[:, :, 0]) * a4[:, :, 1]).reshape(batch, n_out // 2)
+                else:
+                    pos = torch.arange(batch, dtype=torch.int32, device="cuda") * 37 + 3
+                    q = torch.empty(batch, 2, 128, dtype=torch.bfloat16, device="cuda")
+                    kk = torch.empty(batch, 2, 128, dtype=torch.bfloat16, device="cuda")
+                    v = torch.empty(batch, 2, 128, dtype=torch.bfloat16, device="cuda")
+                    L.linear(x, w, batch, None, L.QKV_ROPE, positions=pos, q=q, k_out=kk, v_out=v,
+                             n_q_heads=2, n_kv_heads=2)
+                    heads = acc.view(batch, 6, 128)
+                    inv = 10000.0 ** (-torch.arange(64, device="cuda").float() * 2 / 128)
+                    ang = pos.float()[:, None] * inv[None, :]
+                    cs, sn = torch.cos(ang)[:, None, :], torch.sin(ang)[:, None, :]
+                    lo, hi = heads[:, :4, :64], heads[:, :4, 64:]
+                    rot = torch.cat([lo * cs - hi * sn, hi * cs + lo * sn], dim=-1)
+                    ref = torch.cat([rot, heads[:, 4:]], dim=1)
+                    y = torch.cat([q, kk, v], dim=1)
+                torch.cuda.synchronize()
+                _check(y, ref, f"{epi} splits {sp} stages {st}")
+    finally:
+        _lib.check(h.asv_linear_set_schedule(0, 0))
