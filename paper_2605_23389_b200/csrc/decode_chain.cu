@@ -30,8 +30,11 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include <mutex>
+#include <string>
 
 #include "../../include/asv.h"
 #include "asv_internal.h"
@@ -47,6 +50,12 @@ struct asv_linear_chain_ws {
     uint32_t base[4];  // host: done[] value at the end of the previous launch
     unsigned long long* trace;  // optional timeline of the last launch (asv_linear_chain_ws_trace)
     int32_t trace_grid;         // grid of the last traced launch
+    // cluster split-K chain (default kernel): per-phase CTA counters + exit counter, reset by the
+    // last CTA of every launch (graph-safe); the launch grid that proved co-resident
+    uint32_t* done2;            // [kMaxPhases + 1]
+    int32_t grid2;              // CTAs (clusters x 8); 0 = not yet determined
+    int32_t coop2;              // 1: cooperative launch (co-residency guaranteed by the driver)
+    int32_t logged2;
 };
 
 namespace asv {
@@ -517,6 +526,542 @@ int chain_smem(int bn) {
     return 1024 + chain_stages(bn) * (kABytes + bn * 128) + kChunk * kBM * 4 + 512 * 4 + (2 * kStagesMax + 6) * 8 + 16;
 }
 
+
+// ============================================================================
+// Cluster split-K chain (the default asv_linear_chain kernel).
+//
+// The stream-K kernel above reduces tiles cut between CTAs through global memory, and that
+// reduction sits on every phase boundary while the weight ring keeps the memory system saturated
+// (measured 0.6x the per-GEMM path, profiles/chain_trace_r02g.txt).  This kernel keeps the
+// per-GEMM kernel's reduction — the 8 K splits of a tile are one thread-block cluster and reduce
+// through distributed shared memory — and makes only the phase handoff global:
+//   * persistent grid of G clusters x 8 CTAs (co-resident: cooperative launch), cluster c takes
+//     tiles c, c + G, ... of every phase; CTA rank r streams K blocks [r*per, (r+1)*per) of each;
+//   * warp 4 (TMA producer) streams one ring across tiles and phases: the weights of phase q are
+//     issued as soon as ring slots free up, the activations of phase q only once every CTA has
+//     finished phase q-1 (per-phase counter, release/acquire) — the ring runs ahead across the
+//     boundary by at most its own size;
+//   * warp 5 issues tcgen05.mma into a double-buffered TMEM accumulator (the next tile's MMAs
+//     overlap the previous tile's epilogue);
+//   * warps 0-3 (epilogue): 16 accumulator columns at a time go to a double-buffered smem chunk,
+//     one cluster-scope mbarrier round (remote arrives) publishes it, and every CTA reduces 2 of the
+//     16 columns from all 8 CTAs' chunks (DSMEM) and applies the fused epilogue (same math and
+//     summation order as decode_gemm.cu: results are bit-identical to the per-GEMM launches);
+//   * warps 6-7: fused-RMSNorm scales of a phase from the previous phase's partial sums.
+// ============================================================================
+constexpr int kS2 = 8;            // K splits per tile = cluster size
+constexpr int kChunk2 = 16;       // accumulator columns per cluster reduction round
+constexpr int kRing2Budget = 92 * 1024;
+
+struct Chain2Params {
+    int32_t nphases, batch, bn, stages, nslots, ncols;
+    uint32_t* done;               // [kMaxPhases] CTAs finished per phase, [kMaxPhases] = exit counter
+    unsigned long long* trace;    // optional [grid][kMaxPhases][kTraceSlots]
+    ChainPhase ph[kMaxPhases];
+};
+
+__device__ __forceinline__ void stamp2(const Chain2Params& p, int q, int k) {
+    if (p.trace == nullptr) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[(static_cast<int64_t>(blockIdx.x) * kMaxPhases + q) * kTraceSlots + k] = t;
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t local, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t bar, uint32_t phase) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(phase)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t phase) {
+    uint32_t n = 0;
+    while (!mbar_try_wait_cluster(bar, phase)) {
+        if (++n > (1u << 28)) __trap();
+    }
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// the activations of phase q may be read once every CTA finished phase q-1 (q = 0: the previous kernel)
+__device__ __forceinline__ bool dep_ready2(const Chain2Params& p, int q) {
+    return q == 0 || static_cast<int32_t>(ld_acquire(p.done + (q - 1)) - gridDim.x) >= 0;
+}
+__device__ __forceinline__ void dep_wait2(const Chain2Params& p, int q) {
+    if (q == 0) {
+        grid_dep_wait();
+    } else {
+        wait_count(p.done + (q - 1), gridDim.x);
+    }
+}
+
+// one (batch column, row pair) of a phase's fused epilogue: same math as decode_gemm.cu
+__device__ __forceinline__ void epilogue2(const ChainPhase& P, int tile, int b, int r, float lo, float hi,
+                                          float scale, bool do_ss) {
+    lo *= scale;
+    hi *= scale;
+    if (P.epi == ASV_EPI_STORE || P.epi == ASV_EPI_RESIDUAL) {
+        __nv_bfloat16* dst = P.y + static_cast<int64_t>(b) * P.y_ld + tile * kBM + r;
+        if (P.epi == ASV_EPI_RESIDUAL) {
+            lo += __bfloat162float(__ldcg(dst));
+            hi += __bfloat162float(__ldcg(dst + 64));
+        }
+        const __nv_bfloat16 blo = __float2bfloat16(lo), bhi = __float2bfloat16(hi);
+        dst[0] = blo;
+        dst[64] = bhi;
+        if (do_ss) {  // next linear's fused RMSNorm: sum of squares of the stored row (warp-uniform branch)
+            const float fl = __bfloat162float(blo), fh = __bfloat162float(bhi);
+            float sq = fl * fl + fh * fh;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, off);
+            if ((threadIdx.x & 31) == 0)
+                P.ss_out[static_cast<int64_t>(tile * 2 + ((threadIdx.x >> 5) & 1)) * P.ss_ld + b] = sq;
+        }
+    } else if (P.epi == ASV_EPI_SILU_MUL) {
+        P.y[static_cast<int64_t>(b) * P.y_ld + tile * 64 + r] = __float2bfloat16(silu(lo) * hi);
+    } else {  // ASV_EPI_QKV_ROPE
+        const int head = tile;
+        const bool is_q = head < P.n_q_heads, is_k = !is_q && head < P.n_q_heads + P.n_kv_heads;
+        __nv_bfloat16* dst = is_q ? P.q : is_k ? P.kk : P.v;
+        const int h = is_q ? head : is_k ? head - P.n_q_heads : head - P.n_q_heads - P.n_kv_heads;
+        const int nh = is_q ? P.n_q_heads : P.n_kv_heads;
+        if (is_q || is_k) {
+            const float inv_freq = exp2f(-P.rope_log2_theta * (2.f * r / 128.f));
+            float sn, cs;
+            sincosf(static_cast<float>(__ldcg(P.positions + b)) * inv_freq, &sn, &cs);
+            const float a0 = lo * cs - hi * sn, a1 = hi * cs + lo * sn;
+            lo = a0;
+            hi = a1;
+        }
+        __nv_bfloat16* o = dst + (static_cast<int64_t>(b) * nh + h) * 128;
+        o[r] = __float2bfloat16(lo);
+        o[r + 64] = __float2bfloat16(hi);
+    }
+}
+
+// smem: ring [stages][W 16 KiB | X bn*128 B] | chunk [2][16][128] fp32 | rs [2][256] fp32 |
+//       full[8] empty[8] tfull[2] tempty[2] rsfull[2] cready[2] | tmem base
+__global__ void __launch_bounds__(kThreads, 2)
+    linear_chain2_kernel(const __grid_constant__ ChainMaps maps, const __grid_constant__ Chain2Params p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int stage_bytes = kABytes + p.bn * 128;
+    const int nst = p.stages;
+    float* chunk = reinterpret_cast<float*>(smem + nst * stage_bytes);
+    float* rsbuf = chunk + 2 * kChunk2 * kBM;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(rsbuf + 512);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStagesMax + 8);
+    const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * kStagesMax, tfull0 = empty0 + 8 * kStagesMax,
+                   tempty0 = tfull0 + 16, rsfull0 = tempty0 + 16, cready0 = rsfull0 + 16;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int G = gridDim.x / kS2, cid = blockIdx.x / kS2;
+    const int rank = static_cast<int>(cluster_rank());
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < nst; ++s) {
+            mbar_init(full0 + 8 * s, 1);
+            mbar_init(empty0 + 8 * s, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(tfull0 + 8 * i, 1);
+            mbar_init(tempty0 + 8 * i, 4);    // the four epilogue warps
+            mbar_init(rsfull0 + 8 * i, 2);    // the two scale warps
+            mbar_init(cready0 + 8 * i, kS2);  // one remote arrive per cluster CTA and chunk
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int q = 0; q < p.nphases; ++q) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.w[q])) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.x[q])) : "memory");
+        }
+    }
+    if (warp == kMmaWarp) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(static_cast<uint32_t>(p.nslots * p.ncols))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    cluster_sync_all();  // every CTA's chunk barriers exist before any remote arrive
+    const uint32_t tmem = *tmem_slot;
+    // (no early griddepcontrol.launch_dependents: the next kernel's CTAs must not take SM room
+    // before every CTA of this grid is resident — the phase handoff waits on all of them)
+
+    if (warp == kProducerWarp) {
+        if (lane == 0) {
+            const uint64_t pw = policy_evict_first(), px = policy_evict_last();
+            int s = 0;
+            uint32_t ph = 0;
+            int pend_slot[kStagesMax], pend_kb[kStagesMax];
+            bool prev_grid_done = false;  // the counters belong to this launch only after griddepcontrol.wait
+            for (int q = 0; q < p.nphases; ++q) {
+                const ChainPhase& P = p.ph[q];
+                const int per = (P.kbs + kS2 - 1) / kS2;
+                const int kb0 = rank * per, kb1 = min(kb0 + per, P.kbs);
+                bool dep = false;
+                int npend = 0;
+                if (q > 0 && !prev_grid_done) {  // (a CTA without phase-0 tiles has not waited yet)
+                    grid_dep_wait();
+                    prev_grid_done = true;
+                }
+                auto flush = [&]() {
+                    dep_wait2(p, q);
+                    prev_grid_done = true;
+                    fence_proxy_async();
+                    stamp2(p, q, 0);
+                    for (int i = 0; i < npend; ++i)
+                        tma_load_2d(smem_u32(smem + pend_slot[i] * stage_bytes) + kABytes, &maps.x[q],
+                                    pend_kb[i] * kBK, 0, full0 + 8 * pend_slot[i], px);
+                    npend = 0;
+                    dep = true;
+                };
+                for (int t = cid; t < P.tiles; t += G) {
+                    for (int kb = kb0; kb < kb1; ++kb) {
+                        mbar_wait(empty0 + 8 * s, ph ^ 1);
+                        if (q > 0 && !dep && dep_ready2(p, q)) flush();
+                        const uint32_t a = smem_u32(smem + s * stage_bytes);
+                        mbar_expect_tx(full0 + 8 * s, static_cast<uint32_t>(stage_bytes));
+                        tma_load_2d(a, &maps.w[q], kb * kBK, t * kBM, full0 + 8 * s, pw);
+                        if (dep) {
+                            tma_load_2d(a + kABytes, &maps.x[q], kb * kBK, 0, full0 + 8 * s, px);
+                        } else {
+                            pend_slot[npend] = s;
+                            pend_kb[npend] = kb;
+                            if (++npend == nst) flush();  // the ring holds nothing but weights: wait
+                        }
+                        if (++s == nst) {
+                            s = 0;
+                            ph ^= 1;
+                        }
+                    }
+                }
+                if (!dep && npend > 0) flush();
+            }
+        }
+    } else if (warp == kMmaWarp) {
+        if (lane == 0) {
+            const uint32_t idesc = umma_idesc(static_cast<uint32_t>(p.bn));
+            int s = 0, seg = 0;
+            uint32_t ph = 0;
+            for (int q = 0; q < p.nphases; ++q) {
+                const ChainPhase& P = p.ph[q];
+                const int per = (P.kbs + kS2 - 1) / kS2;
+                const int kb0 = rank * per, kb1 = min(kb0 + per, P.kbs);
+                for (int t = cid; t < P.tiles; t += G, ++seg) {
+                    const int slot = p.nslots == 2 ? (seg & 1) : 0;
+                    const int use = p.nslots == 2 ? (seg >> 1) : seg;
+                    mbar_wait(tempty0 + 8 * slot, static_cast<uint32_t>(use & 1) ^ 1u);
+                    tc_fence_after();
+                    const uint32_t dacc = tmem + static_cast<uint32_t>(slot * p.ncols);
+                    for (int kb = kb0; kb < kb1; ++kb) {
+                        mbar_wait(full0 + 8 * s, ph);
+                        tc_fence_after();
+                        const uint32_t a = smem_u32(smem + s * stage_bytes);
+                        const uint64_t ad = umma_desc_sw128(a), bd = umma_desc_sw128(a + kABytes);
+#pragma unroll
+                        for (int kk = 0; kk < kBK / kUmmaK; ++kk)
+                            umma_f16(dacc, ad + 2 * kk, bd + 2 * kk, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+                        umma_commit(empty0 + 8 * s);
+                        if (++s == nst) {
+                            s = 0;
+                            ph ^= 1;
+                        }
+                    }
+                    umma_commit(tfull0 + 8 * slot);  // (an empty split commits at once: its epilogue reads zeros)
+                }
+            }
+        }
+    } else if (warp >= kHelperWarp0) {
+        const int t = static_cast<int>(threadIdx.x) - kHelperWarp0 * 32;
+        grid_dep_wait();  // the phase counters belong to this launch only after the previous grid is done
+        for (int q = 0; q < p.nphases; ++q) {
+            const ChainPhase& P = p.ph[q];
+            if (P.ss_in == nullptr) continue;
+            if (t == 0) dep_wait2(p, q);
+            helper_bar();
+            for (int b = t; b < p.batch; b += 64) {
+                float acc8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                int i = 0;
+                for (; i + 8 <= P.ss_parts; i += 8) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc8[j] += __ldcg(P.ss_in + static_cast<int64_t>(i + j) * P.ss_ld + b);
+                }
+                for (; i < P.ss_parts; ++i) acc8[0] += __ldcg(P.ss_in + static_cast<int64_t>(i) * P.ss_ld + b);
+                const float ssum =
+                    ((acc8[0] + acc8[1]) + (acc8[2] + acc8[3])) + ((acc8[4] + acc8[5]) + (acc8[6] + acc8[7]));
+                rsbuf[(q & 1) * 256 + b] = rsqrtf(ssum * P.ss_inv_dim + P.ss_eps);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(rsfull0 + 8 * (q & 1));
+        }
+    } else {
+        // ---- epilogue warps 0-3: thread = accumulator row (TMEM lane)
+        grid_dep_wait();  // residual / positions / outputs may belong to the previous kernel
+        const int row = threadIdx.x;
+        const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+        const int ncol = (p.batch + kChunk2 - 1) / kChunk2 * kChunk2;
+        const int r = threadIdx.x & 63, half = threadIdx.x >> 6;
+        uint32_t peer_chunk[kS2];
+#pragma unroll
+        for (int j = 0; j < kS2; ++j) peer_chunk[j] = mapa_u32(smem_u32(chunk), static_cast<uint32_t>(j));
+        uint32_t cc = 0;  // chunk rounds so far (double-buffered chunk, parity of cready)
+        int seg = 0;
+        int rs_uses[2] = {0, 0};
+        for (int q = 0; q < p.nphases; ++q) {
+            const ChainPhase& P = p.ph[q];
+            const int per = (P.kbs + kS2 - 1) / kS2;
+            const bool empty_split = rank * per >= P.kbs;
+            if (q > 0) {
+                // the residual rows / positions this phase reads were written by earlier phases
+                if (threadIdx.x == 0) wait_count(p.done + (q - 1), gridDim.x);
+                epi_bar();
+            }
+            const float* rs = nullptr;
+            if (P.ss_in != nullptr) {
+                mbar_wait(rsfull0 + 8 * (q & 1), static_cast<uint32_t>(rs_uses[q & 1]++ & 1));
+                rs = rsbuf + (q & 1) * 256;
+            }
+            const bool do_ss = P.ss_out != nullptr;
+            for (int t = cid; t < P.tiles; t += G, ++seg) {
+                const int slot = p.nslots == 2 ? (seg & 1) : 0;
+                const int use = p.nslots == 2 ? (seg >> 1) : seg;
+                mbar_wait(tfull0 + 8 * slot, static_cast<uint32_t>(use & 1));
+                tc_fence_after();
+                if (threadIdx.x == 0) stamp2(p, q, t == cid ? 1 : 2);
+                const uint32_t taddr = tmem + static_cast<uint32_t>(slot * p.ncols) + lane_off;
+                for (int c0 = 0; c0 < ncol; c0 += kChunk2, ++cc) {
+                    float v[kChunk2];
+                    if (!empty_split) {
+                        tmem_ld16(taddr + static_cast<uint32_t>(c0), v);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < kChunk2; ++i) v[i] = 0.f;
+                    }
+                    if (c0 + kChunk2 >= ncol) {  // accumulator fully read: the MMA may reuse the slot
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(tempty0 + 8 * slot);
+                    }
+                    float* buf = chunk + (cc & 1) * kChunk2 * kBM;
+#pragma unroll
+                    for (int i = 0; i < kChunk2; ++i) buf[i * kBM + row] = v[i];
+                    epi_bar();
+                    if (threadIdx.x == 0) {
+#pragma unroll
+                        for (int j = 0; j < kS2; ++j) mbar_arrive_remote(mapa_u32(cready0 + 8 * (cc & 1), j));
+                    }
+                    mbar_wait_cluster(cready0 + 8 * (cc & 1), (cc >> 1) & 1);
+                    // this CTA's 2 of the 16 columns, summed over the 8 splits in split order
+                    const int cl = 2 * rank + half, b = c0 + cl;
+                    if (b < p.batch) {
+                        const uint32_t off = static_cast<uint32_t>(((cc & 1) * kChunk2 * kBM + cl * kBM + r) * 4);
+                        float x0[kS2], x1[kS2];
+#pragma unroll
+                        for (int j = 0; j < kS2; ++j) {
+                            asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(x0[j]) : "r"(peer_chunk[j] + off));
+                            asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(x1[j]) : "r"(peer_chunk[j] + off + 256));
+                        }
+                        float lo = 0.f, hi = 0.f;
+#pragma unroll
+                        for (int j = 0; j < kS2; ++j) {
+                            lo += x0[j];
+                            hi += x1[j];
+                        }
+                        epilogue2(P, t, b, r, lo, hi, rs != nullptr ? rs[b] : 1.f, do_ss);
+                    }
+                }
+                if (threadIdx.x == 0 && t + G >= P.tiles) stamp2(p, q, 3);
+            }
+            // this CTA's part of phase q is written: publish it (TMA readers: async proxy)
+            fence_proxy_async();
+            __threadfence();
+            epi_bar();
+            if (threadIdx.x == 0) {
+                red_release_add(p.done + q, 1u);
+                stamp2(p, q, 4);
+            }
+        }
+    }
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    cluster_sync_all();  // no CTA leaves while a peer may still read its chunk buffers
+    grid_dep_launch();   // every CTA of this grid is past its last handoff wait
+    if (warp == kMmaWarp) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "r"(static_cast<uint32_t>(p.nslots * p.ncols))
+                     : "memory");
+    }
+    if (threadIdx.x == 0) {
+        // the last CTA out resets the counters for the next launch (which reads them only after its
+        // griddepcontrol.wait, i.e. after this grid completed): graph replays see the same state
+        __threadfence();
+        const uint32_t prev = atomicAdd(p.done + kMaxPhases, 1u);
+        if (prev == gridDim.x - 1) {
+            for (int q = 0; q < kMaxPhases; ++q) p.done[q] = 0u;
+            p.done[kMaxPhases] = 0u;
+            __threadfence();
+        }
+    }
+}
+
+
+// Co-residency probe for the persistent chain: the same launch shape (cluster of 8, 256 threads,
+// the chain's shared memory and TMEM columns) with every CTA counting itself in and spinning until
+// all are in or ~20 ms pass.  The driver's cooperative limit for this kernel is ~1 CTA per SM
+// (15 clusters), far below what actually co-resides, so the grid is measured instead.
+__global__ void __launch_bounds__(kThreads, 2) chain2_probe_kernel(uint32_t* counter, uint32_t* ok, uint32_t ncols) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    __shared__ uint32_t slot;
+    const int warp = threadIdx.x >> 5;
+    if (warp == kMmaWarp) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&slot)), "r"(ncols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    smem_raw[threadIdx.x] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        atomicAdd(counter, 1u);
+        unsigned long long t0, t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        bool all = false;
+        do {
+            all = ld_acquire(counter) >= gridDim.x;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        } while (!all && t - t0 < 20000000ull);
+        if (!all) atomicExch(ok, 0u);
+    }
+    __syncthreads();
+    if (warp == kMmaWarp) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(slot), "r"(ncols) : "memory");
+    }
+}
+
+int chain2_stages(int bn) {
+    const int st = kRing2Budget / (kABytes + bn * 128);
+    return st < 2 ? 2 : st > kStagesMax ? kStagesMax : st;
+}
+int chain2_smem(int bn) {
+    return 1024 + chain2_stages(bn) * (kABytes + bn * 128) + 2 * kChunk2 * kBM * 4 + 512 * 4 +
+           (2 * kStagesMax + 8) * 8 + 16;
+}
+
+
+// Launch of the cluster split-K chain.  Every CTA must be co-resident (the phase handoff waits on
+// all of them): the grid is the largest cluster count (<= 2 CTAs per SM) that the co-residency probe
+// saw resident together on this device, measured once per workspace with the largest shared memory
+// any batch uses; the spin waits trap (kernel error, not a hang) if that ever fails to hold.
+int chain2_grid(asv_linear_chain_ws* ws, cudaStream_t st) {
+    if (ws->grid2 > 0) return ws->grid2;
+    uint32_t* dev = nullptr;
+    if (cudaMalloc(&dev, 8) != cudaSuccess) return 0;
+    cudaFuncSetAttribute(chain2_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, chain2_smem(16));
+    int grid = 0;
+    for (int g = (2 * ws->sms) / kS2 * kS2; g >= kS2; g -= kS2) {
+        const uint32_t init[2] = {0u, 1u};
+        cudaMemcpy(dev, init, 8, cudaMemcpyHostToDevice);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(g);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = chain2_smem(16);  // the largest: 5 stages at bn 16
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = kS2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        const bool log = getenv("ASV_LINEAR_PLAN_LOG") != nullptr;
+        const cudaError_t le = cudaLaunchKernelEx(&cfg, chain2_probe_kernel, dev, dev + 1, 64u);
+        if (le != cudaSuccess) {
+            if (log) fprintf(stderr, "  chain probe grid %d: launch %s\n", g, cudaGetErrorString(le));
+            cudaGetLastError();
+            continue;
+        }
+        uint32_t res[2] = {0u, 0u};
+        cudaError_t ce = cudaMemcpyAsync(res, dev, 8, cudaMemcpyDeviceToHost, st);
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+        if (log) fprintf(stderr, "  chain probe grid %d: %s counter %u ok %u\n", g, cudaGetErrorString(ce), res[0], res[1]);
+        if (ce != cudaSuccess) break;
+        if (res[1] == 1u && res[0] == static_cast<uint32_t>(g)) {
+            grid = g;
+            break;
+        }
+    }
+    cudaFree(dev);
+    ws->grid2 = grid;
+    if (getenv("ASV_LINEAR_PLAN_LOG") != nullptr)
+        fprintf(stderr, "asv_linear_chain: co-resident grid %d CTAs (%d clusters of %d)\n", grid, grid / kS2, kS2);
+    return grid;
+}
+
+int chain2_launch(const ChainParams& p1, const ChainMaps& maps, bool pdl, asv_linear_chain_ws* ws, cudaStream_t st) {
+    Chain2Params p{};
+    p.nphases = p1.nphases;
+    p.batch = p1.batch;
+    p.bn = p1.bn;
+    p.stages = chain2_stages(p1.bn);
+    p.ncols = p1.ncols;
+    p.nslots = p1.ncols <= 128 ? 2 : 1;
+    p.done = ws->done2;
+    p.trace = ws->trace;
+    for (int q = 0; q < p1.nphases; ++q) p.ph[q] = p1.ph[q];
+    static bool configured = false;
+    if (!configured) {
+        const cudaError_t e = cudaFuncSetAttribute(linear_chain2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   227 * 1024);
+        if (e != cudaSuccess) return cuda_fail(e, "linear_chain: smem attribute");
+        configured = true;
+    }
+    const int grid = chain2_grid(ws, st);
+    if (grid <= 0) return fail(ASV_ERR_CUDA, "linear_chain: no co-resident cluster grid");
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = chain2_smem(p.bn);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = kS2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+    if (pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    ws->trace_grid = grid;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, linear_chain2_kernel, maps, p);
+    if (e != cudaSuccess) return cuda_fail(e, "linear_chain launch");
+    return ASV_OK;
+}
+
 int chain_run(const asv_linear_args* ph, int n, asv_linear_chain_ws* ws, cudaStream_t st) {
     if (ph == nullptr || ws == nullptr || n < 1 || n > kMaxPhases)
         return fail(ASV_ERR_INVALID, "linear_chain: need 1-4 phases and a workspace");
@@ -582,6 +1127,11 @@ int chain_run(const asv_linear_args* ph, int n, asv_linear_chain_ws* ws, cudaStr
         P.ss_eps = a.ss_eps;
         if (P.units < min_units) min_units = P.units;
     }
+    static const bool streamk = [] {  // ASV_CHAIN_KIND=streamk: the stream-K kernel (A/B only)
+        const char* e = getenv("ASV_CHAIN_KIND");
+        return e != nullptr && std::string(e) == "streamk";
+    }();
+    if (!streamk && bn <= 128) return chain2_launch(p, maps, ph[0].pdl != 0, ws, st);
     // every CTA gets a non-empty unit range in every phase (the owner protocol counts on it)
     const int grid = static_cast<int>(2 * ws->sms < min_units ? 2 * ws->sms : min_units);
     for (int q = 0; q < n; ++q) {
@@ -615,7 +1165,9 @@ int chain_run(const asv_linear_args* ph, int n, asv_linear_chain_ws* ws, cudaStr
 
 cudaError_t linear_chain_preload() {
     cudaFuncAttributes fa;
-    return cudaFuncGetAttributes(&fa, linear_chain_kernel);
+    cudaError_t e = cudaFuncGetAttributes(&fa, linear_chain_kernel);
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, linear_chain2_kernel);
+    return e;
 }
 
 }  // namespace asv
@@ -638,6 +1190,8 @@ int asv_linear_chain_ws_create(int32_t device, asv_linear_chain_ws** out) {
     if (e == cudaSuccess) e = cudaMalloc(&ws->arrive, asv::kMaxPhases * asv::kMaxTiles * sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMalloc(&ws->part, part);
     if (e == cudaSuccess) e = cudaMalloc(&ws->pre, part);
+    if (e == cudaSuccess) e = cudaMalloc(&ws->done2, (asv::kMaxPhases + 1) * sizeof(uint32_t));
+    if (e == cudaSuccess) e = cudaMemset(ws->done2, 0, (asv::kMaxPhases + 1) * sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMemset(ws->done, 0, asv::kMaxPhases * sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaMemset(ws->arrive, 0, asv::kMaxPhases * asv::kMaxTiles * sizeof(uint32_t));
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -659,6 +1213,7 @@ void asv_linear_chain_ws_destroy(asv_linear_chain_ws* ws) {
     if (ws->arrive) cudaFree(ws->arrive);
     if (ws->part) cudaFree(ws->part);
     if (ws->pre) cudaFree(ws->pre);
+    if (ws->done2) cudaFree(ws->done2);
     if (ws->trace) cudaFree(ws->trace);
     cudaSetDevice(prev);
     delete ws;

@@ -16,6 +16,11 @@ from paper_2605_23389_b200 import linear as L  # noqa: E402
 
 D, INTER, NQ = 4096, 11008, 32
 NAMES = ["dep_ok", "issued", "seg_first", "seg_last", "contrib", "finished"]
+# cluster split-K chain (default kernel) slots: producer dependency satisfied, first tile accumulated,
+# a later tile accumulated, last tile written, phase signalled
+NAMES2 = ["dep_ok", "tile1_acc", "tileN_acc", "last_done", "signaled", "-"]
+if os.environ.get("ASV_CHAIN_KIND") != "streamk":
+    NAMES = NAMES2
 
 
 def main():
