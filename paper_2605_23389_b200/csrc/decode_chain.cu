@@ -667,9 +667,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     float* chunk = reinterpret_cast<float*>(smem + nst * stage_bytes);
     float* rsbuf = chunk + 2 * kChunk2 * kBM;
     uint64_t* bars = reinterpret_cast<uint64_t*>(rsbuf + 512);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStagesMax + 8);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStagesMax + 12);
     const uint32_t full0 = smem_u32(bars), empty0 = full0 + 8 * kStagesMax, tfull0 = empty0 + 8 * kStagesMax,
-                   tempty0 = tfull0 + 16, rsfull0 = tempty0 + 16, cready0 = rsfull0 + 16;
+                   tempty0 = tfull0 + 32, rsfull0 = tempty0 + 32, cready0 = rsfull0 + 16;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int G = gridDim.x / kS2, cid = blockIdx.x / kS2;
@@ -680,9 +680,11 @@ __global__ void __launch_bounds__(kThreads, 2)
             mbar_init(full0 + 8 * s, 1);
             mbar_init(empty0 + 8 * s, 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < 4; ++i) {
             mbar_init(tfull0 + 8 * i, 1);
             mbar_init(tempty0 + 8 * i, 4);    // the four epilogue warps
+        }
+        for (int i = 0; i < 2; ++i) {
             mbar_init(rsfull0 + 8 * i, 2);    // the two scale warps
             mbar_init(cready0 + 8 * i, kS2);  // one remote arrive per cluster CTA and chunk
         }
@@ -767,8 +769,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                 const int per = (P.kbs + kS2 - 1) / kS2;
                 const int kb0 = rank * per, kb1 = min(kb0 + per, P.kbs);
                 for (int t = cid; t < P.tiles; t += G, ++seg) {
-                    const int slot = p.nslots == 2 ? (seg & 1) : 0;
-                    const int use = p.nslots == 2 ? (seg >> 1) : seg;
+                    const int slot = seg % p.nslots;
+                    const int use = seg / p.nslots;
                     mbar_wait(tempty0 + 8 * slot, static_cast<uint32_t>(use & 1) ^ 1u);
                     tc_fence_after();
                     const uint32_t dacc = tmem + static_cast<uint32_t>(slot * p.ncols);
@@ -842,8 +844,8 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
             const bool do_ss = P.ss_out != nullptr;
             for (int t = cid; t < P.tiles; t += G, ++seg) {
-                const int slot = p.nslots == 2 ? (seg & 1) : 0;
-                const int use = p.nslots == 2 ? (seg >> 1) : seg;
+                const int slot = seg % p.nslots;
+                const int use = seg / p.nslots;
                 mbar_wait(tfull0 + 8 * slot, static_cast<uint32_t>(use & 1));
                 tc_fence_after();
                 if (threadIdx.x == 0) stamp2(p, q, t == cid ? 1 : 2);
@@ -964,7 +966,7 @@ int chain2_stages(int bn) {
 }
 int chain2_smem(int bn) {
     return 1024 + chain2_stages(bn) * (kABytes + bn * 128) + 2 * kChunk2 * kBM * 4 + 512 * 4 +
-           (2 * kStagesMax + 8) * 8 + 16;
+           (2 * kStagesMax + 12) * 8 + 16;
 }
 
 
@@ -1024,7 +1026,18 @@ int chain2_launch(const ChainParams& p1, const ChainMaps& maps, bool pdl, asv_li
     p.bn = p1.bn;
     p.stages = chain2_stages(p1.bn);
     p.ncols = p1.ncols;
-    p.nslots = p1.ncols <= 128 ? 2 : 1;
+    // TMEM accumulator slots: as many as 2 CTAs per SM can hold (<= 4): the MMA runs up to
+    // nslots - 1 tiles ahead of the epilogue
+    {
+        static const int want = [] {
+            const char* e = getenv("ASV_CHAIN_SLOTS");
+            return e != nullptr ? atoi(e) : 4;
+        }();
+        int ns = 256 / p1.ncols;
+        if (ns > want) ns = want;
+        if (ns > 4) ns = 4;
+        p.nslots = ns < 1 ? 1 : ns;
+    }
     p.done = ws->done2;
     p.trace = ws->trace;
     for (int q = 0; q < p1.nphases; ++q) p.ph[q] = p1.ph[q];
