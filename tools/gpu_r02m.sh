@@ -1,6 +1,6 @@
 #!/bin/bash
 # GQA (C4) planner split-size sweep with the deferred merge
-for c in 0 12 16 20 24 28 32; do
+for c in 6 8 10 12; do
   if [ $c = 0 ]; then unset ASV_PLAN_CHUNK; else export ASV_PLAN_CHUNK=$c; fi
   echo "== chunk $c"
   timeout 600 python tools/run_configs.py --only c4_13b_gqa8 --bubble 2>&1 | python -c "
