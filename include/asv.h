@@ -272,12 +272,16 @@ typedef struct asv_linear_args {
  * workspace is needed.  Stream-ordered; no host synchronisation. */
 int asv_linear(const asv_linear_args* args, void* stream);
 
-/* Persistent stream-K CHAIN of up to 4 dependent linear layers in ONE launch (decode_chain.cu):
+/* Persistent CHAIN of up to 4 dependent linear layers in ONE launch (decode_chain.cu; measured
+ * slower than one asv_linear per GEMM, DESIGN §4 — an experiment, opt-in in the engine):
  * phase i+1 may read what phase i writes (x, residual stream, fused-RMSNorm sums) — e.g. per
- * decoder layer O-proj+residual -> gate/up+SiLU -> down+residual -> next layer's QKV+RoPE.  Every
- * phase's (tile, 64-K block) units are split evenly over a persistent grid of 2 CTAs per SM; tiles
- * cut between CTAs are reduced (fixed CTA order: deterministic) by the CTA holding their first K
- * block; the weight stream runs ahead across phase boundaries.  Same per-phase semantics and
+ * decoder layer O-proj+residual -> gate/up+SiLU -> down+residual -> next layer's QKV+RoPE.  Default
+ * kernel (batch <= 128): 8-CTA clusters take whole tiles, the K splits of a tile reduce through
+ * distributed shared memory (results bit-identical to asv_linear), phases hand off through per-phase
+ * counters; otherwise (or ASV_CHAIN_KIND=streamk) every phase's (tile, 64-K block) units are split
+ * evenly over a grid of 2 CTAs per SM and tiles cut between CTAs are reduced (fixed CTA order:
+ * deterministic) by the CTA holding their first K block.  The weight stream runs ahead across phase
+ * boundaries in both.  Same per-phase semantics and
  * weight layouts as asv_linear (all phases share `batch`; `pdl` is taken from phases[0]).
  * The workspace holds the cross-CTA counters and partials of one device; launches that share a
  * workspace must be stream-ordered (one compute stream). */
@@ -285,6 +289,9 @@ typedef struct asv_linear_chain_ws asv_linear_chain_ws;
 int asv_linear_chain_ws_create(int32_t device, asv_linear_chain_ws** out);
 void asv_linear_chain_ws_destroy(asv_linear_chain_ws* ws);
 int asv_linear_chain(const asv_linear_args* phases, int32_t n, asv_linear_chain_ws* ws, void* stream);
+/* (The default chain kernel keeps 8-CTA clusters co-resident; the first launch on a workspace measures
+ * how many are with a probe kernel (synchronous), so it must not be stream-captured.  ASV_CHAIN_KIND=
+ * streamk selects the stream-K kernel.) */
 /* Measurement only: enable (1) / disable (0) a per-CTA, per-phase %globaltimer timeline of the chain
  * launches on `ws`; with `out` (capacity `cap` words) copies the last launch's [grid][4][6] stamps
  * (decode_chain.cu kTraceSlots) and sets *n.  Synchronous. */

@@ -952,6 +952,9 @@ int chain2_smem(int bn) {
 // any batch uses; the spin waits trap (kernel error, not a hang) if that ever fails to hold.
 int chain2_grid(asv_linear_chain_ws* ws, cudaStream_t st) {
     if (ws->grid2 > 0) return ws->grid2;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone)
+        return -1;  // the probe synchronises: run one chain launch before capturing a graph
     uint32_t* dev = nullptr;
     if (cudaMalloc(&dev, 8) != cudaSuccess) return 0;
     cudaFuncSetAttribute(chain2_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, chain2_smem(16));
@@ -1025,7 +1028,10 @@ int chain2_launch(const ChainParams& p1, const ChainMaps& maps, bool pdl, asv_li
         configured = true;
     }
     const int grid = chain2_grid(ws, st);
-    if (grid <= 0) return fail(ASV_ERR_CUDA, "linear_chain: no co-resident cluster grid");
+    if (grid < 0)
+        return fail(ASV_ERR_INVALID, "linear_chain: the first launch on a workspace measures the co-resident grid "
+                                     "and cannot be stream-captured");
+    if (grid == 0) return fail(ASV_ERR_CUDA, "linear_chain: no co-resident cluster grid");
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
