@@ -296,6 +296,11 @@ int asv_linear_chain(const asv_linear_args* phases, int32_t n, asv_linear_chain_
  * launches on `ws`; with `out` (capacity `cap` words) copies the last launch's [grid][4][6] stamps
  * (decode_chain.cu kTraceSlots) and sets *n.  Synchronous. */
 int asv_linear_chain_ws_trace(asv_linear_chain_ws* ws, int32_t enable, uint64_t* out, int64_t cap, int64_t* n);
+/* The schedule asv_linear picks for a shape (host-only, no GPU needed): K splits (= cluster size),
+ * ring stages and the CTA's dynamic shared memory, on a device with `sms` SMs (decode_gemm.cu
+ * linear_plan: bytes in flight maximised within one wave). */
+int asv_linear_schedule(int32_t n_out, int32_t k, int32_t batch, int32_t epilogue, int32_t sms, int32_t* splits,
+                        int32_t* stages, int32_t* smem_bytes);
 /* Measurement only: force every following asv_linear launch to `splits` K splits (cluster size,
  * 1-8) and `stages` ring stages (2-8; 0 keeps the schedule's); splits = 0 restores the automatic
  * schedule (decode_gemm.cu linear_plan).  Results are identical up to fp32 summation order. */

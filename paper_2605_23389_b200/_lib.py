@@ -229,6 +229,8 @@ SIGNATURES = [
     ("asv_linear_chain_ws_trace", C.c_int,
      [C.c_void_p, C.c_int32, C.POINTER(C.c_uint64), C.c_int64, C.POINTER(C.c_int64)]),
     ("asv_linear_set_schedule", C.c_int, [C.c_int32, C.c_int32]),
+    ("asv_linear_schedule", C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32),
+                                      C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     ("asv_linear_trace", C.c_int, [C.c_int32, C.POINTER(C.c_uint64), C.c_int64, C.POINTER(C.c_int64)]),
     ("asv_rmsnorm", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_float,
                               C.c_int32, C.c_void_p]),

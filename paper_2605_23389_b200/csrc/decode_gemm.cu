@@ -768,6 +768,25 @@ int asv_linear(const asv_linear_args* args, void* stream) {
     return asv::linear_run(args, static_cast<cudaStream_t>(stream));
 }
 
+int asv_linear_schedule(int32_t n_out, int32_t k, int32_t batch, int32_t epilogue, int32_t sms, int32_t* splits,
+                        int32_t* stages, int32_t* smem_bytes) {
+    if (n_out <= 0 || n_out % asv::kBM != 0 || k <= 0 || k % asv::kBK != 0 || batch < 1 || batch > 256 || sms < 1)
+        return asv::fail(ASV_ERR_INVALID, "linear_schedule: bad shape");
+    const int bn = (batch + 15) / 16 * 16;
+    asv::LinPlan pl{1, 2};
+    switch (epilogue) {
+        case ASV_EPI_STORE: pl = asv::linear_plan<ASV_EPI_STORE>(n_out, k, bn, sms); break;
+        case ASV_EPI_RESIDUAL: pl = asv::linear_plan<ASV_EPI_RESIDUAL>(n_out, k, bn, sms); break;
+        case ASV_EPI_SILU_MUL: pl = asv::linear_plan<ASV_EPI_SILU_MUL>(n_out, k, bn, sms); break;
+        case ASV_EPI_QKV_ROPE: pl = asv::linear_plan<ASV_EPI_QKV_ROPE>(n_out, k, bn, sms); break;
+        default: return asv::fail(ASV_ERR_INVALID, "linear_schedule: unknown epilogue");
+    }
+    if (splits != nullptr) *splits = pl.splits;
+    if (stages != nullptr) *stages = pl.stages;
+    if (smem_bytes != nullptr) *smem_bytes = asv::smem_for(bn, pl.stages, asv::kStageMargin[epilogue]);
+    return ASV_OK;
+}
+
 int asv_linear_set_schedule(int32_t splits, int32_t stages) {
     if (splits < 0 || splits > asv::kMaxSplits || stages < 0) return asv::fail(ASV_ERR_INVALID, "linear_set_schedule");
     std::lock_guard<std::mutex> lk(asv::g_force_mu);
