@@ -260,11 +260,14 @@ typedef struct asv_linear_args {
     int32_t ss_parts, ss_ld, ss_dim;
     float ss_eps;
     /* Optional: the weights of the NEXT linear on the stream ([next_n_out][next_k], same batch).  With
-     * ASV_LINEAR_NEXT_PF=N set, a CTA that has issued its last weight load prefetches a share of the
-     * first N ring stages the next launch's CTAs will request into L2 (cp.async.bulk.prefetch.tensor).
-     * Off by default (measured no gain on B200).  No effect on results. */
+     * ASV_LINEAR_NEXT_PF=N set, a CTA that has issued its last weight load prefetches into L2
+     * (cp.async.bulk.prefetch.tensor) a share of the N stages each CTA of the next launch streams right
+     * AFTER its ring (which it requests itself at entry), so the next launch's refills after its
+     * dependency wait hit L2.  No effect on results. */
     const void* next_w;
     int32_t next_n_out, next_k;
+    int32_t next_epilogue;   /* the next linear's ASV_EPI_* (its schedule decides which stages come after
+                                its ring) */
 } asv_linear_args;
 
 /* One launch: one CTA per (128-row tile, K split); the K splits of a tile are one

@@ -97,6 +97,7 @@ class LinearArgs(C.Structure):
         ("next_w", C.c_void_p),
         ("next_n_out", C.c_int32),
         ("next_k", C.c_int32),
+        ("next_epilogue", C.c_int32),
     ]
 
 

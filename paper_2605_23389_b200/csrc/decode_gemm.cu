@@ -61,7 +61,7 @@ struct LinearParams {
     int32_t ss_parts, ss_ld;
     float ss_inv_dim, ss_eps;
     // next linear's first ring stages -> L2 (0 tiles: off)
-    int32_t next_tiles, next_splits, next_kb_per_split, next_kbs, next_pre;
+    int32_t next_tiles, next_splits, next_kb_per_split, next_kbs, next_pre, next_first;
     unsigned long long* trace;       // optional [grid][kTrSlots] %globaltimer stamps (asv_linear_trace)
     int32_t staged_bytes;            // smem bytes of the staged inputs
     int32_t stage_in;                // 1: the idle warps stage the epilogue's inputs (residual rows /
@@ -173,8 +173,9 @@ __global__ void __launch_bounds__(128, 2)
             for (int i = blockIdx.x; i < total; i += gridDim.x) {
                 const int j = i / p.next_pre, st = i - j * p.next_pre;
                 const int nt = j / p.next_splits, ns = j - nt * p.next_splits;
-                const int kb = ns * p.next_kb_per_split + st;
-                if (st < p.next_kb_per_split && kb < p.next_kbs) tma_prefetch_l2(&tm_next, kb * kBK, nt * kBM);
+                const int kb = ns * p.next_kb_per_split + p.next_first + st;  // after the next CTA's ring
+                if (p.next_first + st < p.next_kb_per_split && kb < p.next_kbs)
+                    tma_prefetch_l2(&tm_next, kb * kBK, nt * kBM);
             }
         }
     } else if (warp == 1 && lane == 0) {
@@ -631,12 +632,20 @@ static int linear_run(const asv_linear_args* a, cudaStream_t st) {
     if (a->next_w != nullptr && next_pf != 0 && a->next_n_out > 0 && a->next_n_out % kBM == 0 && a->next_k > 0 &&
         a->next_k % kBK == 0 && make_map(&tn, a->next_w, static_cast<uint64_t>(a->next_n_out),
                                          static_cast<uint64_t>(a->next_k), kBM)) {
-        const int nsp = linear_splits_r1(a->next_n_out, a->next_k, sms);  // (opt-in experiment)
+        LinPlan np{1, 2};  // the next launch's schedule: its ring covers its first np.stages K blocks
+        switch (a->next_epilogue) {
+            case ASV_EPI_RESIDUAL: np = linear_plan<ASV_EPI_RESIDUAL>(a->next_n_out, a->next_k, bn, sms); break;
+            case ASV_EPI_SILU_MUL: np = linear_plan<ASV_EPI_SILU_MUL>(a->next_n_out, a->next_k, bn, sms); break;
+            case ASV_EPI_QKV_ROPE: np = linear_plan<ASV_EPI_QKV_ROPE>(a->next_n_out, a->next_k, bn, sms); break;
+            default: np = linear_plan<ASV_EPI_STORE>(a->next_n_out, a->next_k, bn, sms); break;
+        }
+        const int nsp = np.splits;
         p.next_tiles = a->next_n_out / kBM;
         p.next_splits = nsp;
         p.next_kbs = a->next_k / kBK;
         p.next_kb_per_split = (p.next_kbs + nsp - 1) / nsp;
-        p.next_pre = next_pf;
+        p.next_first = next_pf > 0 ? np.stages : 0;  // ASV_LINEAR_NEXT_PF < 0: the ring's own stages (A/B)
+        p.next_pre = next_pf > 0 ? next_pf : -next_pf;
     }
     const int grid = tiles * splits;
     {

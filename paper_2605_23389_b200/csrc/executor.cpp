@@ -1430,12 +1430,13 @@ class GpuExecutor : public prefixsim::DataPlane {
     static void row_chunks(int32_t b, F&& f) {
         for (int32_t r0 = 0; r0 < b; r0 += 256) f(r0, std::min<int32_t>(256, b - r0));
     }
-    // the weights of the linear launched right after this one: its first ring stages are pulled into L2
-    // by this launch's tail (asv.h next_w)
-    static void next_weights(asv_linear_args& a, const void* w, int32_t n_out, int32_t k) {
+    // the weights of the linear launched right after this one (asv.h next_w: with ASV_LINEAR_NEXT_PF the
+    // tail of this launch pulls the stages after the next launch's ring into L2)
+    static void next_weights(asv_linear_args& a, const void* w, int32_t n_out, int32_t k, int32_t epi) {
         a.next_w = w;
         a.next_n_out = n_out;
         a.next_k = k;
+        a.next_epilogue = epi;
     }
     // the next linear takes the raw residual stream h and applies RMSNorm in its epilogue
     void fuse_in(asv_linear_args& a, const float* ss, int32_t r0) const {
@@ -1476,7 +1477,7 @@ class GpuExecutor : public prefixsim::DataPlane {
             if (fuse_norm_) {
                 a.ss_out = ss_b_ + r0;
                 a.ss_ld = ss_ld_;
-                next_weights(a, lw.gate_up, 2 * inter_, hidden_);  // no RMSNorm launch in between
+                next_weights(a, lw.gate_up, 2 * inter_, hidden_, ASV_EPI_SILU_MUL);  // no RMSNorm launch in between
             }
             if (asv_linear(&a, compute_) != ASV_OK) throw CudaError(asv_last_error());
         });
@@ -1488,7 +1489,7 @@ class GpuExecutor : public prefixsim::DataPlane {
             asv_linear_args a = lin(lw.gate_up, 2 * inter_, hidden_, xin + int64_t(r0) * hidden_, n,
                                     act + int64_t(r0) * inter_, inter_, ASV_EPI_SILU_MUL);
             if (fuse_norm_) fuse_in(a, ss_b_, r0);
-            next_weights(a, lw.down, hidden_, inter_);
+            next_weights(a, lw.down, hidden_, inter_, ASV_EPI_RESIDUAL);
             if (asv_linear(&a, compute_) != ASV_OK) throw CudaError(asv_last_error());
         });
         row_chunks(b, [&](int32_t r0, int32_t n) {  // h += act . Wd^T
@@ -1499,7 +1500,7 @@ class GpuExecutor : public prefixsim::DataPlane {
                 a.ss_ld = ss_ld_;
                 if (l + 1 < o_.num_layers)
                     next_weights(a, layers_[static_cast<size_t>(l + 1)].qkv, 128 * (o_.num_q_heads + 2 * o_.num_kv_heads),
-                                 hidden_);
+                                 hidden_, ASV_EPI_QKV_ROPE);
             }
             if (asv_linear(&a, compute_) != ASV_OK) throw CudaError(asv_last_error());
         });

@@ -17,8 +17,8 @@ STORE, RESIDUAL, SILU_MUL, QKV_ROPE = _lib.EPI_STORE, _lib.EPI_RESIDUAL, _lib.EP
 
 
 def _args(x, w, batch, y=None, epilogue=STORE, positions=None, rope_theta=10000.0, q=None, k_out=None, v_out=None,
-          n_q_heads=0, n_kv_heads=0, pdl=False, ss_out=None, ss_in=None, ss_eps=1e-5, next_w=None
-          ) -> _lib.LinearArgs:
+          n_q_heads=0, n_kv_heads=0, pdl=False, ss_out=None, ss_in=None, ss_eps=1e-5, next_w=None,
+          next_epilogue=STORE) -> _lib.LinearArgs:
     if x.dtype != torch.bfloat16 or w.dtype != torch.bfloat16:
         raise TypeError("x and w must be bfloat16")
     n_out, k = w.shape
@@ -41,6 +41,7 @@ def _args(x, w, batch, y=None, epilogue=STORE, positions=None, rope_theta=10000.
         a.ss_in, a.ss_parts, a.ss_ld, a.ss_dim, a.ss_eps = ss_in.data_ptr(), ss_in.shape[0], ss_in.shape[-1], k, ss_eps
     if next_w is not None:  # the next linear's weights: L2 prefetch of its first ring stages
         a.next_w, a.next_n_out, a.next_k = next_w.data_ptr(), next_w.shape[0], next_w.shape[1]
+        a.next_epilogue = next_epilogue
     return a
 
 
@@ -100,15 +101,16 @@ def linear(x: torch.Tensor, w: torch.Tensor, batch: int, y: torch.Tensor | None 
            q: torch.Tensor | None = None, k_out: torch.Tensor | None = None, v_out: torch.Tensor | None = None,
            n_q_heads: int = 0, n_kv_heads: int = 0, pdl: bool = False, stream=None,
            ss_out: torch.Tensor | None = None, ss_in: torch.Tensor | None = None, ss_eps: float = 1e-5,
-           next_w: torch.Tensor | None = None) -> torch.Tensor | None:
+           next_w: torch.Tensor | None = None, next_epilogue: int = STORE) -> torch.Tensor | None:
     """y[:batch] = epilogue(x[:batch] @ w.T) on tcgen05 (x has >= batch rounded up to 16 rows).
 
     Fused RMSNorm: ss_out ([2 * n_out/128][ld] fp32, RESIDUAL only) receives the per-tile sums of
     squares of the updated y rows; a following call with ss_in = that tensor treats x as the raw
     residual stream and scales each output row by rsqrt(mean(x^2) + ss_eps).  next_w: the weights of
-    the next linear on the stream (L2 prefetch of its first ring stages; results unchanged)."""
+    the next linear on the stream and next_epilogue its epilogue (ASV_LINEAR_NEXT_PF: L2 prefetch of the
+    stages after its ring; results unchanged)."""
     a = _args(x, w, batch, y, epilogue, positions, rope_theta, q, k_out, v_out, n_q_heads, n_kv_heads, pdl,
-              ss_out, ss_in, ss_eps, next_w)
+              ss_out, ss_in, ss_eps, next_w, next_epilogue)
     st = (stream or torch.cuda.current_stream(x.device)).cuda_stream
     _lib.check(_lib.lib().asv_linear(C.byref(a), C.c_void_p(st)))
     return y

@@ -55,12 +55,15 @@ def main():
         plans = [phases(l) for l in range(LAYERS)]
         # per-GEMM launches with the next launch's weights prefetched into L2 (asv.h next_w), as the engine
         # runs them (QKV -> O crosses the attention kernel in the engine: no prefetch there)
+        def plans_next_o(l):  # the next layer's O projection follows this layer's QKV in the stack
+            return layers[(l + 1) % LAYERS]["o"]
+
         pf_plans = []
         for l, ph in enumerate(plans):
             ph2 = [dict(p) for p in ph]
-            ph2[0]["next_w"] = ph[1]["w"]
-            ph2[1]["next_w"] = ph[2]["w"]
-            ph2[2]["next_w"] = ph[3]["w"]
+            for i in range(3):
+                ph2[i]["next_w"], ph2[i]["next_epilogue"] = ph[i + 1]["w"], ph[i + 1]["epilogue"]
+            ph2[3]["next_w"], ph2[3]["next_epilogue"] = plans_next_o(l), L.RESIDUAL
             pf_plans.append(ph2)
 
         def stack(mode):
