@@ -124,7 +124,8 @@ class PagedDecodeAttention:
     def run(self, q: torch.Tensor, kv_pool: torch.Tensor, layer: int, plan: Plan,
             out: torch.Tensor, lse: torch.Tensor | None = None, k_new: torch.Tensor | None = None,
             v_new: torch.Tensor | None = None, stream=None, defer_merge: bool = False,
-            prev_out: torch.Tensor | None = None, prev_lse: torch.Tensor | None = None) -> torch.Tensor:
+            prev_out: torch.Tensor | None = None, prev_lse: torch.Tensor | None = None,
+            warp_ts: torch.Tensor | None = None) -> torch.Tensor:
         """out[b][n_h][128] (self.dtype) = softmax(q K^T * sm_scale) V for every request of the plan.
 
         defer_merge / prev_out (include/asv.h): consecutive calls with the same plan may leave the split
@@ -157,6 +158,8 @@ class PagedDecodeAttention:
         args.defer_merge = 1 if defer_merge else 0
         args.prev_out = prev_out.data_ptr() if prev_out is not None else None
         args.prev_lse = prev_lse.data_ptr() if prev_lse is not None else None
+        if warp_ts is not None:  # [num_workers][2] uint64 (int64 tensor): %globaltimer start / end per warp
+            args.warp_timestamps = warp_ts.data_ptr()
         self._launches += 1
         with torch.cuda.device(self.device):
             _lib.check(self.lib.asv_decode_attention(C.byref(self.shape), C.byref(args),
