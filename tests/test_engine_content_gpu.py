@@ -62,16 +62,19 @@ def smoke_l2():
 
 def reference_log(cfg, policy):
     from paper_2605_23389_b200 import engine
-    if os.path.exists(U.REF_SO):
+    if os.path.exists(U.REF_SO) and "num_kv_heads" not in cfg["model"]:
         return U.RefEngine().run_config_jsonl(cfg, policy)[0]
-    return engine.run_config_jsonl(cfg, policy)  # pinned to the reference by test_engine_parity.py
+    # pinned to the reference by test_engine_parity.py (MHA); GQA configs extend the reference's cost
+    # model (num_kv_heads), which the reference itself cannot express
+    return engine.run_config_jsonl(cfg, policy)
 
 
 def run_content(cfg, policy, tmp_path, pair_mode=False, **kw):
     from paper_2605_23389_b200 import engine
     L = cfg["b200"]["num_layers"]
+    nq, nkv = cfg["b200"]["num_q_heads"], cfg["b200"]["num_kv_heads"]
     cap = str(tmp_path / f"cap_{policy}_{int(pair_mode)}.bin")
-    st, log = engine.engine_run(cfg, device=0, num_q_heads=32, num_kv_heads=32, num_layers=L,
+    st, log = engine.engine_run(cfg, device=0, num_q_heads=nq, num_kv_heads=nkv, num_layers=L,
                                 execute_transfers=True, exec_begin=0, exec_end=-1, timed_begin=0, copy_begin=0,
                                 host_pool_bytes=6 << 30, run_ahead=8, policy=policy, pair_mode=pair_mode,
                                 content_check=True, capture_path=cap, capture_every=8, return_log=True, **kw)
@@ -90,12 +93,13 @@ def run_content(cfg, policy, tmp_path, pair_mode=False, **kw):
     full = 0
     for rec in recs:
         if rec["head"] < 0:
-            want = o.content_attention(32, 32, L, rec["ids"], rec["lens"], SCALE)
+            want = o.content_attention(nq, nkv, L, rec["ids"], rec["lens"], SCALE)
             got = rec["out"]
             full += 1
         else:
-            h = rec["head"]
-            want = o.content_attention(32, 32, L, rec["ids"], rec["lens"], SCALE, only_kvh=h)[:, :, h]
+            h = rec["head"]  # a query head; its kv head is h // (nq / nkv)
+            want = o.content_attention(nq, nkv, L, rec["ids"], rec["lens"], SCALE,
+                                       only_kvh=h // (nq // nkv))[:, :, h]
             got = rec["out"]
         assert np.isfinite(got).all(), f"iteration {rec['seq']}: non-finite output (poisoned page read)"
         err = np.abs(got - want) - (TOL_ABS + TOL_REL * np.abs(want))
@@ -161,3 +165,37 @@ def test_aligned_two_device_pair_c1_slice(tmp_path):
     assert st["p2p_bytes"] == _bytes(st, "admit", "evict") > 0
     assert st["h2d_bytes"] == _bytes(st, "batch_prefetch", "stray_prefetch")
     assert st["d2h_bytes"] == _bytes(st, "spill", "flush") > 0
+
+
+def c4_gqa_slice(tmp_path, layers=2):
+    """First 64 requests of the C4 trace (Llama-2-13B shape, GQA-8: 40 query heads over 8 KV heads;
+    outputs x2), two layers, a decode pool tight enough that the aligned policy evicts, spills and
+    flushes (found by a decision-only sweep)."""
+    from paper_2605_23389_b200 import engine
+    cfg = engine.load_config(os.path.join(ROOT, "configs", "c4_13b_gqa8.json"))
+    trace = [json.loads(l) for l in open(cfg["workload"]["path"])][:64]
+    p = tmp_path / "c4_slice.jsonl"
+    with open(p, "w") as f:
+        for r in trace:
+            f.write(json.dumps(dict(r, output_tokens=2 * r["output_tokens"])) + "\n")
+    cfg["workload"]["path"] = str(p)
+    cfg["model"]["num_layers"] = layers
+    cfg["cluster"].update(decode_hbm_blocks=300, prefill_hbm_blocks=600)
+    cfg["constraints"].update(b_max_blocks=350, k_min=8, candidate_buffer_fraction=0.2)
+    cfg["b200"].update(num_layers=layers)
+    return cfg
+
+
+@pytest.mark.parametrize("pair", [False, True])
+def test_aligned_gqa_c4_slice(tmp_path, pair):
+    """GQA through the executed engine (grouped KV heads in the page pool, the mma.sync attention path,
+    KV append per KV head): outputs of every captured iteration vs the fp32 content oracle with the
+    query-head -> KV-head map, page tables in the decision log's order, bytes moved == logical bytes."""
+    cfg = c4_gqa_slice(tmp_path)
+    st, iters, worst = run_content(cfg, "aligned", tmp_path, pair_mode=pair)
+    lb = st["logical_bytes"]
+    assert lb["batch_prefetch"] > 0 and lb["admit"] > 0 and lb["evict"] > 0 and lb["spill"] > 0 and lb["flush"] > 0
+    assert st["h2d_bytes"] == _bytes(st, "batch_prefetch", "stray_prefetch")
+    assert st["d2h_bytes"] == _bytes(st, "spill", "flush")
+    assert st["p2p_bytes"] == (_bytes(st, "admit", "evict") if pair else 0)
+    print(f"GQA C4 slice pair={pair}: {len(iters)} iterations, worst abs err {worst:.3g}, bytes {lb}")
