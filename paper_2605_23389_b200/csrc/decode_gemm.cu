@@ -467,6 +467,21 @@ struct LinPlan {
 LinPlan g_force{0, 0};
 std::mutex g_force_mu;
 constexpr double kFlyCap = 24e6, kFlyTie = 1.03, kClusterFill = 0.9;
+// tuning experiments only: ASV_LINEAR_FLYCAP_MB / ASV_LINEAR_FILL override the two model constants
+double fly_cap() {
+    static const double v = [] {
+        const char* e = getenv("ASV_LINEAR_FLYCAP_MB");
+        return e != nullptr ? atof(e) * 1e6 : kFlyCap;
+    }();
+    return v;
+}
+double cluster_fill() {
+    static const double v = [] {
+        const char* e = getenv("ASV_LINEAR_FILL");
+        return e != nullptr ? atof(e) : kClusterFill;
+    }();
+    return v;
+}
 
 template <int EPI>
 LinPlan linear_plan(int n_out, int k, int bn, int sms) {
@@ -500,9 +515,9 @@ LinPlan linear_plan(int n_out, int k, int bn, int sms) {
                 const int by_smem = (228 * 1024) / (smem + 1024), by_tmem = 512 / ncols;
                 const int slots = (by_smem < by_tmem ? by_smem : by_tmem) * sms;
                 const int ctas = tiles * sp;
-                if (ctas > (sp > 1 ? static_cast<int>(slots * kClusterFill) : slots)) continue;
+                if (ctas > (sp > 1 ? static_cast<int>(slots * cluster_fill()) : slots)) continue;
                 double fly = static_cast<double>(ctas) * (st < per ? st : per) * stage_bytes;
-                if (fly > kFlyCap) fly = kFlyCap;
+                if (fly > fly_cap()) fly = fly_cap();
                 if (verbose > 1)
                     fprintf(stderr, "  cand splits %d stages %d: %d CTAs, %d slots, %.1f MB in flight\n", sp, st, ctas,
                             slots, fly / 1e6);
